@@ -1,0 +1,282 @@
+"""Benchmark of the B200 FMM evaluation path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config B]
+
+A "step" is one FMM evaluation (all payloads of the reference task graph: P2M, M2M,
+M2L, L2L, L2P, P2P + reduce, fields gathered to input order) over the resident
+octree of config B: 10M uniform particles (bench.cpp:29-39, seed 42), height 7,
+Chebyshev order 5, eps 1e-5, group size 250 -- BASELINE.json configs[1].
+
+ours:       value = Mparticles/s from CUDA events on the launching stream (max over
+            ranks), inputs resident in HBM; e2e = the same metric through the C ABI
+            (fmmgpu_run) with pinned host buffers: H2D of the particles, tree build,
+            evaluation, D2H of the four fields, every step.
+reference:  the reference's own CPU implementation (oracle/_ref: the unmodified
+            reference sources, FmmContext + execute with all host threads) on a
+            bounded sample of the workload, rank 0 only.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n, dist, height, order, description)
+    "A": (100_000, "uniform", 4, 5, "uniform cube N=100k, height 4, order 5"),
+    "B": (10_000_000, "uniform", 7, 5, "uniform cube N=10M, height 7, order 5"),
+    "C": (10_000_000, "uniform", 7, 7, "uniform cube N=10M, height 7, order 7"),
+}
+# Bounded CPU sample of config B: same particles per leaf (~38) and order, one level
+# shallower (1/8 of the particles): the reference's per-particle work is the same.
+CPU_SAMPLE = {"B": (1_250_000, "uniform", 6, 5), "C": (1_250_000, "uniform", 6, 7), "A": (100_000, "uniform", 4, 5)}
+
+METRIC = "FMM eval time (s) and Mparticles/s at N=10M, order 5; scaling 1/2/4/8 B200"
+UNIT = "Mparticles/s"
+FP64_PEAK_TFLOPS = 37.15  # own DMMA m8n8k4 microbenchmark, profiles/r01_fp64_peaks.txt
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def reference_sample(cfg_name, workers, warmup, steps):
+    """The reference itself (oracle/_ref) on the bounded sample; returns (Mparticles/s list, info)."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"  # the reference's GEMMs run inside its own workers
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracles import Oracle, RefContext, RefLib
+    n, dist, h, order = CPU_SAMPLE[cfg_name]
+    xyzw = Oracle.generate_particles(n, dist, 42)
+    if RefLib.available():
+        ref = RefContext(xyzw, h, order)
+        for _ in range(warmup):
+            ref.execute(workers=workers)
+        times = [ref.execute(workers=workers) for _ in range(steps)]
+        kind = "reference"
+        setup = ref.setup_seconds()
+    else:  # the CPU restatement (single thread), when the reference was never built here
+        from oracles import OracleOps, OracleTree
+        t = OracleTree(xyzw, h)
+        ops = OracleOps.cached(order)
+        times = []
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            t.evaluate(ops)
+            if i >= warmup:
+                times.append(time.perf_counter() - t0)
+        kind, workers, setup = "port", 1, None
+    rates = [n / t / 1e6 for t in times]
+    info = {"kind": kind, "cores": workers,
+            "sample": f"N={n} {dist}, height {h}, order {order} (config {cfg_name} at the same ~38 particles "
+                      f"per leaf, 1/8 of the particles); timed = the reference's execute() of the whole task "
+                      f"graph ({'%d workers' % workers}), setup ({setup and round(setup, 2)} s) excluded"}
+    return rates, info
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    rates, info = reference_sample(args.config, workers, args.warmup, args.steps)
+    v = float(np.mean(rates))
+    n = CONFIGS[args.config][0]
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": CPU_SAMPLE[args.config][0] / v / 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator, seed 42)", "impl": "reference",
+            "config": {"workload": CONFIGS[args.config][4], "n": n, "sample_n": CPU_SAMPLE[args.config][0]},
+            "cpu_baseline": dict(info, value=v, unit=UNIT),
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import paper_1206_0115_b200 as P
+    n, dist, h, order, desc = CONFIGS[args.config]
+    xyzw = P.generate_particles(n, dist, 42)
+    ctx = P.FmmContext(None, order=order, device=local)
+    ctx.build_tree(xyzw, h, 250)
+    ledger = ctx.ledger()
+    for _ in range(args.warmup):
+        ctx.evaluate()
+    ctx.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier(world)
+    total_ms, kinds, launches = ctx.time_evaluations(args.steps)
+    barrier(world)
+    clk = clocks.stop()
+    ms_step = max_over_ranks(total_ms / args.steps, world)
+    value = world * n / (ms_step / 1e3) / 1e6
+
+    # e2e through the C ABI with pinned host buffers, every step: H2D + tree + eval + D2H
+    import torch
+    pin_in = torch.from_numpy(xyzw).pin_memory()
+    outs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(4)]
+    lib = P.lib()
+    from ctypes import c_void_p
+
+    def e2e_step():
+        rc = lib.fmmgpu_run(ctx.h, c_void_p(pin_in.data_ptr()), n, h, 250, *[c_void_p(o.data_ptr()) for o in outs])
+        ctx._check(rc)
+
+    e2e_step()
+    ksteps = max(1, min(args.steps, 5))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(ksteps):
+        e2e_step()
+    barrier(world)
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / ksteps, world)
+    e2e = {"value": world * n / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": 32 * n, "d2h_bytes_per_step": 32 * n,
+           "ms_per_step": e2e_s * 1e3, "path": "fmmgpu_run (C ABI): pinned H2D, build_tree, evaluate, D2H"}
+
+    # roofline of the dominant kernel family (per-kind device time inside the timed region)
+    per = {k: v / args.steps for k, v in kinds.items()}
+    flops = ledger["flops"]
+    fam = "M2L" if per["M2L"] >= per["P2P"] else "P2P"
+    achieved = flops[fam] / (per[fam] / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{args.config}:{fam}")
+    roof = {"bound": "tensor" if fam == "M2L" else "fp64", "kernel": fam, "achieved": achieved,
+            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+            "flops_per_launch": flops[fam], "ms_per_launch": per[fam],
+            "peak_source": "FP64 DMMA peak measured by tools/microbench/fp64_peaks.cu (not in MEASURED_PEAKS.json)",
+            "flop_convention": "reference ledger (bench.cpp:104-122): M2L 4 l^3 r + r^2 per pair, P2P 15 per "
+                               "directional interaction"}
+    per_op = {}
+    for k in ("P2M", "M2M", "M2L", "L2L", "L2P", "P2P"):
+        if per[k] > 0:
+            per_op[k] = {"ms": per[k], "tflops_ref_convention": flops[k] / (per[k] / 1e3) / 1e12,
+                         "frac_fp64_peak": flops[k] / (per[k] / 1e3) / 1e12 / FP64_PEAK_TFLOPS}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "eval_seconds": ms_step / 1e3,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (reference generator bench.cpp:29-39, seed 42, unit weights)",
+            "config": {"workload": desc, "n": n, "height": h, "order": order, "eps": 10.0 ** -order,
+                       "group_size": 250, "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs (320 MB particles, 262 MB leaf expansions) exceed the 126 MB L2"},
+            "gpu_launches": launches, "e2e": e2e, "roofline": roof, "per_operator": per_op,
+            "tree_ms": per["TREE"], "clocks": clk,
+            "note": "P2P runs on its own stream concurrently with the far-field chain; per-operator times "
+                    "of the far chain include waiting for SMs the P2P kernel holds"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            rates, info = reference_sample(args.config, os.cpu_count() or 1, 1, 2)
+            line["cpu_baseline"] = dict(info, value=float(np.mean(rates)), unit=UNIT)
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,156 @@
+/* fmmgpu.h — C ABI of the B200-native black-box Chebyshev FMM evaluation path.
+ *
+ * Drop-in boundary for the reference ("taskfmm", /root/reference/proj) operator
+ * seam: FmmContext::run_task (bench.cpp:255-344) dispatching P2M / M2M / M2L /
+ * L2L / L2P / P2P payloads over a GroupTree (geometry.hpp:70-112) with an
+ * InteractionPlan (taskflow.hpp:60-70). Plain pointers and sizes only; no C++ or
+ * torch types cross this boundary. One context owns all device memory of one
+ * device and is driven by one host thread.
+ *
+ * Semantics follow the reference:
+ *   - operators ACCUMULATE into arrays zeroed by fmmgpu_reset (FmmContext::reset,
+ *     bench.cpp:240-253); M2L writes only local_own, L2L writes the child's
+ *     local_down, L2L and L2P read own+down (bench.cpp:300-336);
+ *   - fields are returned in INPUT order (FmmContext::gather, bench.cpp:350-365);
+ *   - errors are status codes, one per reference exception class, with the text in
+ *     fmmgpu_last_error (bench.hpp / geometry.cpp:65-69, 86-87, 134; m2l.cpp:60-61).
+ *
+ * Every entry point replaces the reference interface cited beside it.
+ */
+#ifndef FMMGPU_H_
+#define FMMGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fmmgpu_ctx fmmgpu_ctx;
+
+enum fmmgpu_status {
+  FMMGPU_OK = 0,
+  FMMGPU_INVALID_ARGUMENT = 1, /* std::invalid_argument (geometry.cpp:65-69, chebyshev.cpp:58-59) */
+  FMMGPU_DOMAIN_ERROR = 2,     /* std::domain_error (geometry.cpp:86-87, 134) */
+  FMMGPU_OUT_OF_RANGE = 3,     /* std::out_of_range (direct.cpp:79-80) */
+  FMMGPU_LOGIC_ERROR = 4,      /* std::logic_error (m2l.cpp:69, taskflow.cpp:271) */
+  FMMGPU_RUNTIME_ERROR = 5     /* std::runtime_error, CUDA / cuSOLVER failures */
+};
+
+/* Task kinds, same numbering as taskfmm::TaskKind (taskflow.hpp:15). */
+enum fmmgpu_kind {
+  FMMGPU_P2M = 0, FMMGPU_M2M = 1, FMMGPU_M2L = 2, FMMGPU_L2L = 3,
+  FMMGPU_L2P = 4, FMMGPU_P2P = 5, FMMGPU_P2PREDUCE = 6
+};
+
+/* ---- context: InterpolationEngine(order) + M2LOperatorSet(order, eps) ----------
+ * chebyshev.cpp:57-76, m2l.cpp:136-163. The 16 canonical operators are assembled
+ * (m2l.cpp:90-111) and compressed with a truncated SVD on the device (cuSOLVER),
+ * rank rule of m2l.cpp:116-122. order in [2,10]; eps > 0 (reference: 10^-order). */
+int fmmgpu_create(int device, int order, double eps, fmmgpu_ctx** out);
+void fmmgpu_destroy(fmmgpu_ctx* ctx);
+const char* fmmgpu_last_error(const fmmgpu_ctx* ctx); /* never NULL */
+/* Process-wide error text for failures before a context exists. */
+const char* fmmgpu_global_error(void);
+
+/* M2LOperatorSet::load_cache / save_cache binary format (m2l.cpp:212-288):
+ * magic 0x4c324d4d4d465400, int32 order, f64 eps, 16 x int32 ranks, then per class
+ * row-major U (l^3 x r), sigma (r), V (l^3 x r). load replaces the operators. */
+int fmmgpu_load_m2l_cache(fmmgpu_ctx* ctx, const char* path);
+int fmmgpu_save_m2l_cache(const fmmgpu_ctx* ctx, const char* path);
+/* CompressionReport (m2l.hpp:56-62): ranks and multiplicities per canonical class. */
+int fmmgpu_m2l_report(const fmmgpu_ctx* ctx, int32_t* ranks16, int32_t* multiplicity16,
+                      double* weighted_mean_rank);
+
+/* ---- tree: GroupTree(particles, height, group_size[, root]) ---------------------
+ * geometry.cpp:59-161. xyzw: n particles as {x, y, z, w} doubles (Particle,
+ * geometry.hpp:16-19), in HOST memory (copied to the device inside the call) or
+ * DEVICE memory when xyzw_on_device != 0. root4 = {cx, cy, cz, width} or NULL for
+ * bounding_cube (geometry.cpp:18-36). height in [3,21], group_size >= 1. */
+int fmmgpu_build_tree(fmmgpu_ctx* ctx, const double* xyzw, uint64_t n, int xyzw_on_device,
+                      int height, int group_size, const double* root4);
+
+/* ---- interaction plan: build_interaction_plan (taskflow.cpp:67-105) -------------
+ * near CSR (direct.cpp:22-61: near_offsets / near_cells, plus total_directional) and
+ * per level v >= 2 the LevelM2L far pairs grouped by (block, canonical)
+ * (taskflow.cpp:78-94). The evaluation itself enumerates interactions implicitly;
+ * the explicit lists exist for parity, ledgers and reference tooling. */
+int fmmgpu_build_lists(fmmgpu_ctx* ctx);
+
+/* ---- evaluation: the payloads of FmmContext::run_task, level granular ----------
+ * Each call enqueues device work on the context's streams and returns; errors of
+ * asynchronous work surface at the next fmmgpu_synchronize / download. */
+int fmmgpu_reset(fmmgpu_ctx* ctx);                  /* bench.cpp:240-253 */
+int fmmgpu_p2m(fmmgpu_ctx* ctx);                    /* bench.cpp:259-273 (all leaf blocks) */
+int fmmgpu_m2m(fmmgpu_ctx* ctx, int parent_level);  /* bench.cpp:274-287, level 2..leaf-1 */
+int fmmgpu_m2l(fmmgpu_ctx* ctx, int level);         /* bench.cpp:288-299, level 2..leaf */
+int fmmgpu_l2l(fmmgpu_ctx* ctx, int parent_level);  /* bench.cpp:300-316, level 2..leaf-1 */
+int fmmgpu_l2p(fmmgpu_ctx* ctx);                    /* bench.cpp:317-336 */
+int fmmgpu_p2p(fmmgpu_ctx* ctx);                    /* bench.cpp:337-342: P2P + P2PREDUCE */
+/* reset, then the whole DAG as a level-synchronous two-stream schedule
+ * (far field on one stream, near field concurrently on another). */
+int fmmgpu_evaluate(fmmgpu_ctx* ctx);
+int fmmgpu_synchronize(fmmgpu_ctx* ctx);
+
+/* FmmContext::gather (bench.cpp:350-365): fields in input order into HOST or DEVICE
+ * arrays of n doubles each (any may be NULL). Synchronizes. */
+int fmmgpu_download_fields(fmmgpu_ctx* ctx, double* potential, double* fx, double* fy,
+                           double* fz, int dst_on_device);
+
+/* Whole run with host buffers: build_tree + evaluate + download_fields
+ * (run_fmm minus the oracle check, bench.cpp:415-469). */
+int fmmgpu_run(fmmgpu_ctx* ctx, const double* xyzw, uint64_t n, int height, int group_size,
+               double* potential, double* fx, double* fy, double* fz);
+
+/* ---- tree / plan / expansion access (parity dumps) ---------------------------- */
+int fmmgpu_tree_info(const fmmgpu_ctx* ctx, uint64_t* n, int* height, int* group_size,
+                     double* root4);
+uint64_t fmmgpu_level_cells(const fmmgpu_ctx* ctx, int level);
+/* cells as taskfmm::Cell AoS (geometry.hpp:34-41, 32 bytes each) and block_offsets
+ * (cells/group_size rounded up, plus one). */
+int fmmgpu_download_level(fmmgpu_ctx* ctx, int level, void* cells32, uint32_t* block_offsets);
+/* ParticleStore in Morton order (geometry.hpp:59-65). */
+int fmmgpu_download_particles(fmmgpu_ctx* ctx, double* x, double* y, double* z, double* w,
+                              uint32_t* id);
+/* Morton-order accumulators (potential/fx/fy/fz of ParticleStore). */
+int fmmgpu_download_sorted_fields(fmmgpu_ctx* ctx, double* potential, double* fx, double* fy,
+                                  double* fz);
+/* which: 0 multipole, 1 local_own, 2 local_down; cells x l^3 doubles, cell-major
+ * (GroupTree::allocate_expansions, geometry.cpp:199-206). */
+int fmmgpu_download_expansion(fmmgpu_ctx* ctx, int level, int which, double* out);
+int fmmgpu_upload_expansion(fmmgpu_ctx* ctx, int level, int which, const double* in);
+
+uint64_t fmmgpu_near_entries(const fmmgpu_ctx* ctx);
+int fmmgpu_download_near(fmmgpu_ctx* ctx, uint32_t* near_offsets, uint32_t* near_cells,
+                         uint64_t* total_directional);
+uint64_t fmmgpu_far_pairs(const fmmgpu_ctx* ctx, int level);
+/* M2LPairRef (m2l.hpp:66-70) as three arrays, and group_offsets (blocks*16+1). */
+int fmmgpu_download_far(fmmgpu_ctx* ctx, int level, uint32_t* target, uint32_t* source,
+                        uint16_t* vec, uint64_t* group_offsets);
+
+/* ---- measurement --------------------------------------------------------------- */
+/* Device time (ms, CUDA events) of the last fmmgpu_evaluate per kind (index =
+ * fmmgpu_kind; P2PREDUCE slot = field gather), plus [7] = whole evaluation,
+ * [8] = last build_tree, [9] = last build_lists. */
+int fmmgpu_timings(const fmmgpu_ctx* ctx, double* ms10);
+/* Analytic work of the current tree (flop_cost, bench.cpp:102-122; ledger,
+ * bench.cpp:151-181): flops per kind (7), near directional interactions, M2L pairs. */
+int fmmgpu_ledger(fmmgpu_ctx* ctx, uint64_t* flops7, uint64_t* near_directional,
+                  uint64_t* m2l_pairs);
+/* Number of kernels launched by the last fmmgpu_evaluate. */
+uint64_t fmmgpu_last_launch_count(const fmmgpu_ctx* ctx);
+/* Runs `steps` back-to-back evaluations bracketed by CUDA events on the launching
+ * stream: total_ms = device time of all steps; kind_ms10 (optional) = per-kind sums
+ * as in fmmgpu_timings; launches (optional) = kernels launched in the region. */
+int fmmgpu_time_evaluations(fmmgpu_ctx* ctx, int steps, double* total_ms, double* kind_ms10,
+                            uint64_t* launches);
+
+/* bench.cpp:19-61 generate_particles (mt19937_64, explicit scaling); dist 0 uniform,
+ * 1 sphere. Host-side input generator so both sides see identical doubles. */
+void fmmgpu_generate_particles(uint64_t n, int dist, uint64_t seed, double* xyzw);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMMGPU_H_ */

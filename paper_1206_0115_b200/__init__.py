@@ -1,0 +1,347 @@
+"""B200-native black-box Chebyshev FMM evaluation path (arXiv 1206.0115, "taskfmm").
+
+Host-side mirror of the reference's operator interface, over the C ABI of
+``include/fmmgpu.h`` (``libfmmgpu.so``, CUDA sm_100a). Names follow the reference:
+
+* ``RunConfig``            bench.hpp:21-35
+* ``generate_particles``   bench.cpp:29-61 (same mt19937_64 stream, host side)
+* ``FmmContext``           bench.hpp:86-121 -- tree + operators + evaluation; the
+  reference's ``run_task(Task)`` seam is exposed per operator and level
+  (``p2m``, ``m2m(v)``, ``m2l(v)``, ``l2l(v)``, ``l2p``, ``p2p``) and as the whole
+  schedule (``evaluate``); ``gather`` returns fields in input order.
+* ``run_fmm``              bench.cpp:415-469 (without the oracle check)
+
+There is no CPU fallback: if the CUDA library is missing or no GPU is present the
+calls raise. The reference's exception classes map to Python exceptions of the
+same meaning (ValueError = invalid_argument, DomainError = domain_error, ...).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import c_double, c_int, c_uint64, c_void_p, byref
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfmmgpu.so")
+
+KINDS = ("P2M", "M2M", "M2L", "L2L", "L2P", "P2P", "P2PREDUCE")
+CELL_DTYPE = np.dtype(
+    [("code", "<u8"), ("first_particle", "<u4"), ("particle_count", "<u4"), ("parent", "<u4"),
+     ("first_child", "<u4"), ("child_count", "<u4"), ("_pad", "<u4")])
+
+
+class FmmError(RuntimeError):
+    code = 5
+
+
+class DomainError(FmmError, ValueError):      # std::domain_error
+    code = 2
+
+
+class InvalidArgument(FmmError, ValueError):  # std::invalid_argument
+    code = 1
+
+
+class OutOfRange(FmmError, IndexError):       # std::out_of_range
+    code = 3
+
+
+class LogicError(FmmError):                   # std::logic_error
+    code = 4
+
+
+_ERRORS = {1: InvalidArgument, 2: DomainError, 3: OutOfRange, 4: LogicError, 5: FmmError}
+
+_lib = None
+
+
+def lib():
+    """Loads libfmmgpu.so (built by ``__graft_entry__.build()`` / ``make -C paper_1206_0115_b200``)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FmmError(f"{LIB_PATH} missing: build it with `make -C {_HERE}` (no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.fmmgpu_last_error.restype = ctypes.c_char_p
+        L.fmmgpu_last_error.argtypes = [c_void_p]
+        L.fmmgpu_global_error.restype = ctypes.c_char_p
+        L.fmmgpu_create.argtypes = [c_int, c_int, c_double, ctypes.POINTER(c_void_p)]
+        L.fmmgpu_destroy.argtypes = [c_void_p]
+        L.fmmgpu_build_tree.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_int, c_int, c_void_p]
+        L.fmmgpu_level_cells.restype = c_uint64
+        L.fmmgpu_level_cells.argtypes = [c_void_p, c_int]
+        L.fmmgpu_near_entries.restype = c_uint64
+        L.fmmgpu_near_entries.argtypes = [c_void_p]
+        L.fmmgpu_far_pairs.restype = c_uint64
+        L.fmmgpu_far_pairs.argtypes = [c_void_p, c_int]
+        L.fmmgpu_last_launch_count.restype = c_uint64
+        L.fmmgpu_last_launch_count.argtypes = [c_void_p]
+        L.fmmgpu_generate_particles.argtypes = [c_uint64, c_int, c_uint64, c_void_p]
+        L.fmmgpu_run.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]
+        for name in ("fmmgpu_reset", "fmmgpu_p2m", "fmmgpu_l2p", "fmmgpu_p2p", "fmmgpu_evaluate",
+                     "fmmgpu_synchronize", "fmmgpu_build_lists"):
+            getattr(L, name).argtypes = [c_void_p]
+        for name in ("fmmgpu_m2m", "fmmgpu_m2l", "fmmgpu_l2l"):
+            getattr(L, name).argtypes = [c_void_p, c_int]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(c_void_p)
+
+
+@dataclass
+class RunConfig:
+    """bench.hpp:21-35 (the fields this path uses)."""
+    n: int = 10000
+    dist: str = "uniform"
+    height: int = 4
+    acc: int = 5          # interpolation order l = acc, SVD eps = 10^-acc
+    group_size: int = 250
+    seed: int = 42
+    device: int = 0
+
+
+def generate_particles(n: int, dist: str = "uniform", seed: int = 42) -> np.ndarray:
+    """bench.cpp:29-61: (n, 4) array of x, y, z, w (unit weights)."""
+    out = np.zeros((n, 4), dtype=np.float64)
+    lib().fmmgpu_generate_particles(n, 0 if dist == "uniform" else 1, seed, _p(out))
+    return out
+
+
+class FmmContext:
+    """FmmContext (bench.hpp:86-121) on one B200.
+
+    ``FmmContext(particles, cfg)`` builds the operators (InterpolationEngine +
+    M2LOperatorSet, device SVD) and the tree on the GPU; ``evaluate()`` runs the
+    whole evaluation; ``gather()`` returns (potential, fx, fy, fz) in input order.
+    """
+
+    def __init__(self, particles=None, cfg: RunConfig | None = None, *, order=None, eps=None, device=0):
+        self.cfg = cfg or RunConfig()
+        self.order = order if order is not None else self.cfg.acc
+        if self.order < 2:
+            raise InvalidArgument("accuracy parameter must be at least 2")  # bench.cpp:223
+        self.eps = eps if eps is not None else 10.0 ** (-self.order)
+        self._lib = lib()
+        h = c_void_p()
+        rc = self._lib.fmmgpu_create(device if cfg is None else cfg.device, self.order, self.eps, byref(h))
+        if rc:
+            raise _ERRORS.get(rc, FmmError)(self._lib.fmmgpu_global_error().decode())
+        self.h = h
+        self.n = 0
+        if particles is not None:
+            self.build_tree(particles, self.cfg.height, self.cfg.group_size)
+
+    # -- plumbing
+    def _check(self, rc):
+        if rc:
+            raise _ERRORS.get(rc, FmmError)(self._lib.fmmgpu_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.fmmgpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- M2LOperatorSet
+    def load_m2l_cache(self, path: str):
+        self._check(self._lib.fmmgpu_load_m2l_cache(self.h, path.encode()))
+
+    def save_m2l_cache(self, path: str):
+        self._check(self._lib.fmmgpu_save_m2l_cache(self.h, path.encode()))
+
+    def compression_report(self):
+        r = np.zeros(16, dtype=np.int32)
+        m = np.zeros(16, dtype=np.int32)
+        w = c_double()
+        self._check(self._lib.fmmgpu_m2l_report(self.h, _p(r), _p(m), byref(w)))
+        return {"ranks": r, "multiplicity": m, "weighted_mean_rank": w.value}
+
+    # -- GroupTree
+    def build_tree(self, particles, height: int, group_size: int = 250, root=None, on_device_ptr=None):
+        """GroupTree(particles, height, group_size[, root]); particles (n,4) float64."""
+        if on_device_ptr is not None:
+            n = int(particles)
+            self._check(self._lib.fmmgpu_build_tree(self.h, c_void_p(on_device_ptr), n, 1, height, group_size,
+                                                    _p(None if root is None else np.asarray(root, np.float64))))
+        else:
+            xyzw = np.ascontiguousarray(particles, dtype=np.float64)
+            if xyzw.ndim != 2 or (len(xyzw) and xyzw.shape[1] != 4):
+                raise InvalidArgument("particles must be an (n, 4) array of x, y, z, w")
+            n = len(xyzw)
+            r = None if root is None else np.ascontiguousarray(root, dtype=np.float64)
+            self._check(self._lib.fmmgpu_build_tree(self.h, _p(xyzw) if n else None, n, 0, height, group_size, _p(r)))
+        self.n, self.height, self.group_size = n, height, group_size
+
+    def build_lists(self):
+        self._check(self._lib.fmmgpu_build_lists(self.h))
+
+    def root_cube(self):
+        out = np.zeros(4)
+        n = c_uint64()
+        self._check(self._lib.fmmgpu_tree_info(self.h, byref(n), None, None, _p(out)))
+        return out
+
+    def level(self, v: int):
+        n = self._lib.fmmgpu_level_cells(self.h, v)
+        cells = np.zeros(n, dtype=CELL_DTYPE)
+        nb = (n + self.group_size - 1) // self.group_size
+        bo = np.zeros(nb + 1, dtype=np.uint32)
+        self._check(self._lib.fmmgpu_download_level(self.h, v, _p(cells), _p(bo)))
+        return cells, bo
+
+    def particles(self):
+        x, y, z, w = (np.zeros(self.n) for _ in range(4))
+        ids = np.zeros(self.n, dtype=np.uint32)
+        self._check(self._lib.fmmgpu_download_particles(self.h, _p(x), _p(y), _p(z), _p(w), _p(ids)))
+        return x, y, z, w, ids
+
+    def near(self):
+        ne = self._lib.fmmgpu_near_entries(self.h)
+        nc = self._lib.fmmgpu_level_cells(self.h, self.height - 1)
+        off = np.zeros(nc + 1, dtype=np.uint32)
+        cells = np.zeros(max(ne, 1), dtype=np.uint32)
+        tot = c_uint64()
+        self._check(self._lib.fmmgpu_download_near(self.h, _p(off), _p(cells), byref(tot)))
+        return off, cells[:ne], tot.value
+
+    def far(self, v: int):
+        npairs = self._lib.fmmgpu_far_pairs(self.h, v)
+        nc = self._lib.fmmgpu_level_cells(self.h, v)
+        nb = (nc + self.group_size - 1) // self.group_size
+        t = np.zeros(max(npairs, 1), dtype=np.uint32)
+        s = np.zeros(max(npairs, 1), dtype=np.uint32)
+        vec = np.zeros(max(npairs, 1), dtype=np.uint16)
+        go = np.zeros(nb * 16 + 1, dtype=np.uint64)
+        self._check(self._lib.fmmgpu_download_far(self.h, v, _p(t), _p(s), _p(vec), _p(go)))
+        return t[:npairs], s[:npairs], vec[:npairs], go
+
+    def expansion(self, v: int, which: int):
+        """which: 0 multipole, 1 local_own, 2 local_down; (cells, l^3)."""
+        n = self._lib.fmmgpu_level_cells(self.h, v)
+        out = np.zeros((n, self.order ** 3))
+        self._check(self._lib.fmmgpu_download_expansion(self.h, v, which, _p(out)))
+        return out
+
+    def set_expansion(self, v: int, which: int, values):
+        a = np.ascontiguousarray(values, dtype=np.float64)
+        self._check(self._lib.fmmgpu_upload_expansion(self.h, v, which, _p(a)))
+
+    # -- the run_task seam, level granular (bench.cpp:255-344)
+    def reset(self):
+        self._check(self._lib.fmmgpu_reset(self.h))
+
+    def p2m(self):
+        self._check(self._lib.fmmgpu_p2m(self.h))
+
+    def m2m(self, parent_level: int):
+        self._check(self._lib.fmmgpu_m2m(self.h, parent_level))
+
+    def m2l(self, level: int):
+        self._check(self._lib.fmmgpu_m2l(self.h, level))
+
+    def l2l(self, parent_level: int):
+        self._check(self._lib.fmmgpu_l2l(self.h, parent_level))
+
+    def l2p(self):
+        self._check(self._lib.fmmgpu_l2p(self.h))
+
+    def p2p(self):
+        self._check(self._lib.fmmgpu_p2p(self.h))
+
+    def run_kinds(self, kinds):
+        """reset + the selected payload kinds in DAG order (cf. oracle ref_run_serial)."""
+        self.reset()
+        leaf = self.height - 1
+        if "P2M" in kinds:
+            self.p2m()
+        if "M2M" in kinds:
+            for v in range(leaf - 1, 1, -1):
+                self.m2m(v)
+        if "M2L" in kinds:
+            for v in range(2, leaf + 1):
+                self.m2l(v)
+        if "L2L" in kinds:
+            for v in range(2, leaf):
+                self.l2l(v)
+        if "L2P" in kinds:
+            self.l2p()
+        if "P2P" in kinds:
+            self.p2p()
+        self.synchronize()
+
+    def evaluate(self):
+        """The whole evaluation (all payloads of the task graph), asynchronous."""
+        self._check(self._lib.fmmgpu_evaluate(self.h))
+
+    def synchronize(self):
+        self._check(self._lib.fmmgpu_synchronize(self.h))
+
+    def gather(self):
+        """FmmContext::gather (bench.cpp:350-365): potential, fx, fy, fz in input order."""
+        out = [np.zeros(self.n) for _ in range(4)]
+        self._check(self._lib.fmmgpu_download_fields(self.h, *[_p(a) for a in out], 0))
+        return out
+
+    def gather_device(self, ptrs):
+        self._check(self._lib.fmmgpu_download_fields(self.h, *[c_void_p(p) for p in ptrs], 1))
+
+    def sorted_fields(self):
+        out = [np.zeros(self.n) for _ in range(4)]
+        self._check(self._lib.fmmgpu_download_sorted_fields(self.h, *[_p(a) for a in out]))
+        return out
+
+    def timings(self):
+        ms = np.zeros(10)
+        self._check(self._lib.fmmgpu_timings(self.h, _p(ms)))
+        keys = list(KINDS[:6]) + ["GATHER", "EVAL", "TREE", "LISTS"]
+        return dict(zip(keys, ms.tolist()))
+
+    def ledger(self):
+        flops = np.zeros(7, dtype=np.uint64)
+        near = c_uint64()
+        pairs = c_uint64()
+        self._check(self._lib.fmmgpu_ledger(self.h, _p(flops), byref(near), byref(pairs)))
+        return {"flops": dict(zip(KINDS, flops.tolist())), "near_directional": near.value, "m2l_pairs": pairs.value}
+
+    def launch_count(self):
+        return int(self._lib.fmmgpu_last_launch_count(self.h))
+
+    def time_evaluations(self, steps: int):
+        """K back-to-back evaluations timed with CUDA events on the launching stream.
+        Returns (total_ms, per-kind ms sums, kernel launches)."""
+        total = c_double()
+        ms = np.zeros(10)
+        nl = c_uint64()
+        self._check(self._lib.fmmgpu_time_evaluations(self.h, steps, byref(total), _p(ms), byref(nl)))
+        keys = list(KINDS[:6]) + ["GATHER", "EVAL", "TREE", "LISTS"]
+        return total.value, dict(zip(keys, ms.tolist())), nl.value
+
+    def run(self, particles, height, group_size=250):
+        """Whole run through the C ABI with host buffers (fmmgpu_run)."""
+        xyzw = np.ascontiguousarray(particles, dtype=np.float64)
+        n = len(xyzw)
+        out = [np.zeros(n) for _ in range(4)]
+        self._check(self._lib.fmmgpu_run(self.h, _p(xyzw), n, height, group_size, *[_p(a) for a in out]))
+        self.n, self.height, self.group_size = n, height, group_size
+        return out
+
+
+def run_fmm(cfg: RunConfig, particles=None):
+    """run_fmm (bench.cpp:415-469) minus the oracle check: returns fields in input order."""
+    xyzw = generate_particles(cfg.n, cfg.dist, cfg.seed) if particles is None else particles
+    with FmmContext(None, cfg) as ctx:
+        return ctx.run(xyzw, cfg.height, cfg.group_size)

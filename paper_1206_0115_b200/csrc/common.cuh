@@ -1,0 +1,218 @@
+// Shared definitions of the B200 FMM path: context layout in HBM, Morton helpers,
+// cell lookup, FP64 reciprocal square root. See DESIGN.md "Data layout in HBM".
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fmmgpu.h"
+
+namespace fmmgpu {
+
+constexpr uint32_t NPOS = 0xffffffffu;
+constexpr int MAX_ORDER = 10;
+constexpr int DENSE_MAP_MAX_LEVEL = 9;  // 8^9 x 4 B = 512 MB worst case
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define FMM_CUDA(x)                                                                       \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::fmmgpu::Error(FMMGPU_RUNTIME_ERROR, std::string("CUDA: ") +                 \
+                                                      cudaGetErrorString(e_) + " at " +   \
+                                                      __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// ---------------------------------------------------------------- Morton codes
+// geometry.cpp:38-57: bit b of i -> 3b+2, j -> 3b+1, k -> 3b.
+__host__ __device__ inline uint64_t spread3(uint32_t x) {
+  uint64_t v = x & 0x1fffffu;
+  v = (v | (v << 32)) & 0x1f00000000ffffULL;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffULL;
+  v = (v | (v << 8)) & 0x100f00f00f00f00fULL;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ULL;
+  v = (v | (v << 2)) & 0x1249249249249249ULL;
+  return v;
+}
+__host__ __device__ inline uint32_t compact3(uint64_t v) {
+  v &= 0x1249249249249249ULL;
+  v = (v ^ (v >> 2)) & 0x10c30c30c30c30c3ULL;
+  v = (v ^ (v >> 4)) & 0x100f00f00f00f00fULL;
+  v = (v ^ (v >> 8)) & 0x1f0000ff0000ffULL;
+  v = (v ^ (v >> 16)) & 0x1f00000000ffffULL;
+  v = (v ^ (v >> 32)) & 0x1fffffULL;
+  return static_cast<uint32_t>(v);
+}
+__host__ __device__ inline uint64_t morton(uint32_t i, uint32_t j, uint32_t k) {
+  return (spread3(i) << 2) | (spread3(j) << 1) | spread3(k);
+}
+__host__ __device__ inline void demorton(uint64_t c, int* ijk) {
+  ijk[0] = static_cast<int>(compact3(c >> 2));
+  ijk[1] = static_cast<int>(compact3(c >> 1));
+  ijk[2] = static_cast<int>(compact3(c));
+}
+
+// Cell lookup on one level (GroupTree::find_cell, geometry.cpp:177-186): O(1) on a
+// full level, a dense code->index map up to DENSE_MAP_MAX_LEVEL, else binary search.
+struct LevelView {
+  const uint64_t* code;
+  const uint32_t* map;
+  uint32_t n;
+  int level;
+  int full;
+};
+__device__ inline uint32_t find_cell(const LevelView& L, uint64_t code) {
+  if (L.full) return static_cast<uint32_t>(code);
+  if (L.map) return L.map[code];
+  uint32_t lo = 0, hi = L.n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (L.code[mid] < code) lo = mid + 1; else hi = mid;
+  }
+  return (lo < L.n && L.code[lo] == code) ? lo : NPOS;
+}
+// grid coords -> cell index or NPOS (out of range / absent)
+__device__ inline uint32_t find_ijk(const LevelView& L, int i, int j, int k) {
+  const int g = 1 << L.level;
+  if (i < 0 || j < 0 || k < 0 || i >= g || j >= g || k >= g) return NPOS;
+  return find_cell(L, morton(static_cast<uint32_t>(i), static_cast<uint32_t>(j), static_cast<uint32_t>(k)));
+}
+
+// FP64 1/sqrt(x), x > 0: MUFU.RSQ64H seed (rsqrt.approx.ftz.f64) and one
+// third-order Newton step: e = 1 - x y^2, y *= 1 + e/2 + 3e^2/8. With the seed's
+// ~2^-22 relative error the residual is ~2^-65, i.e. rounding-level (checked by
+// tests/test_gpu_kernels.py against 1/sqrt). 5 DP ops + 1 MUFU versus ~12 DP-op
+// equivalents for the libdevice rsqrt (profiles/r01_fp64_peaks.txt).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double t = x * y;
+  const double e = fma(-t, y, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  return fma(y, e * p, y);
+}
+
+// ---------------------------------------------------------------- context
+struct Level {
+  uint32_t n = 0;
+  bool full = false;
+  uint64_t* code = nullptr;
+  uint32_t *first_particle = nullptr, *particle_count = nullptr, *parent = nullptr,
+           *first_child = nullptr, *child_count = nullptr;
+  uint32_t* map = nullptr;         // dense code -> index (sparse levels <= DENSE_MAP_MAX_LEVEL)
+  uint32_t* cls_cells = nullptr;   // cell indices grouped by parity class (code & 7)
+  uint32_t cls_off[9] = {};        // class offsets into cls_cells (host copy)
+  double *multipole = nullptr, *local_own = nullptr, *local_down = nullptr;  // n x ldE
+  std::vector<uint32_t> block_offsets;
+  // far plan (LevelM2L), built by fmmgpu_build_lists
+  uint64_t far_pairs = 0;
+  uint32_t *far_target = nullptr, *far_source = nullptr;
+  uint16_t* far_vec = nullptr;
+  uint64_t* far_group_off = nullptr;
+  LevelView view(int v) const { return LevelView{code, map, n, v, full ? 1 : 0}; }
+};
+
+struct M2LTables {
+  // host-side operator factors (cache format): per class row-major U, sigma, V
+  int rank[16] = {};
+  int mult[16] = {};
+  std::vector<double> u[16], sigma[16], v[16];
+  int canonical[343];
+  std::vector<uint32_t> perm[343];  // grid permutation per vector slot
+  // stacked operators
+  int R = 0;        // rows of the source-side stack = columns of the target-side stack
+  int ldY = 0;      // round_up(R, 16): stride of one target's compressed vector
+  int rowsA = 0;    // round_up(R, 64): padded M of phase A
+  int rowsB = 0;    // round_up(l^3, 64)... padded M of phase B
+  double* dM1 = nullptr;    // [8][rowsA][ldE]
+  double* dM2 = nullptr;    // [8][rowsB][ldY]
+  int2* dRowA = nullptr;    // [8][rowsA]: {slot or -1, destination column in Yt}
+  int* dKslot = nullptr;    // [8][ldY]: vector slot of column kk of the target stack, -1 = pad
+  double* dYt = nullptr;    // compressed intermediates, cells x ldY of the largest level
+  size_t yt_cells = 0;
+};
+
+struct Timing {
+  cudaEvent_t ev[32];
+  int used = 0;
+};
+
+}  // namespace fmmgpu
+
+struct fmmgpu_ctx {
+  int device = 0;
+  int order = 0;
+  double eps = 0;
+  int l3 = 0;
+  int ldE = 0;  // padded expansion stride (multiple of 16 doubles)
+  std::string err;
+  cudaStream_t s_far = nullptr, s_near = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_t[16] = {};
+  double timings[10] = {};
+  uint64_t launches = 0;
+  // interpolation tables (device): tn[l][l-1], child[2][l*l], child_t[2][l*l]
+  double* d_interp = nullptr;
+  std::vector<double> h_roots, h_tn, h_child[2], h_child_t[2];
+  fmmgpu::M2LTables m2l;
+  // tree
+  bool have_tree = false;
+  uint64_t n = 0;
+  int height = 0, group = 0;
+  double root[4] = {};
+  double lo[3] = {};
+  std::vector<fmmgpu::Level> lv;
+  double4* d_in = nullptr;       // input particles, input order
+  size_t d_in_cap = 0;
+  double4* d_pw = nullptr;       // Morton-ordered {x,y,z,w}
+  uint32_t* d_id = nullptr;      // original index per Morton slot
+  uint32_t* d_pcell = nullptr;   // leaf cell per Morton slot
+  double* d_near = nullptr;      // near-field fields [4][n] (Morton order)
+  double* d_far = nullptr;       // far-field fields [4][n] (Morton order)
+  double* d_out = nullptr;       // gathered fields [4][n] (input order)
+  bool out_valid = false;        // d_out holds near + far of the current arrays
+  int* d_flag = nullptr;         // error flags
+  // near plan
+  bool have_lists = false;
+  uint32_t* d_near_off = nullptr;
+  uint32_t* d_near_cells = nullptr;
+  uint64_t near_entries = 0;
+  uint64_t near_directional = 0;
+  // scratch
+  void* d_tmp = nullptr;
+  size_t d_tmp_cap = 0;
+  int* d_canon = nullptr;  // canonical class per vector slot (343)
+};
+
+namespace fmmgpu {
+// implemented in the .cu files
+void interp_setup(fmmgpu_ctx* c);
+void m2l_setup(fmmgpu_ctx* c, bool compute_factors);
+void m2l_free(fmmgpu_ctx* c);
+void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, int height, int group,
+                const double* root4);
+void tree_free(fmmgpu_ctx* c);
+void lists_build(fmmgpu_ctx* c);
+void lists_free(fmmgpu_ctx* c);
+void launch_p2m(fmmgpu_ctx* c, cudaStream_t s);
+void launch_m2m(fmmgpu_ctx* c, int parent_level, cudaStream_t s);
+void launch_l2l(fmmgpu_ctx* c, int parent_level, cudaStream_t s);
+void launch_l2p(fmmgpu_ctx* c, cudaStream_t s);
+void launch_m2l(fmmgpu_ctx* c, int level, cudaStream_t s);
+void launch_p2p(fmmgpu_ctx* c, cudaStream_t s);
+void launch_gather(fmmgpu_ctx* c, cudaStream_t s);
+void* scratch(fmmgpu_ctx* c, size_t bytes);
+uint64_t near_directional_count(fmmgpu_ctx* c);
+int canonicalize_host(const int v[3], int perm[3], int sign[3]);
+inline int vec_slot(int i, int j, int k) { return (i + 3) * 49 + (j + 3) * 7 + (k + 3); }
+}  // namespace fmmgpu

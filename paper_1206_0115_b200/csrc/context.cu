@@ -1,0 +1,628 @@
+// C ABI (include/fmmgpu.h): context lifetime, operator dispatch, the evaluation
+// schedule, downloads for parity, timings and the flop ledger.
+//
+// The schedule replaces the reference's task DAG + worker pool (taskflow.cpp:143-289,
+// runtime.cpp:91-216) by a fixed level-synchronous order on two CUDA streams:
+//   s_far : P2M -> M2M(leaf-1..2) -> M2L(2..leaf) -> L2L(2..leaf-1) -> L2P
+//   s_near: P2P (concurrent with the whole far chain; the paper's pipelining of
+//           near and far field)
+// joined before the gather that sums both and returns input order. Every output
+// array has one writer per phase, so results are run-to-run bitwise reproducible
+// (the reference's single-writer property, README.md:84-92).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "common.cuh"
+
+using namespace fmmgpu;
+
+namespace {
+
+thread_local std::string g_global_err;
+
+template <typename F>
+int guarded(fmmgpu_ctx* c, F&& f) {
+  try {
+    f();
+    return FMMGPU_OK;
+  } catch (const Error& e) {
+    if (c) c->err = e.what();
+    g_global_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    g_global_err = e.what();
+    return FMMGPU_RUNTIME_ERROR;
+  }
+}
+
+void need_tree(const fmmgpu_ctx* c) {
+  if (!c->have_tree) throw Error(FMMGPU_LOGIC_ERROR, "no tree: call fmmgpu_build_tree first");
+}
+void need_level(const fmmgpu_ctx* c, int v, int lo, int hi, const char* what) {
+  need_tree(c);
+  if (v < lo || v > hi) throw Error(FMMGPU_OUT_OF_RANGE, std::string(what) + ": level out of range");
+}
+
+__global__ void k_pad_copy(const double* __restrict__ src, int l3, int ldE, uint64_t cells, double* __restrict__ dst,
+                           int to_padded) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= cells * l3) return;
+  const uint64_t c = i / l3, k = i % l3;
+  if (to_padded) dst[c * ldE + k] = src[i];
+  else dst[i] = src[c * ldE + k];
+}
+
+__global__ void k_cells_aos(const uint64_t* code, const uint32_t* fp, const uint32_t* pc, const uint32_t* par,
+                            const uint32_t* fc, const uint32_t* cc, uint32_t n, uint32_t* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t* o = out + 8ull * i;
+  const uint64_t cd = code[i];
+  o[0] = static_cast<uint32_t>(cd);
+  o[1] = static_cast<uint32_t>(cd >> 32);
+  o[2] = fp[i];
+  o[3] = pc[i];
+  o[4] = par[i];
+  o[5] = fc[i];
+  o[6] = cc[i];
+  o[7] = 0;
+}
+
+__global__ void k_soa(const double4* pw, uint64_t n, double* x, double* y, double* z, double* w) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double4 p = pw[i];
+  x[i] = p.x; y[i] = p.y; z[i] = p.z; w[i] = p.w;
+}
+
+__global__ void k_sum4(const double* a, const double* b, uint64_t n4, double* out) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n4) out[i] = a[i] + b[i];
+}
+
+void reset_arrays(fmmgpu_ctx* c, cudaStream_t s) {
+  for (auto& L : c->lv) {
+    const size_t e = size_t(L.n) * c->ldE * sizeof(double);
+    FMM_CUDA(cudaMemsetAsync(L.multipole, 0, e, s));
+    FMM_CUDA(cudaMemsetAsync(L.local_own, 0, e, s));
+    FMM_CUDA(cudaMemsetAsync(L.local_down, 0, e, s));
+  }
+  FMM_CUDA(cudaMemsetAsync(c->d_near, 0, 32 * c->n, s));
+  FMM_CUDA(cudaMemsetAsync(c->d_far, 0, 32 * c->n, s));
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fmmgpu_global_error(void) { return g_global_err.c_str(); }
+const char* fmmgpu_last_error(const fmmgpu_ctx* c) { return c ? c->err.c_str() : g_global_err.c_str(); }
+
+int fmmgpu_create(int device, int order, double eps, fmmgpu_ctx** out) {
+  if (!out) return FMMGPU_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* c = new fmmgpu_ctx;
+  const int rc = guarded(c, [&] {
+    if (order < 2 || order > MAX_ORDER) throw Error(FMMGPU_INVALID_ARGUMENT, "InterpolationEngine: order must be in [2, 10]");
+    if (!(eps > 0)) throw Error(FMMGPU_INVALID_ARGUMENT, "M2LOperatorSet: eps must be positive");
+    int ndev = 0;
+    FMM_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Error(FMMGPU_INVALID_ARGUMENT, "no such CUDA device");
+    c->device = device;
+    c->order = order;
+    c->eps = eps;
+    c->l3 = order * order * order;
+    c->ldE = round_up(c->l3, 16);
+    FMM_CUDA(cudaSetDevice(device));
+    cudaMemPool_t pool;
+    FMM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    FMM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    FMM_CUDA(cudaStreamCreateWithFlags(&c->s_far, cudaStreamNonBlocking));
+    FMM_CUDA(cudaStreamCreateWithFlags(&c->s_near, cudaStreamNonBlocking));
+    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    for (auto& e : c->ev_t) FMM_CUDA(cudaEventCreate(&e));
+    FMM_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
+    interp_setup(c);
+    m2l_setup(c, true);
+  });
+  if (rc != FMMGPU_OK) {
+    g_global_err = c->err;
+    fmmgpu_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return FMMGPU_OK;
+}
+
+void fmmgpu_destroy(fmmgpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->s_far) {
+    cudaStreamSynchronize(c->s_far);
+    cudaStreamSynchronize(c->s_near);
+    try {
+      lists_free(c);
+      tree_free(c);
+    } catch (...) {
+    }
+    if (c->d_in) cudaFreeAsync(c->d_in, c->s_far);
+    if (c->d_tmp) cudaFreeAsync(c->d_tmp, c->s_far);
+    cudaStreamSynchronize(c->s_far);
+  }
+  m2l_free(c);
+  if (c->d_interp) cudaFree(c->d_interp);
+  if (c->d_flag) cudaFree(c->d_flag);
+  if (c->d_canon) cudaFree(c->d_canon);
+  for (auto& e : c->ev_t)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->s_far) cudaStreamDestroy(c->s_far);
+  if (c->s_near) cudaStreamDestroy(c->s_near);
+  delete c;
+}
+
+int fmmgpu_load_m2l_cache(fmmgpu_ctx* c, const char* path) {
+  return guarded(c, [&] {
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) throw Error(FMMGPU_RUNTIME_ERROR, std::string("cannot open M2L cache ") + path);
+    uint64_t magic = 0;
+    int32_t order = 0;
+    double eps = 0;
+    bool ok = std::fread(&magic, 8, 1, f) == 1 && std::fread(&order, 4, 1, f) == 1 && std::fread(&eps, 8, 1, f) == 1;
+    if (!ok || magic != 0x4c324d4d4d465400ull || order != c->order || eps != c->eps) {
+      std::fclose(f);
+      throw Error(FMMGPU_INVALID_ARGUMENT, "M2L cache does not match (magic, order, eps)");
+    }
+    int32_t ranks[16];
+    ok = std::fread(ranks, 4, 16, f) == 16;
+    auto& T = c->m2l;
+    for (int cl = 0; cl < 16 && ok; ++cl) {
+      if (ranks[cl] < 1 || ranks[cl] > c->l3) { ok = false; break; }
+      T.rank[cl] = ranks[cl];
+      T.u[cl].resize(size_t(c->l3) * ranks[cl]);
+      T.sigma[cl].resize(ranks[cl]);
+      T.v[cl].resize(size_t(c->l3) * ranks[cl]);
+      ok = ok && std::fread(T.u[cl].data(), 8, T.u[cl].size(), f) == T.u[cl].size();
+      ok = ok && std::fread(T.sigma[cl].data(), 8, T.sigma[cl].size(), f) == T.sigma[cl].size();
+      ok = ok && std::fread(T.v[cl].data(), 8, T.v[cl].size(), f) == T.v[cl].size();
+    }
+    std::fclose(f);
+    if (!ok) throw Error(FMMGPU_RUNTIME_ERROR, "truncated or corrupt M2L cache");
+    m2l_setup(c, false);
+  });
+}
+
+int fmmgpu_save_m2l_cache(const fmmgpu_ctx* cc, const char* path) {
+  auto* c = const_cast<fmmgpu_ctx*>(cc);
+  return guarded(c, [&] {
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) throw Error(FMMGPU_RUNTIME_ERROR, std::string("cannot write ") + path);
+    const uint64_t magic = 0x4c324d4d4d465400ull;
+    const int32_t order = c->order;
+    bool ok = std::fwrite(&magic, 8, 1, f) == 1 && std::fwrite(&order, 4, 1, f) == 1 && std::fwrite(&c->eps, 8, 1, f) == 1;
+    const auto& T = c->m2l;
+    for (int cl = 0; cl < 16; ++cl) {
+      const int32_t r = T.rank[cl];
+      ok = ok && std::fwrite(&r, 4, 1, f) == 1;
+    }
+    for (int cl = 0; cl < 16; ++cl) {
+      ok = ok && std::fwrite(T.u[cl].data(), 8, T.u[cl].size(), f) == T.u[cl].size();
+      ok = ok && std::fwrite(T.sigma[cl].data(), 8, T.sigma[cl].size(), f) == T.sigma[cl].size();
+      ok = ok && std::fwrite(T.v[cl].data(), 8, T.v[cl].size(), f) == T.v[cl].size();
+    }
+    std::fclose(f);
+    if (!ok) throw Error(FMMGPU_RUNTIME_ERROR, "write failed");
+  });
+}
+
+int fmmgpu_m2l_report(const fmmgpu_ctx* c, int32_t* ranks16, int32_t* mult16, double* wmean) {
+  if (!c) return FMMGPU_INVALID_ARGUMENT;
+  double acc = 0;
+  for (int cl = 0; cl < 16; ++cl) {
+    if (ranks16) ranks16[cl] = c->m2l.rank[cl];
+    if (mult16) mult16[cl] = c->m2l.mult[cl];
+    acc += double(c->m2l.mult[cl]) * c->m2l.rank[cl];
+  }
+  if (wmean) *wmean = acc / 316.0;  // m2l.cpp:159-162
+  return FMMGPU_OK;
+}
+
+int fmmgpu_build_tree(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int on_device, int height, int group,
+                      const double* root4) {
+  return guarded(c, [&] {
+    FMM_CUDA(cudaSetDevice(c->device));
+    FMM_CUDA(cudaEventRecord(c->ev_t[14], c->s_far));
+    c->out_valid = false;
+    tree_build(c, xyzw, n, on_device != 0, height, group, root4);
+    FMM_CUDA(cudaEventRecord(c->ev_t[15], c->s_far));
+    FMM_CUDA(cudaEventSynchronize(c->ev_t[15]));
+    c->timings[8] = elapsed(c->ev_t[14], c->ev_t[15]);
+  });
+}
+
+int fmmgpu_build_lists(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    need_tree(c);
+    FMM_CUDA(cudaEventRecord(c->ev_t[14], c->s_far));
+    lists_build(c);
+    FMM_CUDA(cudaEventRecord(c->ev_t[15], c->s_far));
+    FMM_CUDA(cudaEventSynchronize(c->ev_t[15]));
+    c->timings[9] = elapsed(c->ev_t[14], c->ev_t[15]);
+  });
+}
+
+int fmmgpu_reset(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    need_tree(c);
+    c->out_valid = false;
+    reset_arrays(c, c->s_far);
+  });
+}
+int fmmgpu_p2m(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    need_tree(c);
+    c->out_valid = false;
+    launch_p2m(c, c->s_far);
+  });
+}
+int fmmgpu_m2m(fmmgpu_ctx* c, int v) {
+  return guarded(c, [&] {
+    need_level(c, v, 0, c->height - 2, "m2m");
+    launch_m2m(c, v, c->s_far);
+  });
+}
+int fmmgpu_m2l(fmmgpu_ctx* c, int v) {
+  return guarded(c, [&] {
+    need_level(c, v, 2, c->height - 1, "m2l");
+    launch_m2l(c, v, c->s_far);
+  });
+}
+int fmmgpu_l2l(fmmgpu_ctx* c, int v) {
+  return guarded(c, [&] {
+    need_level(c, v, 0, c->height - 2, "l2l");
+    launch_l2l(c, v, c->s_far);
+  });
+}
+int fmmgpu_l2p(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    need_tree(c);
+    c->out_valid = false;
+    launch_l2p(c, c->s_far);
+  });
+}
+int fmmgpu_p2p(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    need_tree(c);
+    c->out_valid = false;
+    launch_p2p(c, c->s_far);
+  });
+}
+
+int fmmgpu_evaluate(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    need_tree(c);
+    FMM_CUDA(cudaSetDevice(c->device));
+    const int leaf = c->height - 1;
+    cudaStream_t s = c->s_far;
+    c->launches = 0;
+    cudaEvent_t* e = c->ev_t;
+    FMM_CUDA(cudaEventRecord(e[0], s));
+    reset_arrays(c, s);
+    FMM_CUDA(cudaEventRecord(c->ev_fork, s));
+    FMM_CUDA(cudaStreamWaitEvent(c->s_near, c->ev_fork, 0));
+    FMM_CUDA(cudaEventRecord(e[6], c->s_near));
+    launch_p2p(c, c->s_near);
+    FMM_CUDA(cudaEventRecord(e[7], c->s_near));
+    FMM_CUDA(cudaEventRecord(e[1], s));
+    launch_p2m(c, s);
+    FMM_CUDA(cudaEventRecord(e[2], s));
+    for (int v = leaf - 1; v >= 2; --v) launch_m2m(c, v, s);
+    FMM_CUDA(cudaEventRecord(e[3], s));
+    for (int v = 2; v <= leaf; ++v) launch_m2l(c, v, s);
+    FMM_CUDA(cudaEventRecord(e[4], s));
+    for (int v = 2; v < leaf; ++v) launch_l2l(c, v, s);
+    FMM_CUDA(cudaEventRecord(e[5], s));
+    launch_l2p(c, s);
+    FMM_CUDA(cudaEventRecord(e[8], s));
+    FMM_CUDA(cudaEventRecord(c->ev_join, c->s_near));
+    FMM_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+    FMM_CUDA(cudaEventRecord(e[9], s));
+    launch_gather(c, s);
+    FMM_CUDA(cudaEventRecord(e[10], s));
+    c->out_valid = true;
+  });
+}
+
+int fmmgpu_synchronize(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    FMM_CUDA(cudaStreamSynchronize(c->s_near));
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+int fmmgpu_timings(const fmmgpu_ctx* cc, double* ms) {
+  auto* c = const_cast<fmmgpu_ctx*>(cc);
+  return guarded(c, [&] {
+    FMM_CUDA(cudaEventSynchronize(c->ev_t[10]));
+    cudaEvent_t* e = c->ev_t;
+    ms[FMMGPU_P2M] = elapsed(e[1], e[2]);
+    ms[FMMGPU_M2M] = elapsed(e[2], e[3]);
+    ms[FMMGPU_M2L] = elapsed(e[3], e[4]);
+    ms[FMMGPU_L2L] = elapsed(e[4], e[5]);
+    ms[FMMGPU_L2P] = elapsed(e[5], e[8]);
+    ms[FMMGPU_P2P] = elapsed(e[6], e[7]);
+    ms[FMMGPU_P2PREDUCE] = elapsed(e[9], e[10]);
+    ms[7] = elapsed(e[0], e[10]);
+    ms[8] = c->timings[8];
+    ms[9] = c->timings[9];
+  });
+}
+
+uint64_t fmmgpu_last_launch_count(const fmmgpu_ctx* c) { return c ? c->launches : 0; }
+
+int fmmgpu_time_evaluations(fmmgpu_ctx* c, int steps, double* total_ms, double* kind_ms10, uint64_t* launches) {
+  return guarded(c, [&] {
+    need_tree(c);
+    if (steps < 1) throw Error(FMMGPU_INVALID_ARGUMENT, "steps must be >= 1");
+    double acc[10] = {};
+    uint64_t nl = 0;
+    FMM_CUDA(cudaStreamSynchronize(c->s_near));
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+    FMM_CUDA(cudaEventRecord(c->ev_t[12], c->s_far));
+    for (int i = 0; i < steps; ++i) {
+      if (fmmgpu_evaluate(c) != FMMGPU_OK) throw Error(FMMGPU_RUNTIME_ERROR, c->err);
+      nl += c->launches;
+      double ms[10];
+      if (fmmgpu_timings(c, ms) != FMMGPU_OK) throw Error(FMMGPU_RUNTIME_ERROR, c->err);
+      for (int k = 0; k < 8; ++k) acc[k] += ms[k];
+    }
+    FMM_CUDA(cudaEventRecord(c->ev_t[13], c->s_far));
+    FMM_CUDA(cudaEventSynchronize(c->ev_t[13]));
+    if (total_ms) *total_ms = elapsed(c->ev_t[12], c->ev_t[13]);
+    if (kind_ms10) {
+      for (int k = 0; k < 8; ++k) kind_ms10[k] = acc[k];
+      kind_ms10[8] = c->timings[8];
+      kind_ms10[9] = c->timings[9];
+    }
+    if (launches) *launches = nl;
+  });
+}
+
+int fmmgpu_download_fields(fmmgpu_ctx* c, double* pot, double* fx, double* fy, double* fz, int dst_on_device) {
+  return guarded(c, [&] {
+    need_tree(c);
+    if (!c->out_valid) {  // per-operator use: gather near + far now
+      FMM_CUDA(cudaEventRecord(c->ev_join, c->s_near));
+      FMM_CUDA(cudaStreamWaitEvent(c->s_far, c->ev_join, 0));
+      launch_gather(c, c->s_far);
+      c->out_valid = true;
+    }
+    const cudaMemcpyKind k = dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    double* dst[4] = {pot, fx, fy, fz};
+    for (int i = 0; i < 4; ++i)
+      if (dst[i]) FMM_CUDA(cudaMemcpyAsync(dst[i], c->d_out + i * c->n, 8 * c->n, k, c->s_far));
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+int fmmgpu_run(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, int group, double* pot, double* fx,
+               double* fy, double* fz) {
+  int rc = fmmgpu_build_tree(c, xyzw, n, 0, height, group, nullptr);
+  if (rc) return rc;
+  rc = fmmgpu_evaluate(c);
+  if (rc) return rc;
+  return fmmgpu_download_fields(c, pot, fx, fy, fz, 0);
+}
+
+int fmmgpu_tree_info(const fmmgpu_ctx* c, uint64_t* n, int* height, int* group, double* root4) {
+  if (!c || !c->have_tree) return FMMGPU_LOGIC_ERROR;
+  if (n) *n = c->n;
+  if (height) *height = c->height;
+  if (group) *group = c->group;
+  if (root4) std::copy(c->root, c->root + 4, root4);
+  return FMMGPU_OK;
+}
+
+uint64_t fmmgpu_level_cells(const fmmgpu_ctx* c, int v) {
+  if (!c || !c->have_tree || v < 0 || v >= c->height) return 0;
+  return c->lv[v].n;
+}
+
+int fmmgpu_download_level(fmmgpu_ctx* c, int v, void* cells32, uint32_t* bo) {
+  return guarded(c, [&] {
+    need_level(c, v, 0, c->height - 1, "download_level");
+    const Level& L = c->lv[v];
+    if (cells32 && L.n) {
+      uint32_t* d = static_cast<uint32_t*>(scratch(c, 32ull * L.n));
+      k_cells_aos<<<(L.n + 255) / 256, 256, 0, c->s_far>>>(L.code, L.first_particle, L.particle_count, L.parent,
+                                                          L.first_child, L.child_count, L.n, d);
+      FMM_CUDA(cudaGetLastError());
+      FMM_CUDA(cudaMemcpyAsync(cells32, d, 32ull * L.n, cudaMemcpyDeviceToHost, c->s_far));
+    }
+    if (bo) std::copy(L.block_offsets.begin(), L.block_offsets.end(), bo);
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+int fmmgpu_download_particles(fmmgpu_ctx* c, double* x, double* y, double* z, double* w, uint32_t* id) {
+  return guarded(c, [&] {
+    need_tree(c);
+    double* d = static_cast<double*>(scratch(c, 32 * c->n));
+    k_soa<<<(c->n + 255) / 256, 256, 0, c->s_far>>>(c->d_pw, c->n, d, d + c->n, d + 2 * c->n, d + 3 * c->n);
+    FMM_CUDA(cudaGetLastError());
+    double* dst[4] = {x, y, z, w};
+    for (int i = 0; i < 4; ++i)
+      if (dst[i]) FMM_CUDA(cudaMemcpyAsync(dst[i], d + i * c->n, 8 * c->n, cudaMemcpyDeviceToHost, c->s_far));
+    if (id) FMM_CUDA(cudaMemcpyAsync(id, c->d_id, 4 * c->n, cudaMemcpyDeviceToHost, c->s_far));
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+int fmmgpu_download_sorted_fields(fmmgpu_ctx* c, double* pot, double* fx, double* fy, double* fz) {
+  return guarded(c, [&] {
+    need_tree(c);
+    FMM_CUDA(cudaStreamSynchronize(c->s_near));
+    double* d = static_cast<double*>(scratch(c, 32 * c->n));
+    k_sum4<<<(4 * c->n + 255) / 256, 256, 0, c->s_far>>>(c->d_far, c->d_near, 4 * c->n, d);
+    FMM_CUDA(cudaGetLastError());
+    double* dst[4] = {pot, fx, fy, fz};
+    for (int i = 0; i < 4; ++i)
+      if (dst[i]) FMM_CUDA(cudaMemcpyAsync(dst[i], d + i * c->n, 8 * c->n, cudaMemcpyDeviceToHost, c->s_far));
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+int fmmgpu_download_expansion(fmmgpu_ctx* c, int v, int which, double* out) {
+  return guarded(c, [&] {
+    need_level(c, v, 0, c->height - 1, "download_expansion");
+    if (which < 0 || which > 2) throw Error(FMMGPU_INVALID_ARGUMENT, "which must be 0, 1 or 2");
+    const Level& L = c->lv[v];
+    if (L.n == 0) return;
+    const double* src = which == 0 ? L.multipole : which == 1 ? L.local_own : L.local_down;
+    double* d = static_cast<double*>(scratch(c, 8ull * L.n * c->l3));
+    const uint64_t tot = uint64_t(L.n) * c->l3;
+    FMM_CUDA(cudaStreamSynchronize(c->s_near));
+    k_pad_copy<<<(tot + 255) / 256, 256, 0, c->s_far>>>(src, c->l3, c->ldE, L.n, d, 0);
+    FMM_CUDA(cudaGetLastError());
+    FMM_CUDA(cudaMemcpyAsync(out, d, 8 * tot, cudaMemcpyDeviceToHost, c->s_far));
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+int fmmgpu_upload_expansion(fmmgpu_ctx* c, int v, int which, const double* in) {
+  return guarded(c, [&] {
+    need_level(c, v, 0, c->height - 1, "upload_expansion");
+    if (which < 0 || which > 2) throw Error(FMMGPU_INVALID_ARGUMENT, "which must be 0, 1 or 2");
+    const Level& L = c->lv[v];
+    if (L.n == 0) return;
+    double* dst = which == 0 ? L.multipole : which == 1 ? L.local_own : L.local_down;
+    double* d = static_cast<double*>(scratch(c, 8ull * L.n * c->l3));
+    const uint64_t tot = uint64_t(L.n) * c->l3;
+    FMM_CUDA(cudaMemcpyAsync(d, in, 8 * tot, cudaMemcpyHostToDevice, c->s_far));
+    k_pad_copy<<<(tot + 255) / 256, 256, 0, c->s_far>>>(d, c->l3, c->ldE, L.n, dst, 1);
+    FMM_CUDA(cudaGetLastError());
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+uint64_t fmmgpu_near_entries(const fmmgpu_ctx* c) { return (c && c->have_lists) ? c->near_entries : 0; }
+
+int fmmgpu_download_near(fmmgpu_ctx* c, uint32_t* off, uint32_t* cells, uint64_t* total) {
+  return guarded(c, [&] {
+    if (!c->have_lists) throw Error(FMMGPU_LOGIC_ERROR, "no lists: call fmmgpu_build_lists first");
+    const Level& L = c->lv[c->height - 1];
+    if (off) FMM_CUDA(cudaMemcpyAsync(off, c->d_near_off, 4ull * (L.n + 1), cudaMemcpyDeviceToHost, c->s_far));
+    if (cells && c->near_entries)
+      FMM_CUDA(cudaMemcpyAsync(cells, c->d_near_cells, 4ull * c->near_entries, cudaMemcpyDeviceToHost, c->s_far));
+    if (total) *total = c->near_directional;
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+uint64_t fmmgpu_far_pairs(const fmmgpu_ctx* c, int v) {
+  if (!c || !c->have_lists || v < 2 || v >= c->height) return 0;
+  return c->lv[v].far_pairs;
+}
+
+int fmmgpu_download_far(fmmgpu_ctx* c, int v, uint32_t* target, uint32_t* source, uint16_t* vec, uint64_t* goff) {
+  return guarded(c, [&] {
+    if (!c->have_lists) throw Error(FMMGPU_LOGIC_ERROR, "no lists: call fmmgpu_build_lists first");
+    need_level(c, v, 2, c->height - 1, "download_far");
+    const Level& L = c->lv[v];
+    const uint64_t np = L.far_pairs;
+    if (np) {
+      if (target) FMM_CUDA(cudaMemcpyAsync(target, L.far_target, 4 * np, cudaMemcpyDeviceToHost, c->s_far));
+      if (source) FMM_CUDA(cudaMemcpyAsync(source, L.far_source, 4 * np, cudaMemcpyDeviceToHost, c->s_far));
+      if (vec) FMM_CUDA(cudaMemcpyAsync(vec, L.far_vec, 2 * np, cudaMemcpyDeviceToHost, c->s_far));
+    }
+    const uint64_t ng = (L.block_offsets.size() - 1) * 16 + 1;
+    if (goff) FMM_CUDA(cudaMemcpyAsync(goff, L.far_group_off, 8 * ng, cudaMemcpyDeviceToHost, c->s_far));
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+int fmmgpu_ledger(fmmgpu_ctx* c, uint64_t* flops7, uint64_t* near_dir, uint64_t* m2l_pairs) {
+  return guarded(c, [&] {
+    if (!c->have_lists) lists_build(c);
+    const uint64_t l = c->order, n = c->n;
+    const int leaf = c->height - 1;
+    uint64_t transfers = 0, m2l = 0, pairs = 0;
+    for (int v = 2; v < leaf; ++v) transfers += c->lv[v + 1].n;  // taskflow.cpp:131-133
+    for (int v = 2; v <= leaf; ++v) {
+      const Level& L = c->lv[v];
+      const uint64_t ng = (L.block_offsets.size() - 1) * 16;
+      std::vector<uint64_t> go(ng + 1);
+      FMM_CUDA(cudaMemcpy(go.data(), L.far_group_off, 8 * (ng + 1), cudaMemcpyDeviceToHost));
+      for (uint64_t g = 0; g < ng; ++g) {
+        const uint64_t cnt = go[g + 1] - go[g];
+        const uint64_t r = c->m2l.rank[g % 16];
+        m2l += cnt * (4 * l * l * l * r + r * r);  // bench.cpp:119-122
+        pairs += cnt;
+      }
+    }
+    if (flops7) {
+      flops7[0] = n * (4 * l * l * l + 15 * l);
+      flops7[1] = transfers * 6 * l * l * l * l;
+      flops7[2] = m2l;
+      flops7[3] = transfers * 6 * l * l * l * l;
+      flops7[4] = n * (16 * l * l * l + 30 * l);
+      flops7[5] = c->near_directional * 15;
+      flops7[6] = 0;
+    }
+    if (near_dir) *near_dir = c->near_directional;
+    if (m2l_pairs) *m2l_pairs = pairs;
+  });
+}
+
+void fmmgpu_generate_particles(uint64_t n, int dist, uint64_t seed, double* xyzw) {
+  // bench.cpp:19-61
+  std::mt19937_64 rng(seed);
+  auto u01 = [&] { return static_cast<double>(rng() >> 11) * 0x1.0p-53; };
+  if (dist == 0) {
+    for (uint64_t i = 0; i < n; ++i) {
+      const double x = u01(), y = u01(), z = u01();
+      xyzw[4 * i] = x;
+      xyzw[4 * i + 1] = y;
+      xyzw[4 * i + 2] = z;
+      xyzw[4 * i + 3] = 1.0;
+    }
+    return;
+  }
+  constexpr double two_pi = 6.283185307179586476925286766559;
+  auto normal_pair = [&](double& a, double& b) {
+    const double u1 = static_cast<double>((rng() >> 11) + 1) * 0x1.0p-53;
+    const double u2 = u01();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    a = r * std::cos(two_pi * u2);
+    b = r * std::sin(two_pi * u2);
+  };
+  for (uint64_t i = 0; i < n; ++i) {
+    double gx, gy, gz, spare, norm = 0;
+    do {
+      normal_pair(gx, gy);
+      normal_pair(gz, spare);
+      norm = std::sqrt(gx * gx + gy * gy + gz * gz);
+    } while (norm < 1e-12);
+    xyzw[4 * i] = 0.5 + 0.5 * gx / norm;
+    xyzw[4 * i + 1] = 0.5 + 0.5 * gy / norm;
+    xyzw[4 * i + 2] = 0.5 + 0.5 * gz / norm;
+    xyzw[4 * i + 3] = 1.0;
+  }
+}
+
+}  // extern "C"

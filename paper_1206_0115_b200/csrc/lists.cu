@@ -1,0 +1,257 @@
+// Interaction lists on the device, bit-exact with the reference plan:
+//   near CSR   = build_near_field_plan (direct.cpp:22-61) over near_field_list
+//                (geometry.cpp:222-242): per leaf cell, existing cells at Chebyshev
+//                distance 1, ascending index;
+//   far pairs  = build_interaction_plan (taskflow.cpp:67-105) over far_field_list
+//                (geometry.cpp:244-280): per level, grouped by (block*16+canonical),
+//                within a group target ascending then source ascending.
+// Both are count -> exclusive scan -> fill passes; the fill writes each cell's
+// entries straight into their final CSR slot (no sort of the pair array).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace fmmgpu {
+
+namespace {
+
+inline unsigned blocks(uint64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+template <typename T>
+T* dalloc(size_t count, cudaStream_t s) {
+  void* p = nullptr;
+  FMM_CUDA(cudaMallocAsync(&p, (count ? count : 1) * sizeof(T), s));
+  return static_cast<T*>(p);
+}
+
+// ---- near field -----------------------------------------------------------------
+__device__ int near_cells_of(const LevelView& L, uint64_t code, uint32_t out[26]) {
+  int ijk[3];
+  demorton(code, ijk);
+  int m = 0;
+  for (int di = -1; di <= 1; ++di)
+    for (int dj = -1; dj <= 1; ++dj)
+      for (int dk = -1; dk <= 1; ++dk) {
+        if (!di && !dj && !dk) continue;
+        const uint32_t f = find_ijk(L, ijk[0] + di, ijk[1] + dj, ijk[2] + dk);
+        if (f != NPOS) out[m++] = f;
+      }
+  // ascending (direct.cpp:22-34 via std::sort in near_field_list)
+  for (int a = 1; a < m; ++a) {
+    const uint32_t x = out[a];
+    int b = a - 1;
+    while (b >= 0 && out[b] > x) { out[b + 1] = out[b]; --b; }
+    out[b + 1] = x;
+  }
+  return m;
+}
+
+__global__ void k_near_count(LevelView L, const uint32_t* __restrict__ pcount, uint32_t* __restrict__ cnt,
+                             unsigned long long* __restrict__ work) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= L.n) return;
+  uint32_t nb[26];
+  const int m = near_cells_of(L, L.code[c], nb);
+  cnt[c] = static_cast<uint32_t>(m);
+  // count_interactions near term (taskflow.cpp:116-122): nc(nc-1) + sum nc*n_nbr
+  const unsigned long long nc = pcount[c];
+  unsigned long long w = nc * (nc - 1);
+  for (int a = 0; a < m; ++a) w += nc * pcount[nb[a]];
+  work[c] = w;
+}
+
+__global__ void k_near_fill(LevelView L, const uint32_t* __restrict__ off, uint32_t* __restrict__ cells) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= L.n) return;
+  uint32_t nb[26];
+  const int m = near_cells_of(L, L.code[c], nb);
+  for (int a = 0; a < m; ++a) cells[off[c] + a] = nb[a];
+}
+
+// ---- far field ------------------------------------------------------------------
+// Sorted parent-neighbour indices; their children are disjoint ascending index
+// ranges, so visiting them in this order yields sources in ascending order
+// (the std::sort by source of geometry.cpp:277-278).
+__device__ int parent_neighbours(const LevelView& P, uint64_t pcode, uint32_t out[27]) {
+  int ijk[3];
+  demorton(pcode, ijk);
+  int m = 0;
+  for (int di = -1; di <= 1; ++di)
+    for (int dj = -1; dj <= 1; ++dj)
+      for (int dk = -1; dk <= 1; ++dk) {
+        const uint32_t f = find_ijk(P, ijk[0] + di, ijk[1] + dj, ijk[2] + dk);
+        if (f != NPOS) out[m++] = f;
+      }
+  for (int a = 1; a < m; ++a) {
+    const uint32_t x = out[a];
+    int b = a - 1;
+    while (b >= 0 && out[b] > x) { out[b + 1] = out[b]; --b; }
+    out[b + 1] = x;
+  }
+  return m;
+}
+
+struct FarArgs {
+  LevelView L, P;
+  const uint32_t* parent;
+  const uint32_t* p_first_child;
+  const uint32_t* p_child_count;
+  const int* canon;  // 343
+  uint32_t group;
+};
+
+template <bool FILL>
+__global__ void k_far(FarArgs a, uint32_t* __restrict__ cnt, const unsigned long long* __restrict__ pos,
+                      uint32_t* __restrict__ tgt, uint32_t* __restrict__ src, uint16_t* __restrict__ vec) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.L.n) return;
+  const uint64_t code = a.L.code[c];
+  int ijk[3];
+  demorton(code, ijk);
+  uint32_t pn[27];
+  const int m = parent_neighbours(a.P, code >> 3, pn);
+  const uint32_t b = c / a.group, cl = c % a.group;
+  uint32_t k16[16];
+  for (int q = 0; q < 16; ++q) k16[q] = 0;
+  for (int t = 0; t < m; ++t) {
+    const uint32_t np = pn[t];
+    const uint32_t f = a.p_first_child[np], e = f + a.p_child_count[np];
+    for (uint32_t ch = f; ch < e; ++ch) {
+      int cijk[3];
+      demorton(a.L.code[ch], cijk);
+      const int ti = cijk[0] - ijk[0], tj = cijk[1] - ijk[1], tk = cijk[2] - ijk[2];
+      const int d = max(abs(ti), max(abs(tj), abs(tk)));
+      if (d <= 1) continue;
+      const int slot = (ti + 3) * 49 + (tj + 3) * 7 + (tk + 3);
+      const int q = a.canon[slot];
+      if (FILL) {
+        const unsigned long long p = pos[(size_t(b) * 16 + q) * a.group + cl] + k16[q];
+        tgt[p] = c;
+        src[p] = ch;
+        vec[p] = static_cast<uint16_t>(slot);
+      }
+      ++k16[q];
+    }
+  }
+  if (!FILL)
+    for (int q = 0; q < 16; ++q) cnt[(size_t(b) * 16 + q) * a.group + cl] = k16[q];
+}
+
+__global__ void k_group_off(const unsigned long long* __restrict__ pos, uint64_t ngroups, uint32_t group,
+                            uint64_t total, uint64_t* __restrict__ goff) {
+  const uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (g < ngroups) goff[g] = pos[g * group];
+  if (g == ngroups) goff[g] = total;
+}
+
+}  // namespace
+
+void lists_free(fmmgpu_ctx* c) {
+  cudaStream_t s = c->s_far;
+  if (c->d_near_off) cudaFreeAsync(c->d_near_off, s);
+  if (c->d_near_cells) cudaFreeAsync(c->d_near_cells, s);
+  c->d_near_off = nullptr;
+  c->d_near_cells = nullptr;
+  for (auto& L : c->lv) {
+    if (L.far_target) cudaFreeAsync(L.far_target, s);
+    if (L.far_source) cudaFreeAsync(L.far_source, s);
+    if (L.far_vec) cudaFreeAsync(L.far_vec, s);
+    if (L.far_group_off) cudaFreeAsync(L.far_group_off, s);
+    L.far_target = L.far_source = nullptr;
+    L.far_vec = nullptr;
+    L.far_group_off = nullptr;
+    L.far_pairs = 0;
+  }
+  c->have_lists = false;
+}
+
+uint64_t near_directional_count(fmmgpu_ctx* c) {
+  cudaStream_t s = c->s_far;
+  const int leaf = c->height - 1;
+  const Level& L = c->lv[leaf];
+  uint32_t* cnt = dalloc<uint32_t>(L.n, s);
+  unsigned long long* work = dalloc<unsigned long long>(L.n + 1, s);
+  k_near_count<<<blocks(L.n, 128), 128, 0, s>>>(L.view(leaf), L.particle_count, cnt, work);
+  FMM_CUDA(cudaGetLastError());
+  size_t tb = 0;
+  FMM_CUDA(cub::DeviceReduce::Sum(nullptr, tb, work, work + L.n, static_cast<int>(L.n), s));
+  FMM_CUDA(cub::DeviceReduce::Sum(scratch(c, tb), tb, work, work + L.n, static_cast<int>(L.n), s));
+  unsigned long long total = 0;
+  FMM_CUDA(cudaMemcpyAsync(&total, work + L.n, 8, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(cnt, s);
+  cudaFreeAsync(work, s);
+  return total;
+}
+
+void lists_build(fmmgpu_ctx* c) {
+  if (!c->have_tree) throw Error(FMMGPU_LOGIC_ERROR, "build_lists: no tree");
+  lists_free(c);
+  cudaStream_t s = c->s_far;
+  const int leaf = c->height - 1;
+  // near CSR
+  {
+    const Level& L = c->lv[leaf];
+    uint32_t* cnt = dalloc<uint32_t>(L.n + 1, s);
+    unsigned long long* work = dalloc<unsigned long long>(L.n + 1, s);
+    FMM_CUDA(cudaMemsetAsync(cnt + L.n, 0, 4, s));
+    k_near_count<<<blocks(L.n, 128), 128, 0, s>>>(L.view(leaf), L.particle_count, cnt, work);
+    FMM_CUDA(cudaGetLastError());
+    c->d_near_off = dalloc<uint32_t>(L.n + 1, s);
+    size_t tb = 0;
+    FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, c->d_near_off, static_cast<int>(L.n + 1), s));
+    FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, cnt, c->d_near_off, static_cast<int>(L.n + 1), s));
+    FMM_CUDA(cub::DeviceReduce::Sum(nullptr, tb, work, work + L.n, static_cast<int>(L.n), s));
+    FMM_CUDA(cub::DeviceReduce::Sum(scratch(c, tb), tb, work, work + L.n, static_cast<int>(L.n), s));
+    uint32_t entries = 0;
+    unsigned long long total = 0;
+    FMM_CUDA(cudaMemcpyAsync(&entries, c->d_near_off + L.n, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaMemcpyAsync(&total, work + L.n, 8, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    c->near_entries = entries;
+    c->near_directional = total;
+    c->d_near_cells = dalloc<uint32_t>(entries, s);
+    k_near_fill<<<blocks(L.n, 128), 128, 0, s>>>(L.view(leaf), c->d_near_off, c->d_near_cells);
+    FMM_CUDA(cudaGetLastError());
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(work, s);
+  }
+  // far pairs per level
+  for (int v = 2; v <= leaf; ++v) {
+    Level& L = c->lv[v];
+    const Level& P = c->lv[v - 1];
+    const uint64_t nb = L.block_offsets.size() - 1;
+    const uint64_t ng = nb * 16;
+    const uint64_t slots = ng * c->group;
+    uint32_t* cnt = dalloc<uint32_t>(slots, s);
+    unsigned long long* pos = dalloc<unsigned long long>(slots + 1, s);
+    FMM_CUDA(cudaMemsetAsync(cnt, 0, 4 * slots, s));
+    FarArgs a{L.view(v), P.view(v - 1), L.parent, P.first_child, P.child_count, c->d_canon,
+              static_cast<uint32_t>(c->group)};
+    k_far<false><<<blocks(L.n, 128), 128, 0, s>>>(a, cnt, nullptr, nullptr, nullptr, nullptr);
+    FMM_CUDA(cudaGetLastError());
+    size_t tb = 0;
+    FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, pos, static_cast<int>(slots), s));
+    FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, cnt, pos, static_cast<int>(slots), s));
+    unsigned long long last_pos = 0;
+    uint32_t last_cnt = 0;
+    FMM_CUDA(cudaMemcpyAsync(&last_pos, pos + slots - 1, 8, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaMemcpyAsync(&last_cnt, cnt + slots - 1, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    const uint64_t total = last_pos + last_cnt;
+    L.far_pairs = total;
+    L.far_target = dalloc<uint32_t>(total, s);
+    L.far_source = dalloc<uint32_t>(total, s);
+    L.far_vec = dalloc<uint16_t>(total, s);
+    L.far_group_off = dalloc<uint64_t>(ng + 1, s);
+    k_group_off<<<blocks(ng + 1, 256), 256, 0, s>>>(pos, ng, c->group, total, L.far_group_off);
+    k_far<true><<<blocks(L.n, 128), 128, 0, s>>>(a, nullptr, pos, L.far_target, L.far_source, L.far_vec);
+    FMM_CUDA(cudaGetLastError());
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(pos, s);
+  }
+  FMM_CUDA(cudaStreamSynchronize(s));
+  c->have_lists = true;
+}
+
+}  // namespace fmmgpu

@@ -1,0 +1,537 @@
+// Compressed M2L on the device (M2LOperatorSet, m2l.cpp:12-204; bench.cpp:288-299).
+//
+// Precompute (once per context): the 16 canonical operators are assembled at unit
+// width (m2l.cpp:90-111) and compressed with a truncated SVD on the device
+// (cuSOLVER dgesvd, rank rule of m2l.cpp:116-122), or loaded from the reference's
+// binary cache (m2l.cpp:247-288). Each admissible transfer vector v (316) gets the
+// permuted factors of its class: since the reference applies
+//     local[t][m] += scale * sum_k U[p_v[m]][k] * sigma_k * sum_n V[p_v[n]][k] * W[s][n]
+// (gather z[p[n]] = W[n], Y = U sigma V^T z, scatter out[m] += scale y[p[m]],
+// m2l.cpp:189-203), the per-vector operator is M2_v M1_v with
+//     M1_v[k][n] = sigma_k V[p_v[n]][k]   (r x l^3)
+//     M2_v[m][k] = U[p_v[m]][k]           (l^3 x r).
+//
+// Evaluation per level as two dense FP64 GEMMs per parity class (DESIGN.md
+// "M2L as two GEMMs"). The admissible vectors of a target depend only on the parity
+// of its grid coordinates (an axis component of +3 needs an even target, -3 an odd
+// one), so for each of the 8 parity classes:
+//   phase A  Y = M1_p (R x l^3) * W (l^3 x sources of parity p), M1_p the stack of
+//            M1_v over the 189 vectors admissible from a parity-p source; the
+//            epilogue scatters block v of source s to target s - v (if it exists)
+//            into Yt[t] (target-side stacking order);
+//   phase B  local_own[t] += scale * M2_q (l^3 x R) * Yt[t] for targets of parity q,
+//            with the B operand zero-filled where the source t + v does not exist.
+// Same arithmetic as the reference (4 l^3 r per pair), on DMMA (mma.sync
+// m8n8k4 f64, the B200 FP64 tensor path: 37.2 TF/s measured, profiles/r01_fp64_peaks.txt).
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace fmmgpu {
+
+// ------------------------------------------------------------------ symmetry tables
+// cube_symmetries (m2l.cpp:12-25): perm-major, sign bit of axis a = bit (2-a).
+int canonicalize_host(const int v[3], int perm_out[3], int sign_out[3]) {
+  static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  const int d = std::max({std::abs(v[0]), std::abs(v[1]), std::abs(v[2])});
+  if (d < 2 || d > 3) throw Error(FMMGPU_INVALID_ARGUMENT, "canonicalize_m2l_vector: max-norm must be 2 or 3");
+  for (const auto& p : perms)
+    for (int bits = 0; bits < 8; ++bits) {
+      int sign[3], u[3];
+      for (int a = 0; a < 3; ++a) {
+        sign[a] = (bits >> (2 - a)) & 1 ? -1 : 1;
+        u[a] = sign[a] * v[p[a]];
+      }
+      if (!(u[0] >= u[1] && u[1] >= u[2] && u[2] >= 0 && u[0] >= 2 && u[0] <= 3)) continue;
+      // canonical list (m2l.cpp:45-55): i = 2..3, j = 0..i, k = 0..j
+      int idx = 0;
+      for (int i = 2; i <= 3; ++i)
+        for (int j = 0; j <= i; ++j)
+          for (int k = 0; k <= j; ++k, ++idx)
+            if (u[0] == i && u[1] == j && u[2] == k) {
+              for (int a = 0; a < 3; ++a) {
+                perm_out[a] = p[a];
+                sign_out[a] = sign[a];
+              }
+              return idx;
+            }
+    }
+  throw Error(FMMGPU_LOGIC_ERROR, "canonicalize_m2l_vector: no symmetry found");
+}
+
+namespace {
+
+void canonical_vector(int c, int out[3]) {
+  int idx = 0;
+  for (int i = 2; i <= 3; ++i)
+    for (int j = 0; j <= i; ++j)
+      for (int k = 0; k <= j; ++k, ++idx)
+        if (idx == c) { out[0] = i; out[1] = j; out[2] = k; return; }
+}
+
+// grid_permutation (m2l.cpp:72-88): p[flat(m)] = flat(g m)
+std::vector<uint32_t> grid_perm(const int perm[3], const int sign[3], int l) {
+  std::vector<uint32_t> p(size_t(l) * l * l);
+  int m[3];
+  for (m[0] = 0; m[0] < l; ++m[0])
+    for (m[1] = 0; m[1] < l; ++m[1])
+      for (m[2] = 0; m[2] < l; ++m[2]) {
+        uint32_t flat = 0;
+        for (int a = 0; a < 3; ++a) {
+          const int cc = sign[a] > 0 ? m[perm[a]] : l - 1 - m[perm[a]];
+          flat = flat * l + cc;
+        }
+        p[(m[0] * l + m[1]) * l + m[2]] = flat;
+      }
+  return p;
+}
+
+void slot_vec(int slot, int v[3]) {
+  v[0] = slot / 49 - 3;
+  v[1] = (slot / 7) % 7 - 3;
+  v[2] = slot % 7 - 3;
+}
+
+// admissible for a target of parity q (bit 2 = i, bit 1 = j, bit 0 = k, the Morton
+// octant): max-norm 2..3 and +3 needs an even, -3 an odd target coordinate
+// (parents adjacent, geometry.cpp:255-275).
+bool admissible_for_target(const int v[3], int q) {
+  if (std::max({std::abs(v[0]), std::abs(v[1]), std::abs(v[2])}) < 2) return false;
+  for (int a = 0; a < 3; ++a) {
+    const int qa = (q >> (2 - a)) & 1;
+    if (v[a] == 3 && qa != 0) return false;
+    if (v[a] == -3 && qa != 1) return false;
+  }
+  return true;
+}
+int vec_parity(const int v[3]) { return ((v[0] & 1) << 2) | ((v[1] & 1) << 1) | (v[2] & 1); }
+
+#define CUSOLVER_CHECK(x)                                                                     \
+  do {                                                                                        \
+    cusolverStatus_t st_ = (x);                                                               \
+    if (st_ != CUSOLVER_STATUS_SUCCESS)                                                       \
+      throw Error(FMMGPU_RUNTIME_ERROR, "cuSOLVER error " + std::to_string(int(st_)) + " at " + \
+                                            std::to_string(__LINE__));                        \
+  } while (0)
+
+// assemble_m2l (m2l.cpp:90-111) at unit width + truncated SVD on the device
+void compute_factors(fmmgpu_ctx* c) {
+  const int l = c->order, n3 = c->l3;
+  std::vector<double> nodes(3 * n3);
+  for (int a = 0, idx = 0; a < l; ++a)
+    for (int b = 0; b < l; ++b)
+      for (int cc = 0; cc < l; ++cc, ++idx) {
+        nodes[3 * idx] = c->h_roots[a] * 0.5 * 1.0;
+        nodes[3 * idx + 1] = c->h_roots[b] * 0.5 * 1.0;
+        nodes[3 * idx + 2] = c->h_roots[cc] * 0.5 * 1.0;
+      }
+  cusolverDnHandle_t h;
+  CUSOLVER_CHECK(cusolverDnCreate(&h));
+  double *dA, *dS, *dU, *dVT, *dWork, *dRW;
+  int* dInfo;
+  int lwork = 0;
+  FMM_CUDA(cudaMalloc(&dA, sizeof(double) * n3 * n3));
+  FMM_CUDA(cudaMalloc(&dU, sizeof(double) * n3 * n3));
+  FMM_CUDA(cudaMalloc(&dVT, sizeof(double) * n3 * n3));
+  FMM_CUDA(cudaMalloc(&dS, sizeof(double) * n3));
+  FMM_CUDA(cudaMalloc(&dRW, sizeof(double) * n3));
+  FMM_CUDA(cudaMalloc(&dInfo, sizeof(int)));
+  CUSOLVER_CHECK(cusolverDnDgesvd_bufferSize(h, n3, n3, &lwork));
+  FMM_CUDA(cudaMalloc(&dWork, sizeof(double) * lwork));
+  std::vector<double> K(size_t(n3) * n3), U(size_t(n3) * n3), VT(size_t(n3) * n3), S(n3);
+  for (int cl = 0; cl < 16; ++cl) {
+    int v[3];
+    canonical_vector(cl, v);
+    for (int m = 0; m < n3; ++m)
+      for (int n = 0; n < n3; ++n) {
+        const double dx = nodes[3 * m] - v[0] * 1.0 - nodes[3 * n];
+        const double dy = nodes[3 * m + 1] - v[1] * 1.0 - nodes[3 * n + 1];
+        const double dz = nodes[3 * m + 2] - v[2] * 1.0 - nodes[3 * n + 2];
+        K[size_t(n) * n3 + m] = 1.0 / std::sqrt(dx * dx + dy * dy + dz * dz);  // column-major
+      }
+    FMM_CUDA(cudaMemcpy(dA, K.data(), sizeof(double) * K.size(), cudaMemcpyHostToDevice));
+    CUSOLVER_CHECK(cusolverDnDgesvd(h, 'S', 'S', n3, n3, dA, n3, dS, dU, n3, dVT, n3, dWork, lwork, dRW, dInfo));
+    int info = 0;
+    FMM_CUDA(cudaMemcpy(&info, dInfo, sizeof(int), cudaMemcpyDeviceToHost));
+    if (info != 0) throw Error(FMMGPU_RUNTIME_ERROR, "cuSOLVER dgesvd did not converge");
+    FMM_CUDA(cudaMemcpy(U.data(), dU, sizeof(double) * U.size(), cudaMemcpyDeviceToHost));
+    FMM_CUDA(cudaMemcpy(VT.data(), dVT, sizeof(double) * VT.size(), cudaMemcpyDeviceToHost));
+    FMM_CUDA(cudaMemcpy(S.data(), dS, sizeof(double) * S.size(), cudaMemcpyDeviceToHost));
+    int r = n3;  // m2l.cpp:116-122
+    for (int i = 1; i < n3; ++i)
+      if (S[i] <= c->eps * S[0]) {
+        r = i;
+        break;
+      }
+    auto& T = c->m2l;
+    T.rank[cl] = r;
+    T.u[cl].assign(size_t(n3) * r, 0.0);
+    T.v[cl].assign(size_t(n3) * r, 0.0);
+    T.sigma[cl].assign(S.begin(), S.begin() + r);
+    for (int i = 0; i < n3; ++i)
+      for (int k = 0; k < r; ++k) {
+        T.u[cl][size_t(i) * r + k] = U[size_t(k) * n3 + i];
+        T.v[cl][size_t(i) * r + k] = VT[size_t(i) * n3 + k];
+      }
+  }
+  cudaFree(dA); cudaFree(dU); cudaFree(dVT); cudaFree(dS); cudaFree(dRW); cudaFree(dInfo); cudaFree(dWork);
+  cusolverDnDestroy(h);
+}
+
+// ------------------------------------------------------------------ GEMM kernels
+constexpr int BK = 16;
+constexpr int SPAD = 20;  // smem row stride in doubles (== 4 mod 16: conflict-free fragments)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp16z(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp8z(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+struct GemmArgs {
+  LevelView lv;
+  const uint32_t* cls_cells;
+  uint32_t cls_off[9];
+  const double* A;        // [8][rows][lda]
+  size_t a_class_stride;  // rows * lda
+  int lda;
+  int K;                  // multiple of BK
+  const double* W;        // phase A: multipoles (ldE)
+  int ldE;
+  double* Yt;             // [cells][ldY]
+  int ldY;
+  const int2* rowA;       // phase A epilogue table [8][rowsA]
+  int rowsA;
+  const int* kslot;       // phase B mask table [8][ldY]
+  double* local;          // phase B output (local_own)
+  int l3;
+  double scale;
+};
+
+template <int BM, int BN, int WM, int WN, int STAGES, bool PHASE_A>
+__global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
+  constexpr int T = WM * WN * 32;
+  constexpr int WTM = BM / WM, WTN = BN / WN;
+  constexpr int MT = WTM / 8, NT = WTN / 8;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                              // [STAGES][BM][SPAD]
+  double* Bs = smem + STAGES * BM * SPAD;         // [STAGES][BN][SPAD]
+  __shared__ uint32_t col_cell[BN];
+  __shared__ int col_ijk[BN][3];
+  __shared__ signed char vtab[343][3];
+
+  const int cls = blockIdx.z;
+  const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
+  const uint32_t n0 = blockIdx.y * BN;
+  if (n0 >= ncls) return;
+  const int m0 = blockIdx.x * BM;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / WN, wn = warp % WN;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  for (int j = tid; j < BN; j += T) {
+    const uint32_t cell = (n0 + j < ncls) ? g.cls_cells[g.cls_off[cls] + n0 + j] : NPOS;
+    col_cell[j] = cell;
+    int ijk[3] = {0, 0, 0};
+    if (cell != NPOS) demorton(g.lv.code[cell], ijk);
+    col_ijk[j][0] = ijk[0];
+    col_ijk[j][1] = ijk[1];
+    col_ijk[j][2] = ijk[2];
+  }
+  for (int s = tid; s < 343; s += T) {
+    vtab[s][0] = static_cast<signed char>(s / 49 - 3);
+    vtab[s][1] = static_cast<signed char>((s / 7) % 7 - 3);
+    vtab[s][2] = static_cast<signed char>(s % 7 - 3);
+  }
+  __syncthreads();
+
+  const double* A = g.A + cls * g.a_class_stride + size_t(m0) * g.lda;
+  const int* kslot = PHASE_A ? nullptr : g.kslot + cls * g.ldY;
+  const int KT = g.K / BK;
+
+  auto load_tile = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * BM * SPAD;
+    double* bs = Bs + stage * BN * SPAD;
+    // A: BM rows x 16 doubles as 16-byte chunks
+    for (int ch = tid; ch < BM * 8; ch += T) {
+      const int r = ch >> 3, q = (ch & 7) * 2;
+      cp16(as + r * SPAD + q, A + size_t(r) * g.lda + k0 + q);
+    }
+    if (PHASE_A) {
+      for (int ch = tid; ch < BN * 8; ch += T) {
+        const int j = ch >> 3, q = (ch & 7) * 2;
+        const uint32_t cell = col_cell[j];
+        const bool ok = cell != NPOS;
+        cp16z(bs + j * SPAD + q, g.W + (ok ? size_t(cell) * g.ldE + k0 + q : 0), ok);
+      }
+    } else {
+      for (int e = tid; e < BN * BK; e += T) {
+        const int j = e / BK, q = e % BK;
+        const uint32_t cell = col_cell[j];
+        const int slot = kslot[k0 + q];
+        bool ok = cell != NPOS && slot >= 0;
+        if (ok) {
+          const uint32_t src = find_ijk(g.lv, col_ijk[j][0] + vtab[slot][0], col_ijk[j][1] + vtab[slot][1],
+                                        col_ijk[j][2] + vtab[slot][2]);
+          ok = src != NPOS;
+        }
+        cp8z(bs + j * SPAD + q, g.Yt + (ok ? size_t(cell) * g.ldY + k0 + q : 0), ok);
+      }
+    }
+  };
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_tile(s, s);
+    cp_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int pf = kt + STAGES - 1;
+    if (pf < KT) load_tile(pf % STAGES, pf);
+    cp_commit();
+    const double* as = As + (kt % STAGES) * BM * SPAD + (wm * WTM + gq) * SPAD + tq;
+    const double* bs = Bs + (kt % STAGES) * BN * SPAD + (wn * WTN + gq) * SPAD + tq;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[MT], b[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[i] = as[i * 8 * SPAD + kk];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = bs[j * 8 * SPAD + kk];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_wait<0>();
+
+  // epilogue: thread holds C[row = gq + 8i][col = 2 tq + e + 8j] of its warp tile
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int row = m0 + wm * WTM + i * 8 + gq;
+    if (PHASE_A) {
+      const int2 info = g.rowA[cls * g.rowsA + row];
+      if (info.x < 0) continue;
+      const int vx = info.x / 49 - 3, vy = (info.x / 7) % 7 - 3, vz = info.x % 7 - 3;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn * WTN + j * 8 + 2 * tq + e;
+          if (col_cell[col] == NPOS) continue;
+          const uint32_t t = find_ijk(g.lv, col_ijk[col][0] - vx, col_ijk[col][1] - vy, col_ijk[col][2] - vz);
+          if (t != NPOS) g.Yt[size_t(t) * g.ldY + info.y] = acc[i][j][e];
+        }
+    } else {
+      if (row >= g.l3) continue;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn * WTN + j * 8 + 2 * tq + e;
+          const uint32_t t = col_cell[col];
+          if (t == NPOS) continue;
+          double* out = g.local + size_t(t) * g.ldE + row;
+          *out += g.scale * acc[i][j][e];
+        }
+    }
+  }
+}
+
+constexpr int A_BM = 64, A_BN = 64, A_WM = 2, A_WN = 2, A_ST = 3;
+constexpr int B_BM = 128, B_BN = 64, B_WM = 4, B_WN = 2, B_ST = 3;
+
+}  // namespace
+
+void m2l_free(fmmgpu_ctx* c) {
+  auto& T = c->m2l;
+  if (T.dM1) cudaFree(T.dM1);
+  if (T.dM2) cudaFree(T.dM2);
+  if (T.dRowA) cudaFree(T.dRowA);
+  if (T.dKslot) cudaFree(T.dKslot);
+  if (T.dYt) cudaFree(T.dYt);
+  T.dM1 = T.dM2 = T.dYt = nullptr;
+  T.dRowA = nullptr;
+  T.dKslot = nullptr;
+  T.yt_cells = 0;
+}
+
+// Builds transport tables and the stacked per-parity operators from T.u/sigma/v.
+void m2l_setup(fmmgpu_ctx* c, bool compute) {
+  auto& T = c->m2l;
+  const int l = c->order, n3 = c->l3;
+  if (compute) compute_factors(c);
+  // transport (m2l.cpp:146-163)
+  std::fill(T.mult, T.mult + 16, 0);
+  for (int s = 0; s < 343; ++s) {
+    T.canonical[s] = -1;
+    T.perm[s].clear();
+    int v[3];
+    slot_vec(s, v);
+    if (std::max({std::abs(v[0]), std::abs(v[1]), std::abs(v[2])}) < 2) continue;
+    int perm[3], sign[3];
+    const int cl = canonicalize_host(v, perm, sign);
+    T.canonical[s] = cl;
+    T.perm[s] = grid_perm(perm, sign, l);
+    ++T.mult[cl];
+  }
+  // target-side stacking per parity q: offB[q][slot]
+  std::vector<int> offB(8 * 343, -1), offA(8 * 343, -1);
+  int R = -1;
+  for (int q = 0; q < 8; ++q) {
+    int off = 0;
+    for (int s = 0; s < 343; ++s) {
+      int v[3];
+      slot_vec(s, v);
+      if (!admissible_for_target(v, q)) continue;
+      offB[q * 343 + s] = off;
+      off += T.rank[T.canonical[s]];
+    }
+    if (R < 0) R = off;
+    if (off != R) throw Error(FMMGPU_LOGIC_ERROR, "M2L stack size differs across parity classes");
+  }
+  // source-side stacking per parity p: vectors with target s - v of parity p ^ par(v)
+  for (int p = 0; p < 8; ++p) {
+    int off = 0;
+    for (int s = 0; s < 343; ++s) {
+      int v[3];
+      slot_vec(s, v);
+      if (!admissible_for_target(v, p ^ vec_parity(v))) continue;
+      offA[p * 343 + s] = off;
+      off += T.rank[T.canonical[s]];
+    }
+    if (off != R) throw Error(FMMGPU_LOGIC_ERROR, "M2L source stack size mismatch");
+  }
+  T.R = R;
+  T.ldY = round_up(R, 16);
+  T.rowsA = round_up(R, A_BM);
+  T.rowsB = round_up(n3, B_BM);
+  std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
+  std::vector<int2> rowA(size_t(8) * T.rowsA, make_int2(-1, 0));
+  std::vector<int> kslot(size_t(8) * T.ldY, -1);
+  for (int p = 0; p < 8; ++p)
+    for (int s = 0; s < 343; ++s) {
+      const int oa = offA[p * 343 + s];
+      if (oa >= 0) {
+        int v[3];
+        slot_vec(s, v);
+        const int cl = T.canonical[s], r = T.rank[cl];
+        const int q = p ^ vec_parity(v);
+        const int ob = offB[q * 343 + s];
+        for (int k = 0; k < r; ++k) {
+          double* row = &M1[(size_t(p) * T.rowsA + oa + k) * c->ldE];
+          for (int n = 0; n < n3; ++n) row[n] = T.sigma[cl][k] * T.v[cl][size_t(T.perm[s][n]) * r + k];
+          rowA[size_t(p) * T.rowsA + oa + k] = make_int2(s, ob + k);
+        }
+      }
+      const int ob = offB[p * 343 + s];  // here p plays the target parity q
+      if (ob >= 0) {
+        const int cl = T.canonical[s], r = T.rank[cl];
+        for (int k = 0; k < r; ++k) {
+          kslot[size_t(p) * T.ldY + ob + k] = s;
+          for (int m = 0; m < n3; ++m)
+            M2[(size_t(p) * T.rowsB + m) * T.ldY + ob + k] = T.u[cl][size_t(T.perm[s][m]) * r + k];
+        }
+      }
+    }
+  m2l_free(c);
+  FMM_CUDA(cudaMalloc(&T.dM1, M1.size() * sizeof(double)));
+  FMM_CUDA(cudaMalloc(&T.dM2, M2.size() * sizeof(double)));
+  FMM_CUDA(cudaMalloc(&T.dRowA, rowA.size() * sizeof(int2)));
+  FMM_CUDA(cudaMalloc(&T.dKslot, kslot.size() * sizeof(int)));
+  FMM_CUDA(cudaMemcpy(T.dM1, M1.data(), M1.size() * sizeof(double), cudaMemcpyHostToDevice));
+  FMM_CUDA(cudaMemcpy(T.dM2, M2.data(), M2.size() * sizeof(double), cudaMemcpyHostToDevice));
+  FMM_CUDA(cudaMemcpy(T.dRowA, rowA.data(), rowA.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  FMM_CUDA(cudaMemcpy(T.dKslot, kslot.data(), kslot.size() * sizeof(int), cudaMemcpyHostToDevice));
+  std::vector<int> canon(T.canonical, T.canonical + 343);
+  if (!c->d_canon) FMM_CUDA(cudaMalloc(&c->d_canon, 343 * sizeof(int)));
+  FMM_CUDA(cudaMemcpy(c->d_canon, canon.data(), 343 * sizeof(int), cudaMemcpyHostToDevice));
+  (void)l;
+}
+
+void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
+  auto& T = c->m2l;
+  const Level& L = c->lv[v];
+  if (L.n == 0) return;
+  if (T.yt_cells < L.n) {
+    if (T.dYt) FMM_CUDA(cudaFree(T.dYt));
+    size_t cells = L.n;
+    for (const auto& x : c->lv) cells = std::max<size_t>(cells, x.n);
+    FMM_CUDA(cudaMalloc(&T.dYt, cells * T.ldY * sizeof(double)));
+    T.yt_cells = cells;
+  }
+  GemmArgs g{};
+  g.lv = L.view(v);
+  g.cls_cells = L.cls_cells;
+  std::copy(L.cls_off, L.cls_off + 9, g.cls_off);
+  g.W = L.multipole;
+  g.ldE = c->ldE;
+  g.Yt = T.dYt;
+  g.ldY = T.ldY;
+  g.rowA = T.dRowA;
+  g.rowsA = T.rowsA;
+  g.kslot = T.dKslot;
+  g.local = L.local_own;
+  g.l3 = c->l3;
+  g.scale = 1.0 / (c->root[3] / static_cast<double>(uint64_t{1} << v));  // bench.cpp:233-234
+  uint32_t maxcls = 0;
+  for (int q = 0; q < 8; ++q) maxcls = std::max(maxcls, L.cls_off[q + 1] - L.cls_off[q]);
+  if (maxcls == 0) return;
+  {
+    g.A = T.dM1;
+    g.lda = c->ldE;
+    g.a_class_stride = size_t(T.rowsA) * c->ldE;
+    g.K = c->ldE;
+    const size_t smem = sizeof(double) * A_ST * (A_BM + A_BN) * SPAD;
+    auto kern = k_m2l_gemm<A_BM, A_BN, A_WM, A_WN, A_ST, true>;
+    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    dim3 grid(T.rowsA / A_BM, (maxcls + A_BN - 1) / A_BN, 8);
+    kern<<<grid, A_WM * A_WN * 32, smem, s>>>(g);
+    FMM_CUDA(cudaGetLastError());
+  }
+  {
+    g.A = T.dM2;
+    g.lda = T.ldY;
+    g.a_class_stride = size_t(T.rowsB) * T.ldY;
+    g.K = T.ldY;
+    const size_t smem = sizeof(double) * B_ST * (B_BM + B_BN) * SPAD;
+    auto kern = k_m2l_gemm<B_BM, B_BN, B_WM, B_WN, B_ST, false>;
+    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    dim3 grid(T.rowsB / B_BM, (maxcls + B_BN - 1) / B_BN, 8);
+    kern<<<grid, B_WM * B_WN * 32, smem, s>>>(g);
+    FMM_CUDA(cudaGetLastError());
+  }
+  c->launches += 2;
+}
+
+}  // namespace fmmgpu

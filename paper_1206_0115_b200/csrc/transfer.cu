@@ -1,0 +1,446 @@
+// Chebyshev transfers on the device (InterpolationEngine, chebyshev.cpp:57-229),
+// one launch per operator per level over all cells of that level:
+//   P2M  CTA per leaf cell; particles staged through shared memory in chunks of 128
+//        as their three 1-D interpolation vectors, then each thread owns l^3/128
+//        coefficients (chebyshev.cpp:116-136).
+//   M2M  CTA per parent: the <=8 children go through the three l x l passes of
+//        tensor_step in shared memory (chebyshev.cpp:181-220), summed in registers.
+//   L2L  CTA per parent: own+down staged once, pushed into each child
+//        (chebyshev.cpp:222-229, bench.cpp:300-316).
+//   L2P  thread per particle, the n3 reduction factored as
+//        sum_{n1,n2} (Sx Sy) * sum_{n3} L Sz (and the three gradient variants)
+//        (chebyshev.cpp:138-179, bench.cpp:317-336).
+// Templated on the order so every loop is unrolled with compile-time bounds.
+#include "common.cuh"
+
+namespace fmmgpu {
+
+namespace {
+
+struct Geo {  // root geometry for cell_cube (geometry.cpp:165-175)
+  double lo[3];
+  double cw;    // cell width at the operator's level
+  double inv;   // 2 / cw
+};
+
+// cell centre exactly as geometry.cpp:173: (center - width/2) + (ijk + 0.5) * cw
+__device__ __forceinline__ void cell_center(const Geo& g, uint64_t code, double c[3]) {
+  int ijk[3];
+  demorton(code, ijk);
+  for (int a = 0; a < 3; ++a) c[a] = __dadd_rn(g.lo[a], __dmul_rn(static_cast<double>(ijk[a]) + 0.5, g.cw));
+}
+
+// eval_all / grad_all (chebyshev.cpp:78-114)
+template <int L>
+__device__ __forceinline__ void eval_all(const double* tn, double x, double* out) {
+  double t[L > 1 ? L - 1 : 1];
+  double tp = 1.0, tc = x;
+#pragma unroll
+  for (int n = 1; n < L; ++n) {
+    t[n - 1] = tc;
+    const double nx = 2.0 * x * tc - tp;
+    tp = tc;
+    tc = nx;
+  }
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    double acc = 0.0;
+#pragma unroll
+    for (int n = 0; n < L - 1; ++n) acc += tn[m * (L - 1) + n] * t[n];
+    out[m] = 1.0 / L + 2.0 / L * acc;
+  }
+}
+template <int L>
+__device__ __forceinline__ void grad_all(const double* tn, double x, double* out) {
+  double dt[L > 1 ? L - 1 : 1];
+  double up = 1.0, uc = 2.0 * x;
+#pragma unroll
+  for (int n = 1; n < L; ++n) {
+    dt[n - 1] = n * up;
+    const double nx = 2.0 * x * uc - up;
+    up = uc;
+    uc = nx;
+  }
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    double acc = 0.0;
+#pragma unroll
+    for (int n = 0; n < L - 1; ++n) acc += tn[m * (L - 1) + n] * dt[n];
+    out[m] = 2.0 / L * acc;
+  }
+}
+
+struct LeafArgs {
+  const uint64_t* code;
+  const uint32_t* first;
+  const uint32_t* count;
+  const double4* pw;
+  const uint32_t* pcell;
+  const double* tn;
+  double* expansion;       // multipole (P2M) or local_own (L2P)
+  const double* down;      // local_down (L2P)
+  double* far;             // [4][n] (L2P)
+  uint64_t n;
+  uint32_t ncells;
+  int ldE;
+  Geo geo;
+};
+
+constexpr int P2M_THREADS = 128;
+
+template <int L>
+__global__ void __launch_bounds__(P2M_THREADS) k_p2m(LeafArgs a) {
+  constexpr int L3 = L * L * L;
+  constexpr int OPT = (L3 + P2M_THREADS - 1) / P2M_THREADS;
+  __shared__ double tn[L * (L - 1) + 1];
+  __shared__ double S[P2M_THREADS][3 * L];
+  const uint32_t c = blockIdx.x;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < L * (L - 1); i += P2M_THREADS) tn[i] = a.tn[i];
+  double ctr[3];
+  cell_center(a.geo, a.code[c], ctr);
+  const uint32_t first = a.first[c], cnt = a.count[c];
+  double acc[OPT];
+#pragma unroll
+  for (int o = 0; o < OPT; ++o) acc[o] = 0.0;
+  for (uint32_t base = 0; base < cnt; base += P2M_THREADS) {
+    __syncthreads();
+    if (tid < cnt - base) {
+      const double4 p = a.pw[first + base + tid];
+      double s[L];
+      eval_all<L>(tn, (p.x - ctr[0]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) S[tid][m] = p.w * s[m];
+      eval_all<L>(tn, (p.y - ctr[1]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) S[tid][L + m] = s[m];
+      eval_all<L>(tn, (p.z - ctr[2]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) S[tid][2 * L + m] = s[m];
+    }
+    __syncthreads();
+    const int m = (cnt - base < P2M_THREADS) ? static_cast<int>(cnt - base) : P2M_THREADS;
+#pragma unroll
+    for (int o = 0; o < OPT; ++o) {
+      const int idx = tid + o * P2M_THREADS;
+      if (idx < L3) {
+        const int n1 = idx / (L * L), n2 = (idx / L) % L, n3 = idx % L;
+        double s = acc[o];
+        for (int j = 0; j < m; ++j) s += (S[j][n1] * S[j][L + n2]) * S[j][2 * L + n3];
+        acc[o] = s;
+      }
+    }
+  }
+  double* out = a.expansion + size_t(c) * a.ldE;
+#pragma unroll
+  for (int o = 0; o < OPT; ++o) {
+    const int idx = tid + o * P2M_THREADS;
+    if (idx < L3) out[idx] += acc[o];
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(128) k_l2p(LeafArgs a) {
+  constexpr int L3 = L * L * L;
+  __shared__ double tn[L * (L - 1) + 1];
+  for (int i = threadIdx.x; i < L * (L - 1); i += blockDim.x) tn[i] = a.tn[i];
+  __syncthreads();
+  const uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (s >= a.n) return;
+  const uint32_t c = a.pcell[s];
+  double ctr[3];
+  cell_center(a.geo, a.code[c], ctr);
+  const double4 p = a.pw[s];
+  const double inv = a.geo.inv;
+  const double rx = (p.x - ctr[0]) * inv, ry = (p.y - ctr[1]) * inv, rz = (p.z - ctr[2]) * inv;
+  double sx[L], sy[L], sz[L], gx[L], gy[L], gz[L];
+  eval_all<L>(tn, rx, sx);
+  eval_all<L>(tn, ry, sy);
+  eval_all<L>(tn, rz, sz);
+  grad_all<L>(tn, rx, gx);
+  grad_all<L>(tn, ry, gy);
+  grad_all<L>(tn, rz, gz);
+  const double* own = a.expansion + size_t(c) * a.ldE;
+  const double* down = a.down + size_t(c) * a.ldE;
+  double pot = 0, dx = 0, dy = 0, dz = 0;
+#pragma unroll 1
+  for (int n1 = 0; n1 < L; ++n1) {
+#pragma unroll
+    for (int n2 = 0; n2 < L; ++n2) {
+      double u = 0, w = 0;
+#pragma unroll
+      for (int n3 = 0; n3 < L; ++n3) {
+        const int i = (n1 * L + n2) * L + n3;
+        const double v = __ldg(own + i) + __ldg(down + i);
+        u += v * sz[n3];
+        w += v * gz[n3];
+      }
+      const double ss = sx[n1] * sy[n2];
+      pot += ss * u;
+      dx += gx[n1] * sy[n2] * u;
+      dy += sx[n1] * gy[n2] * u;
+      dz += ss * w;
+    }
+  }
+  (void)L3;
+  a.far[s] += pot;
+  a.far[a.n + s] -= inv * dx;
+  a.far[2 * a.n + s] -= inv * dy;
+  a.far[3 * a.n + s] -= inv * dz;
+}
+
+struct TransArgs {
+  const uint64_t* child_code;
+  const uint32_t* first_child;
+  const uint32_t* child_count;
+  const double* mats;      // [2][L*L]: child_t (M2M) or child (L2L)
+  const double* parent_a;  // M2M: unused; L2L: local_own of parents
+  const double* parent_b;  // L2L: local_down of parents
+  const double* child_in;  // M2M: child multipoles
+  double* out;             // M2M: parent multipole; L2L: child local_down
+  uint32_t nparents;
+  int ldE;
+};
+
+// dst[r*L + n] = sum_k mt[k*L + n] * src[k*L*L + r]  (tensor_step, chebyshev.cpp:186-199)
+template <int L>
+__device__ __forceinline__ double step_one(const double* mt, const double* src, int idx) {
+  const int r = idx / L, n = idx % L;
+  double acc = 0;
+#pragma unroll
+  for (int k = 0; k < L; ++k) acc += mt[k * L + n] * src[k * L * L + r];
+  return acc;
+}
+
+template <int L, bool IS_M2M>
+__global__ void __launch_bounds__(128) k_transfer(TransArgs a) {
+  constexpr int L3 = L * L * L;
+  constexpr int OPT = (L3 + 127) / 128;
+  __shared__ double mats[2 * L * L];
+  __shared__ double buf0[L3], buf1[L3], par[IS_M2M ? 1 : L3];
+  const uint32_t p = blockIdx.x;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 2 * L * L; i += 128) mats[i] = a.mats[i];
+  if (!IS_M2M)
+    for (int i = tid; i < L3; i += 128) par[i] = a.parent_a[size_t(p) * a.ldE + i] + a.parent_b[size_t(p) * a.ldE + i];
+  const uint32_t f = a.first_child[p], e = f + a.child_count[p];
+  double acc[OPT];
+#pragma unroll
+  for (int o = 0; o < OPT; ++o) acc[o] = 0;
+  for (uint32_t ch = f; ch < e; ++ch) {
+    const int oct = static_cast<int>(a.child_code[ch] & 7);
+    const double* m0 = mats + ((oct >> 2) & 1) * L * L;
+    const double* m1 = mats + ((oct >> 1) & 1) * L * L;
+    const double* m2 = mats + (oct & 1) * L * L;
+    __syncthreads();
+    const double* src0 = par;
+    if (IS_M2M) {
+      for (int i = tid; i < L3; i += 128) buf1[i] = a.child_in[size_t(ch) * a.ldE + i];
+      __syncthreads();
+      src0 = buf1;
+    }
+    for (int i = tid; i < L3; i += 128) buf0[i] = step_one<L>(m0, src0, i);
+    __syncthreads();
+    for (int i = tid; i < L3; i += 128) buf1[i] = step_one<L>(m1, buf0, i);
+    __syncthreads();
+    if (IS_M2M) {
+#pragma unroll
+      for (int o = 0; o < OPT; ++o) {
+        const int i = tid + o * 128;
+        if (i < L3) acc[o] += step_one<L>(m2, buf1, i);
+      }
+    } else {
+      double* out = a.out + size_t(ch) * a.ldE;
+      for (int i = tid; i < L3; i += 128) out[i] += step_one<L>(m2, buf1, i);
+    }
+  }
+  if (IS_M2M) {
+    double* out = a.out + size_t(p) * a.ldE;
+#pragma unroll
+    for (int o = 0; o < OPT; ++o) {
+      const int i = tid + o * 128;
+      if (i < L3) out[i] += acc[o];
+    }
+  }
+}
+
+__global__ void k_gather(const double* __restrict__ far, const double* __restrict__ near,
+                         const uint32_t* __restrict__ id, uint64_t n, double* __restrict__ out) {
+  const uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t o = id[s];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k * n + o] = far[k * n + s] + near[k * n + s];
+}
+
+Geo make_geo(const fmmgpu_ctx* c, int level) {
+  Geo g;
+  for (int a = 0; a < 3; ++a) g.lo[a] = c->lo[a];
+  g.cw = c->root[3] / static_cast<double>(uint64_t{1} << level);  // geometry.cpp:163-165
+  g.inv = 2.0 / g.cw;                                               // chebyshev.cpp:120
+  return g;
+}
+
+template <template <int> class F, typename... Args>
+void dispatch_order(int order, Args&&... args) {
+  switch (order) {
+    case 2: F<2>::run(args...); break;
+    case 3: F<3>::run(args...); break;
+    case 4: F<4>::run(args...); break;
+    case 5: F<5>::run(args...); break;
+    case 6: F<6>::run(args...); break;
+    case 7: F<7>::run(args...); break;
+    case 8: F<8>::run(args...); break;
+    case 9: F<9>::run(args...); break;
+    case 10: F<10>::run(args...); break;
+    default: throw Error(FMMGPU_INVALID_ARGUMENT, "order must be in [2, 10]");
+  }
+}
+
+template <int L>
+struct RunP2M {
+  static void run(const LeafArgs& a, cudaStream_t s) {
+    if (a.ncells) k_p2m<L><<<a.ncells, P2M_THREADS, 0, s>>>(a);
+  }
+};
+template <int L>
+struct RunL2P {
+  static void run(const LeafArgs& a, cudaStream_t s) {
+    if (a.n) k_l2p<L><<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a);
+  }
+};
+template <int L>
+struct RunM2M {
+  static void run(const TransArgs& a, cudaStream_t s) {
+    if (a.nparents) k_transfer<L, true><<<a.nparents, 128, 0, s>>>(a);
+  }
+};
+template <int L>
+struct RunL2L {
+  static void run(const TransArgs& a, cudaStream_t s) {
+    if (a.nparents) k_transfer<L, false><<<a.nparents, 128, 0, s>>>(a);
+  }
+};
+
+LeafArgs leaf_args(fmmgpu_ctx* c) {
+  const int leaf = c->height - 1;
+  const Level& L = c->lv[leaf];
+  LeafArgs a{};
+  a.code = L.code;
+  a.first = L.first_particle;
+  a.count = L.particle_count;
+  a.pw = c->d_pw;
+  a.pcell = c->d_pcell;
+  a.tn = c->d_interp;
+  a.n = c->n;
+  a.ncells = L.n;
+  a.ldE = c->ldE;
+  a.geo = make_geo(c, leaf);
+  return a;
+}
+
+}  // namespace
+
+void interp_setup(fmmgpu_ctx* c) {
+  // InterpolationEngine ctor (chebyshev.cpp:57-76), host arithmetic
+  const int l = c->order;
+  auto cheb_t = [](int n, double x) {
+    double tp = 1.0, t = x;
+    if (n == 0) return tp;
+    for (int i = 1; i < n; ++i) {
+      const double nx = 2.0 * x * t - tp;
+      tp = t;
+      t = nx;
+    }
+    return t;
+  };
+  c->h_roots.resize(l);
+  for (int m = 0; m < l; ++m) c->h_roots[m] = std::cos((2 * m + 1) * 3.14159265358979323846 / (2 * l));
+  c->h_tn.assign(size_t(l) * (l - 1), 0.0);
+  for (int m = 0; m < l; ++m)
+    for (int n = 1; n < l; ++n) c->h_tn[m * (l - 1) + n - 1] = cheb_t(n, c->h_roots[m]);
+  auto s_eval = [&](double root, double x) {
+    double acc = 1.0 / l;
+    for (int n = 1; n < l; ++n) acc += (2.0 / l) * cheb_t(n, root) * cheb_t(n, x);
+    return acc;
+  };
+  for (int side = 0; side < 2; ++side) {
+    c->h_child[side].assign(l * l, 0.0);
+    c->h_child_t[side].assign(l * l, 0.0);
+    const double shift = side == 0 ? -0.5 : 0.5;
+    for (int m = 0; m < l; ++m)
+      for (int k = 0; k < l; ++k) {
+        const double v = s_eval(c->h_roots[m], 0.5 * c->h_roots[k] + shift);
+        c->h_child[side][m * l + k] = v;
+        c->h_child_t[side][k * l + m] = v;
+      }
+  }
+  // device layout: [tn (l*(l-1)) padded to l*l][child0][child1][child_t0][child_t1]
+  std::vector<double> h(5 * l * l, 0.0);
+  std::copy(c->h_tn.begin(), c->h_tn.end(), h.begin());
+  std::copy(c->h_child[0].begin(), c->h_child[0].end(), h.begin() + l * l);
+  std::copy(c->h_child[1].begin(), c->h_child[1].end(), h.begin() + 2 * l * l);
+  std::copy(c->h_child_t[0].begin(), c->h_child_t[0].end(), h.begin() + 3 * l * l);
+  std::copy(c->h_child_t[1].begin(), c->h_child_t[1].end(), h.begin() + 4 * l * l);
+  FMM_CUDA(cudaMalloc(&c->d_interp, h.size() * sizeof(double)));
+  FMM_CUDA(cudaMemcpy(c->d_interp, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+void launch_p2m(fmmgpu_ctx* c, cudaStream_t s) {
+  LeafArgs a = leaf_args(c);
+  a.expansion = c->lv[c->height - 1].multipole;
+  dispatch_order<RunP2M>(c->order, a, s);
+  FMM_CUDA(cudaGetLastError());
+  ++c->launches;
+}
+
+void launch_l2p(fmmgpu_ctx* c, cudaStream_t s) {
+  LeafArgs a = leaf_args(c);
+  a.expansion = c->lv[c->height - 1].local_own;
+  a.down = c->lv[c->height - 1].local_down;
+  a.far = c->d_far;
+  dispatch_order<RunL2P>(c->order, a, s);
+  FMM_CUDA(cudaGetLastError());
+  ++c->launches;
+}
+
+void launch_m2m(fmmgpu_ctx* c, int v, cudaStream_t s) {
+  const int l = c->order;
+  TransArgs a{};
+  a.child_code = c->lv[v + 1].code;
+  a.first_child = c->lv[v].first_child;
+  a.child_count = c->lv[v].child_count;
+  a.mats = c->d_interp + 3 * l * l;  // child_t
+  a.child_in = c->lv[v + 1].multipole;
+  a.out = c->lv[v].multipole;
+  a.nparents = c->lv[v].n;
+  a.ldE = c->ldE;
+  dispatch_order<RunM2M>(l, a, s);
+  FMM_CUDA(cudaGetLastError());
+  ++c->launches;
+}
+
+void launch_l2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
+  const int l = c->order;
+  TransArgs a{};
+  a.child_code = c->lv[v + 1].code;
+  a.first_child = c->lv[v].first_child;
+  a.child_count = c->lv[v].child_count;
+  a.mats = c->d_interp + l * l;  // child
+  a.parent_a = c->lv[v].local_own;
+  a.parent_b = c->lv[v].local_down;
+  a.out = c->lv[v + 1].local_down;
+  a.nparents = c->lv[v].n;
+  a.ldE = c->ldE;
+  dispatch_order<RunL2L>(l, a, s);
+  FMM_CUDA(cudaGetLastError());
+  ++c->launches;
+}
+
+void launch_gather(fmmgpu_ctx* c, cudaStream_t s) {
+  k_gather<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, s>>>(c->d_far, c->d_near, c->d_id, c->n, c->d_out);
+  FMM_CUDA(cudaGetLastError());
+  ++c->launches;
+}
+
+}  // namespace fmmgpu

@@ -1,0 +1,352 @@
+// Octree construction on the device: GroupTree::build (geometry.cpp:73-161) as
+// reductions, a stable LSD radix sort of (Morton key, input index) and run-length
+// encodes. Bit-exact with the reference: keys come from the same IEEE FP64 ops
+// (explicit _rn intrinsics, no FMA contraction), the sort is stable so ties keep
+// input order exactly like std::sort on (key, index) pairs (geometry.cpp:95).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace fmmgpu {
+
+namespace {
+
+template <typename T>
+T* dalloc(size_t count, cudaStream_t s) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  FMM_CUDA(cudaMallocAsync(&p, count * sizeof(T), s));
+  return static_cast<T*>(p);
+}
+template <typename T>
+void dfree(T*& p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+  p = nullptr;
+}
+
+// bounding_cube (geometry.cpp:18-36): per-axis min / max. Exact (order-free).
+__global__ void k_minmax_partial(const double4* __restrict__ p, uint64_t n, double* __restrict__ part) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const double4 q = p[i];
+    mn[0] = fmin(mn[0], q.x); mx[0] = fmax(mx[0], q.x);
+    mn[1] = fmin(mn[1], q.y); mx[1] = fmax(mx[1], q.y);
+    mn[2] = fmin(mn[2], q.z); mx[2] = fmax(mx[2], q.z);
+  }
+  __shared__ double sm[6][32];
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[a] = fmin(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+      mx[a] = fmax(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+    }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0)
+    for (int a = 0; a < 3; ++a) { sm[a][w] = mn[a]; sm[3 + a][w] = mx[a]; }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int nw = blockDim.x >> 5;
+    double r = sm[threadIdx.x][0];
+    for (int i = 1; i < nw; ++i) r = threadIdx.x < 3 ? fmin(r, sm[threadIdx.x][i]) : fmax(r, sm[threadIdx.x][i]);
+    part[threadIdx.x * gridDim.x + blockIdx.x] = r;
+  }
+}
+
+// Morton key per particle (geometry.cpp:76-94): u = floor((c - lo) / cw), clamped.
+__global__ void k_keys(const double4* __restrict__ p, uint64_t n, double lo0, double lo1, double lo2,
+                       double hi0, double hi1, double hi2, double cw, uint32_t grid,
+                       uint64_t* __restrict__ keys, uint32_t* __restrict__ idx, int* __restrict__ flag) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double4 q = p[i];
+  const double c[3] = {q.x, q.y, q.z}, lo[3] = {lo0, lo1, lo2}, hi[3] = {hi0, hi1, hi2};
+  uint32_t ijk[3];
+  for (int a = 0; a < 3; ++a) {
+    if (c[a] < lo[a] || c[a] > hi[a]) atomicOr(flag, 1);  // domain_error
+    double u = floor(__ddiv_rn(__dsub_rn(c[a], lo[a]), cw));
+    if (u < 0) u = 0;
+    if (u >= grid) u = grid - 1;
+    ijk[a] = static_cast<uint32_t>(u);
+  }
+  keys[i] = morton(ijk[0], ijk[1], ijk[2]);
+  idx[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void k_permute(const double4* __restrict__ in, const uint32_t* __restrict__ idx, uint64_t n,
+                          double4* __restrict__ out) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = in[idx[i]];
+}
+
+// leaf cell of every Morton slot, and the coincident-particle check
+// (geometry.cpp:126-136: equal positions inside one leaf -> domain_error).
+__global__ void k_leaf_scan(const uint32_t* __restrict__ first, const uint32_t* __restrict__ count, uint32_t ncells,
+                            const double4* __restrict__ pw, uint32_t* __restrict__ pcell, int* __restrict__ flag) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ncells) return;
+  const uint32_t f = first[warp], m = count[warp];
+  for (uint32_t a = lane; a < m; a += 32) {
+    pcell[f + a] = warp;
+    const double4 pa = pw[f + a];
+    for (uint32_t b = a + 1; b < m; ++b) {
+      const double4 pb = pw[f + b];
+      if (pa.x == pb.x && pa.y == pb.y && pa.z == pb.z) atomicOr(flag, 2);
+    }
+  }
+}
+
+__global__ void k_shift3(const uint64_t* __restrict__ in, uint32_t n, uint64_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i] >> 3;
+}
+
+__global__ void k_set_parent(const uint32_t* __restrict__ first_child, const uint32_t* __restrict__ child_count,
+                             uint32_t nparents, uint32_t* __restrict__ parent_of_child) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nparents) return;
+  for (uint32_t c = first_child[p]; c < first_child[p] + child_count[p]; ++c) parent_of_child[c] = p;
+}
+
+__global__ void k_fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+__global__ void k_scatter_map(const uint64_t* __restrict__ code, uint32_t n, uint32_t* __restrict__ map) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) map[code[i]] = i;
+}
+__global__ void k_octant(const uint64_t* __restrict__ code, uint32_t n, uint8_t* __restrict__ oct,
+                         uint32_t* __restrict__ iota) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { oct[i] = static_cast<uint8_t>(code[i] & 7); iota[i] = i; }
+}
+
+inline unsigned blocks(uint64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+void free_level(fmmgpu::Level& L, cudaStream_t s) {
+  dfree(L.code, s); dfree(L.first_particle, s); dfree(L.particle_count, s); dfree(L.parent, s);
+  dfree(L.first_child, s); dfree(L.child_count, s); dfree(L.map, s); dfree(L.cls_cells, s);
+  dfree(L.multipole, s); dfree(L.local_own, s); dfree(L.local_down, s);
+  dfree(L.far_target, s); dfree(L.far_source, s); dfree(L.far_vec, s); dfree(L.far_group_off, s);
+  L.far_pairs = 0;
+}
+
+}  // namespace
+
+void* scratch(fmmgpu_ctx* c, size_t bytes) {
+  if (bytes > c->d_tmp_cap) {
+    if (c->d_tmp) FMM_CUDA(cudaFreeAsync(c->d_tmp, c->s_far));
+    c->d_tmp_cap = std::max(bytes, c->d_tmp_cap * 3 / 2);
+    FMM_CUDA(cudaMallocAsync(&c->d_tmp, c->d_tmp_cap, c->s_far));
+  }
+  return c->d_tmp;
+}
+
+void tree_free(fmmgpu_ctx* c) {
+  cudaStream_t s = c->s_far;
+  for (auto& L : c->lv) free_level(L, s);
+  c->lv.clear();
+  dfree(c->d_pw, s); dfree(c->d_id, s); dfree(c->d_pcell, s);
+  dfree(c->d_near, s); dfree(c->d_far, s); dfree(c->d_out, s);
+  c->have_tree = false;
+}
+
+void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, int height, int group,
+                const double* root4) {
+  // argument validation, geometry.cpp:65-69 and bounding_cube's empty check
+  if (height < 3 || height > 21) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: height must be in [3, 21]");
+  if (group < 1) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: group size must be positive");
+  if (n == 0) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: empty particle set");
+  if (n >= 0xffffffffull) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: particle count exceeds 32-bit ids");
+  if (root4 && !(root4[3] > 0)) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: root cube width must be positive");
+  cudaStream_t s = c->s_far;
+  tree_free(c);
+  lists_free(c);
+
+  // input -> device (input order)
+  if (c->d_in_cap < n) {
+    if (c->d_in) FMM_CUDA(cudaFreeAsync(c->d_in, s));
+    FMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c->d_in), n * sizeof(double4), s));
+    c->d_in_cap = n;
+  }
+  FMM_CUDA(cudaMemcpyAsync(c->d_in, xyzw, n * sizeof(double4), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
+
+  // root cube
+  double root[4];
+  if (root4) {
+    std::copy(root4, root4 + 4, root);
+  } else {
+    const int nb = static_cast<int>(std::min<uint64_t>(1184, blocks(n, 256)));
+    double* part = static_cast<double*>(scratch(c, sizeof(double) * 6 * nb));
+    k_minmax_partial<<<nb, 256, 0, s>>>(c->d_in, n, part);
+    FMM_CUDA(cudaGetLastError());
+    std::vector<double> h(6 * nb);
+    FMM_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * 6 * nb, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = h[a * nb];
+      hi[a] = h[(3 + a) * nb];
+      for (int b = 1; b < nb; ++b) {
+        lo[a] = std::min(lo[a], h[a * nb + b]);
+        hi[a] = std::max(hi[a], h[(3 + a) * nb + b]);
+      }
+    }
+    double extent = 0;  // geometry.cpp:28-34, host arithmetic without contraction
+    for (int a = 0; a < 3; ++a) {
+      root[a] = 0.5 * (lo[a] + hi[a]);
+      extent = std::max(extent, hi[a] - lo[a]);
+    }
+    root[3] = extent > 0 ? extent * (1.0 + 1e-6) : 1.0;
+  }
+  std::copy(root, root + 4, c->root);
+  c->n = n;
+  c->height = height;
+  c->group = group;
+  const int leaf = height - 1;
+  const uint32_t grid = 1u << leaf;
+  const double cw = root[3] / static_cast<double>(grid);
+  double hib[3];
+  for (int a = 0; a < 3; ++a) {
+    c->lo[a] = root[a] - 0.5 * root[3];
+    hib[a] = c->lo[a] + root[3];
+  }
+
+  // keys + stable radix sort of (key, input index)
+  uint64_t* keys = dalloc<uint64_t>(n, s);
+  uint64_t* keys_sorted = dalloc<uint64_t>(n, s);
+  uint32_t* idx = dalloc<uint32_t>(n, s);
+  c->d_id = dalloc<uint32_t>(n, s);
+  k_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, c->lo[0], c->lo[1], c->lo[2], hib[0], hib[1], hib[2], cw, grid,
+                                         keys, idx, c->d_flag);
+  FMM_CUDA(cudaGetLastError());
+  size_t tb = 0;
+  FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
+                                           std::max(1, 3 * leaf), s));
+  FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
+                                           std::max(1, 3 * leaf), s));
+  c->d_pw = dalloc<double4>(n, s);
+  k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw);
+  FMM_CUDA(cudaGetLastError());
+
+  // leaf cells = runs of equal keys (geometry.cpp:113-122)
+  c->lv.resize(height);
+  Level& L = c->lv[leaf];
+  uint32_t* d_runs = dalloc<uint32_t>(1, s);
+  L.code = dalloc<uint64_t>(n, s);
+  L.particle_count = dalloc<uint32_t>(n, s);
+  FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, keys_sorted, L.code, L.particle_count, d_runs, static_cast<int>(n), s));
+  FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, keys_sorted, L.code, L.particle_count, d_runs, static_cast<int>(n), s));
+  uint32_t runs = 0;
+  FMM_CUDA(cudaMemcpyAsync(&runs, d_runs, 4, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  L.n = runs;
+  L.first_particle = dalloc<uint32_t>(runs, s);
+  FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, L.particle_count, L.first_particle, static_cast<int>(runs), s));
+  FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, L.particle_count, L.first_particle, static_cast<int>(runs), s));
+  L.first_child = dalloc<uint32_t>(runs, s);
+  L.child_count = dalloc<uint32_t>(runs, s);
+  L.parent = dalloc<uint32_t>(runs, s);
+  FMM_CUDA(cudaMemsetAsync(L.first_child, 0, 4ull * runs, s));
+  FMM_CUDA(cudaMemsetAsync(L.child_count, 0, 4ull * runs, s));
+  FMM_CUDA(cudaMemsetAsync(L.parent, 0, 4ull * runs, s));
+  c->d_pcell = dalloc<uint32_t>(n, s);
+  k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs, c->d_pw,
+                                                               c->d_pcell, c->d_flag);
+  FMM_CUDA(cudaGetLastError());
+
+  // parent levels by code >> 3 (geometry.cpp:138-153)
+  uint64_t* shifted = keys;  // reuse
+  for (int v = leaf - 1; v >= 0; --v) {
+    Level& C = c->lv[v + 1];
+    Level& P = c->lv[v];
+    k_shift3<<<blocks(C.n, 256), 256, 0, s>>>(C.code, C.n, shifted);
+    P.code = dalloc<uint64_t>(C.n, s);
+    P.child_count = dalloc<uint32_t>(C.n, s);
+    FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, shifted, P.code, P.child_count, d_runs, static_cast<int>(C.n), s));
+    FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, shifted, P.code, P.child_count, d_runs, static_cast<int>(C.n), s));
+    FMM_CUDA(cudaMemcpyAsync(&runs, d_runs, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    P.n = runs;
+    P.first_child = dalloc<uint32_t>(runs, s);
+    FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, P.child_count, P.first_child, static_cast<int>(runs), s));
+    FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, P.child_count, P.first_child, static_cast<int>(runs), s));
+    k_set_parent<<<blocks(runs, 256), 256, 0, s>>>(P.first_child, P.child_count, runs, C.parent);
+    P.first_particle = dalloc<uint32_t>(runs, s);
+    P.particle_count = dalloc<uint32_t>(runs, s);
+    P.parent = dalloc<uint32_t>(runs, s);
+    FMM_CUDA(cudaMemsetAsync(P.first_particle, 0, 4ull * runs, s));
+    FMM_CUDA(cudaMemsetAsync(P.particle_count, 0, 4ull * runs, s));
+    FMM_CUDA(cudaMemsetAsync(P.parent, 0, 4ull * runs, s));
+    FMM_CUDA(cudaGetLastError());
+  }
+  dfree(keys, s);
+  dfree(keys_sorted, s);
+  dfree(idx, s);
+  dfree(d_runs, s);
+
+  // blocks of group_size cells (geometry.cpp:155-160); lookup maps; parity classes;
+  // expansions (cell-major, stride ldE, zero padding)
+  for (int v = 0; v < height; ++v) {
+    Level& V = c->lv[v];
+    V.block_offsets.clear();
+    for (uint64_t b = 0; b < V.n; b += static_cast<uint64_t>(group)) V.block_offsets.push_back(static_cast<uint32_t>(b));
+    V.block_offsets.push_back(V.n);
+    V.full = static_cast<uint64_t>(V.n) == (uint64_t{1} << (3 * v));
+    if (!V.full && v <= DENSE_MAP_MAX_LEVEL) {
+      const uint64_t cap = uint64_t{1} << (3 * v);
+      V.map = dalloc<uint32_t>(cap, s);
+      k_fill_u32<<<blocks(cap, 256), 256, 0, s>>>(V.map, cap, NPOS);
+      k_scatter_map<<<blocks(V.n, 256), 256, 0, s>>>(V.code, V.n, V.map);
+    }
+    if (v >= 2) {
+      uint8_t* oct = dalloc<uint8_t>(V.n, s);
+      uint8_t* oct_sorted = dalloc<uint8_t>(V.n, s);
+      uint32_t* iota = dalloc<uint32_t>(V.n, s);
+      V.cls_cells = dalloc<uint32_t>(V.n, s);
+      k_octant<<<blocks(V.n, 256), 256, 0, s>>>(V.code, V.n, oct, iota);
+      FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, oct, oct_sorted, iota, V.cls_cells, static_cast<int>(V.n), 0, 3, s));
+      FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, oct, oct_sorted, iota, V.cls_cells, static_cast<int>(V.n), 0, 3, s));
+      std::vector<uint8_t> h(V.n);
+      FMM_CUDA(cudaMemcpyAsync(h.data(), oct_sorted, V.n, cudaMemcpyDeviceToHost, s));
+      FMM_CUDA(cudaStreamSynchronize(s));
+      for (int q = 0; q <= 8; ++q)
+        V.cls_off[q] = static_cast<uint32_t>(std::lower_bound(h.begin(), h.end(), static_cast<uint8_t>(q)) - h.begin());
+      dfree(oct, s);
+      dfree(oct_sorted, s);
+      dfree(iota, s);
+    }
+    const size_t e = size_t(V.n) * c->ldE;
+    V.multipole = dalloc<double>(e, s);
+    V.local_own = dalloc<double>(e, s);
+    V.local_down = dalloc<double>(e, s);
+    FMM_CUDA(cudaMemsetAsync(V.multipole, 0, e * 8, s));
+    FMM_CUDA(cudaMemsetAsync(V.local_own, 0, e * 8, s));
+    FMM_CUDA(cudaMemsetAsync(V.local_down, 0, e * 8, s));
+  }
+  c->d_near = dalloc<double>(4 * n, s);
+  c->d_far = dalloc<double>(4 * n, s);
+  c->d_out = dalloc<double>(4 * n, s);
+  FMM_CUDA(cudaMemsetAsync(c->d_near, 0, 32 * n, s));
+  FMM_CUDA(cudaMemsetAsync(c->d_far, 0, 32 * n, s));
+
+  int flag = 0;
+  FMM_CUDA(cudaMemcpyAsync(&flag, c->d_flag, 4, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  if (flag & 1) {
+    tree_free(c);
+    throw Error(FMMGPU_DOMAIN_ERROR, "GroupTree: particle outside the root cube");
+  }
+  if (flag & 2) {
+    tree_free(c);
+    throw Error(FMMGPU_DOMAIN_ERROR, "GroupTree: coincident particles");
+  }
+  c->have_tree = true;
+}
+
+}  // namespace fmmgpu

@@ -154,6 +154,15 @@ class OracleTree:
 class OracleOps:
     """M2LOperatorSet restatement (m2l.cpp:136-163); cache_path loads reference factors."""
 
+    _memo = {}
+
+    @classmethod
+    def cached(cls, order):
+        """Own-SVD operator set per order, computed once per process (Jacobi at l=7 takes seconds)."""
+        if order not in cls._memo:
+            cls._memo[order] = cls(order)
+        return cls._memo[order]
+
     def __init__(self, order, eps=None, cache_path=None):
         self.L = Oracle.lib()
         self.order = order

@@ -1,0 +1,309 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bars (BASELINE.json north_star):
+* tree, Morton keys, particle order, near CSR and far LevelM2L lists: BIT-EXACT;
+* expansions / fields: relative L2 (bench.cpp:91-100) <= 1e-12 against the CPU
+  restatement (oracle/restate) and, when built, the reference itself (oracle/_ref).
+Sizes are small enough for the CPU checkers to finish in seconds.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracles import Oracle, OracleOps, OracleTree, RefContext, RefLib, force_error, relative_l2_error
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12  # north_star: potentials / forces within relative L2 <= 1e-12
+
+CASES = [
+    # (n, height, order, dist, seed, random weights)
+    (2000, 3, 7, "uniform", 42, False),
+    (10000, 4, 5, "uniform", 42, False),
+    (5000, 5, 4, "sphere", 7, False),
+    (3000, 4, 3, "uniform", 11, True),
+    (20000, 5, 5, "uniform", 3, True),
+]
+
+
+def make_particles(n, dist, seed, random_weights):
+    xyzw = Oracle.generate_particles(n, dist, seed)
+    if random_weights:  # test_direct.cpp:15-21: w in [0.5, 1.5)
+        rng = np.random.default_rng(seed)
+        xyzw[:, 3] = 0.5 + rng.random(n)
+    return xyzw
+
+
+@pytest.fixture(scope="module")
+def fmm():
+    import paper_1206_0115_b200 as P
+    return P
+
+
+def ctx_for(P, xyzw, height, order, group=250, cache=None):
+    c = P.FmmContext(None, order=order)
+    if cache:
+        c.load_m2l_cache(cache)
+    c.build_tree(xyzw, height, group)
+    return c
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"n{c[0]}_h{c[1]}_l{c[2]}_{c[3]}{'_w' if c[5] else ''}" for c in CASES])
+def test_tree_and_lists_bit_exact(fmm, case):
+    n, h, l, dist, seed, rw = case
+    xyzw = make_particles(n, dist, seed, rw)
+    ot = OracleTree(xyzw, h)
+    c = ctx_for(fmm, xyzw, h, l)
+    assert np.array_equal(c.root_cube(), ot.root_cube())
+    for a, b in zip(c.particles(), ot.particles()):
+        assert np.array_equal(a, b)
+    for v in range(h):
+        gc, gb = c.level(v)
+        oc, ob = ot.level(v)
+        gc["_pad"] = 0
+        oc["_pad"] = 0
+        assert np.array_equal(gc, oc), f"level {v} cells"
+        assert np.array_equal(gb, ob), f"level {v} blocks"
+    c.build_lists()
+    goff, gcells, gtot = c.near()
+    ooff, ocells, _, otot = ot.near()
+    assert np.array_equal(goff, ooff) and np.array_equal(gcells, ocells) and gtot == otot
+    for v in range(2, h):
+        for a, b in zip(c.far(v), ot.far(v)):
+            assert np.array_equal(a, b), f"far level {v}"
+
+
+def test_tree_matches_reference_itself(fmm):
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    xyzw = make_particles(8000, "sphere", 5, True)
+    ref = RefContext(xyzw, 5, 4)
+    c = ctx_for(fmm, xyzw, 5, 4)
+    assert np.array_equal(c.root_cube(), ref.root_cube())
+    for v in range(5):
+        gc, gb = c.level(v)
+        rc, rb = ref.level(v)
+        gc["_pad"] = 0
+        rc["_pad"] = 0
+        assert np.array_equal(gc, rc) and np.array_equal(gb, rb)
+    c.build_lists()
+    goff, gcells, gtot = c.near()
+    roff, rcells, _, rtot = ref.near()
+    assert np.array_equal(goff, roff) and np.array_equal(gcells, rcells) and gtot == rtot
+    for v in range(2, 5):
+        for a, b in zip(c.far(v), ref.far(v)):
+            assert np.array_equal(a, b)
+
+
+def test_m2l_ranks_match_reference(fmm):
+    for order, expect in [(5, [23, 18, 16, 15, 14, 10, 13, 12, 10, 9, 9, 9, 9, 9, 9, 9]),
+                          (7, [47, 36, 35, 26, 25, 24, 25, 25, 25, 22, 18, 16, 16, 16, 16, 16])]:
+        c = fmm.FmmContext(None, order=order)
+        rep = c.compression_report()
+        assert list(rep["ranks"]) == expect  # SURVEY.md Appendix B / test_output.txt:8
+        assert list(rep["multiplicity"]) == [6, 24, 24, 12, 24, 8, 6, 24, 24, 24, 48, 24, 12, 24, 24, 8]
+
+
+def _oracle_eval(xyzw, h, l, mask, cache=None):
+    ot = OracleTree(xyzw, h)
+    ops = OracleOps(l, cache_path=cache) if cache else OracleOps.cached(l)
+    f = ot.evaluate(ops, mask=mask)
+    return ot, f
+
+
+@pytest.mark.parametrize("case", CASES[:3], ids=["n2000_h3_l7", "n10000_h4_l5", "n5000_h5_l4_sphere"])
+def test_operators_per_level(fmm, case, tmp_path):
+    """Each operator on the oracle's inputs -> the oracle's outputs (shared M2L factors)."""
+    n, h, l, dist, seed, rw = case
+    xyzw = make_particles(n, dist, seed, rw)
+    cache = str(tmp_path / "m2l.bin")
+    gctx = fmm.FmmContext(None, order=l)
+    gctx.save_m2l_cache(cache)  # both sides use the device-SVD factors
+    ot, _ = _oracle_eval(xyzw, h, l, 63, cache)
+    leaf = h - 1
+    c = ctx_for(fmm, xyzw, h, l, cache=cache)
+    # P2M
+    c.run_kinds({"P2M"})
+    assert relative_l2_error(c.expansion(leaf, 0), ot.expansion(leaf, 0, l)) <= 1e-14
+    # M2M, per parent level from the oracle's child multipoles
+    for v in range(leaf - 1, 1, -1):
+        c.reset()
+        c.set_expansion(v + 1, 0, ot.expansion(v + 1, 0, l))
+        c.m2m(v)
+        assert relative_l2_error(c.expansion(v, 0), ot.expansion(v, 0, l)) <= 1e-14, v
+    # M2L per level
+    for v in range(2, leaf + 1):
+        c.reset()
+        c.set_expansion(v, 0, ot.expansion(v, 0, l))
+        c.m2l(v)
+        assert relative_l2_error(c.expansion(v, 1), ot.expansion(v, 1, l)) <= 1e-13, v
+    # L2L per parent level
+    for v in range(2, leaf):
+        c.reset()
+        c.set_expansion(v, 1, ot.expansion(v, 1, l))
+        c.set_expansion(v, 2, ot.expansion(v, 2, l))
+        c.l2l(v)
+        assert relative_l2_error(c.expansion(v + 1, 2), ot.expansion(v + 1, 2, l)) <= 1e-14, v
+    # L2P: far-field fields from the oracle's leaf locals
+    c.reset()
+    c.set_expansion(leaf, 1, ot.expansion(leaf, 1, l))
+    c.set_expansion(leaf, 2, ot.expansion(leaf, 2, l))
+    c.l2p()
+    far = c.gather()
+    ofar = OracleTree(xyzw, h).evaluate(OracleOps(l, cache_path=cache), mask=1 | 2 | 4 | 8 | 16)
+    assert relative_l2_error(far[0], ofar[0]) <= 1e-13
+    assert force_error(*far[1:], *ofar[1:]) <= 1e-13
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"n{c[0]}_h{c[1]}_l{c[2]}_{c[3]}{'_w' if c[5] else ''}" for c in CASES])
+def test_p2p_near_field(fmm, case):
+    n, h, l, dist, seed, rw = case
+    xyzw = make_particles(n, dist, seed, rw)
+    _, near = _oracle_eval(xyzw, h, l, 32)  # mutual P2P + ordered slot drain
+    c = ctx_for(fmm, xyzw, h, l)
+    c.run_kinds({"P2P"})
+    g = c.gather()
+    assert relative_l2_error(g[0], near[0]) <= 1e-14
+    assert force_error(*g[1:], *near[1:]) <= 1e-13
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"n{c[0]}_h{c[1]}_l{c[2]}_{c[3]}{'_w' if c[5] else ''}" for c in CASES])
+def test_full_evaluation(fmm, case, tmp_path):
+    """Whole evaluation vs the restatement: own device-SVD factors and shared factors."""
+    n, h, l, dist, seed, rw = case
+    xyzw = make_particles(n, dist, seed, rw)
+    # (a) GPU with its own operators vs oracle with its own (Jacobi) operators
+    _, of = _oracle_eval(xyzw, h, l, 63)
+    c = ctx_for(fmm, xyzw, h, l)
+    c.evaluate()
+    g = c.gather()
+    assert relative_l2_error(g[0], of[0]) <= TOL
+    assert force_error(*g[1:], *of[1:]) <= TOL
+    # (b) identical factors on both sides
+    cache = str(tmp_path / "m2l.bin")
+    c.save_m2l_cache(cache)
+    _, of2 = _oracle_eval(xyzw, h, l, 63, cache)
+    assert relative_l2_error(g[0], of2[0]) <= 1e-13
+    assert force_error(*g[1:], *of2[1:]) <= 1e-13
+
+
+def test_full_evaluation_vs_reference_itself(fmm, tmp_path):
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    for (n, h, l, dist, seed, rw) in CASES[:3]:
+        xyzw = make_particles(n, dist, seed, rw)
+        ref = RefContext(xyzw, h, l)
+        ref.execute(workers=4)
+        rf = ref.fields()
+        cache = str(tmp_path / f"ref{l}.bin")
+        ref.save_m2l_cache(cache)
+        for own in (True, False):
+            c = ctx_for(fmm, xyzw, h, l, cache=None if own else cache)
+            c.evaluate()
+            g = c.gather()
+            assert relative_l2_error(g[0], rf[0]) <= TOL, (n, own)
+            assert force_error(*g[1:], *rf[1:]) <= TOL, (n, own)
+
+
+def test_deterministic(fmm):
+    xyzw = make_particles(20000, "uniform", 1, True)
+    c = ctx_for(fmm, xyzw, 5, 5)
+    c.evaluate()
+    a = c.gather()
+    c.evaluate()
+    b = c.gather()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_run_entry_point(fmm):
+    xyzw = make_particles(5000, "uniform", 9, False)
+    c = fmm.FmmContext(None, order=4)
+    g = c.run(xyzw, 4)
+    _, of = _oracle_eval(xyzw, 4, 4, 63)
+    assert relative_l2_error(g[0], of[0]) <= TOL
+    assert force_error(*g[1:], *of[1:]) <= TOL
+
+
+def test_edge_cases(fmm):
+    P = fmm
+    # single particle: zero fields (geometry.cpp bounding_cube width 1, test_geometry.cpp:202-210)
+    c = P.FmmContext(None, order=3)
+    one = np.array([[0.3, 0.4, 0.5, 1.0]])
+    c.build_tree(one, 3)
+    c.evaluate()
+    g = c.gather()
+    assert all(np.all(x == 0) for x in g)
+    # two particles in adjacent leaves: direct interaction only (test_direct.cpp:43-45)
+    two = np.array([[0.0, 0.0, 0.0, 1.0], [0.5, 0.0, 0.0, 1.0]])
+    c.build_tree(two, 3)
+    c.evaluate()
+    g = c.gather()
+    assert abs(g[0][0] - 2.0) < 1e-15 and abs(g[1][0] + 4.0) < 1e-14
+    # two particles three leaves apart: far field only, as in the reference
+    two = np.array([[0.0, 0.0, 0.0, 1.0], [2.0, 0.0, 0.0, 1.0]])
+    c.build_tree(two, 3)
+    c.evaluate()
+    g = c.gather()
+    of = OracleTree(two, 3).evaluate(OracleOps.cached(3))
+    assert relative_l2_error(g[0], of[0]) <= TOL and force_error(*g[1:], *of[1:]) <= TOL
+    # errors mirror the reference exception classes
+    with pytest.raises(P.InvalidArgument):
+        c.build_tree(one, 2)
+    with pytest.raises(P.InvalidArgument):
+        c.build_tree(one, 22)
+    with pytest.raises(P.InvalidArgument):
+        c.build_tree(one, 4, 0)
+    with pytest.raises(P.InvalidArgument):
+        c.build_tree(np.zeros((0, 4)), 4)
+    with pytest.raises(P.DomainError):
+        c.build_tree(np.array([[0.1, 0.1, 0.1, 1.0], [0.1, 0.1, 0.1, 1.0], [0.9, 0.9, 0.9, 1.0]]), 4)
+    with pytest.raises(P.DomainError):
+        c.build_tree(np.array([[2.0, 0.5, 0.5, 1.0]]), 4, root=[0.5, 0.5, 0.5, 1.0])
+    with pytest.raises(P.InvalidArgument):
+        c.build_tree(one, 4, root=[0.5, 0.5, 0.5, 0.0])
+    with pytest.raises(P.InvalidArgument):
+        P.FmmContext(None, order=11)
+    with pytest.raises(P.InvalidArgument):
+        P.FmmContext(None, order=1)
+    # explicit root cube, ragged occupancy, group size 1 and 7
+    xyzw = make_particles(3000, "sphere", 2, True)
+    for g_size in (1, 7):
+        ot = OracleTree(xyzw, 5, g_size, root=[0.5, 0.5, 0.5, 1.25])
+        c = P.FmmContext(None, order=4)
+        c.build_tree(xyzw, 5, g_size, root=[0.5, 0.5, 0.5, 1.25])
+        for v in range(5):
+            gc, gb = c.level(v)
+            oc, ob = ot.level(v)
+            gc["_pad"] = 0
+            oc["_pad"] = 0
+            assert np.array_equal(gc, oc) and np.array_equal(gb, ob)
+        c.build_lists()
+        for v in range(2, 5):
+            for a, b in zip(c.far(v), ot.far(v)):
+                assert np.array_equal(a, b)
+        c.evaluate()
+        g = c.gather()
+        of = ot.evaluate(OracleOps.cached(4))
+        assert relative_l2_error(g[0], of[0]) <= TOL
+        assert force_error(*g[1:], *of[1:]) <= TOL
+
+
+def test_accuracy_against_direct_sum(fmm):
+    """Size-independent property at larger N: FMM vs exact direct sum on sampled
+    targets stays at the reference's accuracy level (test_output.txt:7: ~1e-6 at l=5)."""
+    xyzw = make_particles(200000, "uniform", 42, False)
+    c = ctx_for(fmm, xyzw, 5, 5)
+    c.evaluate()
+    g = c.gather()
+    k = 200
+    targets = np.array([i * len(xyzw) // k for i in range(k)], dtype=np.uint32)
+    out = [np.zeros(k) for _ in range(4)]
+    import ctypes
+    Oracle.lib().orc_direct(xyzw.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint64(len(xyzw)),
+                            targets.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint64(k),
+                            *[a.ctypes.data_as(ctypes.c_void_p) for a in out])
+    ep = relative_l2_error(g[0][targets], out[0])
+    ef = force_error(g[1][targets], g[2][targets], g[3][targets], *out[1:])
+    assert ep < 1e-5 and ef < 1e-3, (ep, ef)

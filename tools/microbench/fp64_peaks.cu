@@ -61,6 +61,35 @@ __global__ void sqrtdiv_kernel(double* out, int iters) {
   if (s == 1234.5) out[0] = s;
 }
 
+__global__ void rsq64h_kernel(double* out, int iters) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = 1.0 + threadIdx.x * 1e-3 + i;
+  double s = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { double y; asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x[i])); x[i] = y; }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 1234.5) out[0] = s;
+}
+
+__global__ void rsqnr_kernel(double* out, int iters) {
+  double x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] = 1.0 + threadIdx.x * 1e-3 + i;
+  double s = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double y; asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x[i]));
+      const double t = x[i] * y; const double e = fma(-t, y, 1.0); const double p = fma(e, 0.375, 0.5);
+      s += fma(y, e * p, y); x[i] += 1e-9; }
+  }
+  if (s == 1234.5) out[0] = s;
+}
+
 int main() {
   cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
   int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
@@ -104,6 +133,23 @@ int main() {
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     cudaEventElapsedTime(&ms, e0, e1);
     printf("1/sqrt(double): %.2f G/s\n", 4.0 * iters * blocks * threads / ms / 1e6);
+  }
+  {
+    int blocks = sms * 8, threads = 256, iters = 20000;
+    float ms;
+    rsq64h_kernel<<<blocks, threads>>>(d, 100); CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    rsq64h_kernel<<<blocks, threads>>>(d, iters);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("MUFU.RSQ64H: %.2f G/s = %.2f per SM per clk at 1965 MHz\n", 8.0 * iters * blocks * threads / ms / 1e6,
+           8.0 * iters * blocks * threads / (ms * 1e-3) / sms / 1.965e9);
+    rsqnr_kernel<<<blocks, threads>>>(d, 100); CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    rsqnr_kernel<<<blocks, threads>>>(d, iters);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("rsqrt_nr (MUFU + 5 DP + add): %.2f G/s\n", 4.0 * iters * blocks * threads / ms / 1e6);
   }
   return 0;
 }

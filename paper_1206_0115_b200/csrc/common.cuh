@@ -113,6 +113,7 @@ struct Level {
   uint32_t* cls_cells = nullptr;   // cell indices grouped by parity class (code & 7)
   uint32_t cls_off[9] = {};        // class offsets into cls_cells (host copy)
   double *multipole = nullptr, *local_own = nullptr, *local_down = nullptr;  // n x ldE
+  double* yt = nullptr;  // M2L compressed intermediates, n x ldY (zero where no source)
   std::vector<uint32_t> block_offsets;
   // far plan (LevelM2L), built by fmmgpu_build_lists
   uint64_t far_pairs = 0;
@@ -138,8 +139,6 @@ struct M2LTables {
   double* dM2 = nullptr;    // [8][rowsB][ldY]
   int2* dRowA = nullptr;    // [8][rowsA]: {slot or -1, destination column in Yt}
   int* dKslot = nullptr;    // [8][ldY]: vector slot of column kk of the target stack, -1 = pad
-  double* dYt = nullptr;    // compressed intermediates, cells x ldY of the largest level
-  size_t yt_cells = 0;
 };
 
 struct Timing {
@@ -177,8 +176,9 @@ struct fmmgpu_ctx {
   double4* d_pw = nullptr;       // Morton-ordered {x,y,z,w}
   uint32_t* d_id = nullptr;      // original index per Morton slot
   uint32_t* d_pcell = nullptr;   // leaf cell per Morton slot
-  double* d_near = nullptr;      // near-field fields [4][n] (Morton order)
-  double* d_far = nullptr;       // far-field fields [4][n] (Morton order)
+  uint32_t* d_inv = nullptr;     // Morton slot per input index (inverse of d_id)
+  double* d_near = nullptr;      // near-field fields [n] x {pot,fx,fy,fz} (Morton order)
+  double* d_far = nullptr;       // far-field fields [n] x {pot,fx,fy,fz} (Morton order)
   double* d_out = nullptr;       // gathered fields [4][n] (input order)
   bool out_valid = false;        // d_out holds near + far of the current arrays
   int* d_flag = nullptr;         // error flags

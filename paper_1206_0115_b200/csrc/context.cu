@@ -81,9 +81,15 @@ __global__ void k_soa(const double4* pw, uint64_t n, double* x, double* y, doubl
   x[i] = p.x; y[i] = p.y; z[i] = p.z; w[i] = p.w;
 }
 
-__global__ void k_sum4(const double* a, const double* b, uint64_t n4, double* out) {
+// Morton-order AoS near + far -> SoA [4][n]
+__global__ void k_sum4(const double4* a, const double4* b, uint64_t n, double* out) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (i < n4) out[i] = a[i] + b[i];
+  if (i >= n) return;
+  const double4 x = a[i], y = b[i];
+  out[i] = x.x + y.x;
+  out[n + i] = x.y + y.y;
+  out[2 * n + i] = x.z + y.z;
+  out[3 * n + i] = x.w + y.w;
 }
 
 void reset_arrays(fmmgpu_ctx* c, cudaStream_t s) {
@@ -478,7 +484,8 @@ int fmmgpu_download_sorted_fields(fmmgpu_ctx* c, double* pot, double* fx, double
     need_tree(c);
     FMM_CUDA(cudaStreamSynchronize(c->s_near));
     double* d = static_cast<double*>(scratch(c, 32 * c->n));
-    k_sum4<<<(4 * c->n + 255) / 256, 256, 0, c->s_far>>>(c->d_far, c->d_near, 4 * c->n, d);
+    k_sum4<<<(c->n + 255) / 256, 256, 0, c->s_far>>>(reinterpret_cast<const double4*>(c->d_far),
+                                                      reinterpret_cast<const double4*>(c->d_near), c->n, d);
     FMM_CUDA(cudaGetLastError());
     double* dst[4] = {pot, fx, fy, fz};
     for (int i = 0; i < 4; ++i)

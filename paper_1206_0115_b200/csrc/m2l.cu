@@ -19,8 +19,9 @@
 //            M1_v over the 189 vectors admissible from a parity-p source; the
 //            epilogue scatters block v of source s to target s - v (if it exists)
 //            into Yt[t] (target-side stacking order);
-//   phase B  local_own[t] += scale * M2_q (l^3 x R) * Yt[t] for targets of parity q,
-//            with the B operand zero-filled where the source t + v does not exist.
+//   phase B  local_own[t] += scale * M2_q (l^3 x R) * Yt[t] for targets of parity q.
+//            Yt is one array per level, zeroed once at allocation; the blocks of
+//            absent sources t + v are never written, so they stay exactly zero.
 // Same arithmetic as the reference (4 l^3 r per pair), on DMMA (mma.sync
 // m8n8k4 f64, the B200 FP64 tensor path: 37.2 TF/s measured, profiles/r01_fp64_peaks.txt).
 #include <cusolverDn.h>
@@ -238,7 +239,6 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
   double* Bs = smem + STAGES * BM * SPAD;         // [STAGES][BN][SPAD]
   __shared__ uint32_t col_cell[BN];
   __shared__ int col_ijk[BN][3];
-  __shared__ signed char vtab[343][3];
 
   const int cls = blockIdx.z;
   const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
@@ -258,15 +258,9 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
     col_ijk[j][1] = ijk[1];
     col_ijk[j][2] = ijk[2];
   }
-  for (int s = tid; s < 343; s += T) {
-    vtab[s][0] = static_cast<signed char>(s / 49 - 3);
-    vtab[s][1] = static_cast<signed char>((s / 7) % 7 - 3);
-    vtab[s][2] = static_cast<signed char>(s % 7 - 3);
-  }
   __syncthreads();
 
   const double* A = g.A + cls * g.a_class_stride + size_t(m0) * g.lda;
-  const int* kslot = PHASE_A ? nullptr : g.kslot + cls * g.ldY;
   const int KT = g.K / BK;
 
   auto load_tile = [&](int stage, int kt) {
@@ -286,17 +280,13 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
         cp16z(bs + j * SPAD + q, g.W + (ok ? size_t(cell) * g.ldE + k0 + q : 0), ok);
       }
     } else {
-      for (int e = tid; e < BN * BK; e += T) {
-        const int j = e / BK, q = e % BK;
+      // Yt rows of absent sources are never written by phase A and stay zero from
+      // the allocation (one Yt per level), so the operand is a plain copy.
+      for (int ch = tid; ch < BN * 8; ch += T) {
+        const int j = ch >> 3, q = (ch & 7) * 2;
         const uint32_t cell = col_cell[j];
-        const int slot = kslot[k0 + q];
-        bool ok = cell != NPOS && slot >= 0;
-        if (ok) {
-          const uint32_t src = find_ijk(g.lv, col_ijk[j][0] + vtab[slot][0], col_ijk[j][1] + vtab[slot][1],
-                                        col_ijk[j][2] + vtab[slot][2]);
-          ok = src != NPOS;
-        }
-        cp8z(bs + j * SPAD + q, g.Yt + (ok ? size_t(cell) * g.ldY + k0 + q : 0), ok);
+        const bool ok = cell != NPOS;
+        cp16z(bs + j * SPAD + q, g.Yt + (ok ? size_t(cell) * g.ldY + k0 + q : 0), ok);
       }
     }
   };
@@ -379,11 +369,9 @@ void m2l_free(fmmgpu_ctx* c) {
   if (T.dM2) cudaFree(T.dM2);
   if (T.dRowA) cudaFree(T.dRowA);
   if (T.dKslot) cudaFree(T.dKslot);
-  if (T.dYt) cudaFree(T.dYt);
-  T.dM1 = T.dM2 = T.dYt = nullptr;
+  T.dM1 = T.dM2 = nullptr;
   T.dRowA = nullptr;
   T.dKslot = nullptr;
-  T.yt_cells = 0;
 }
 
 // Builds transport tables and the stacked per-parity operators from T.u/sigma/v.
@@ -465,6 +453,11 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
       }
     }
   m2l_free(c);
+  for (auto& L : c->lv)  // the Yt layout depends on the ranks: drop stale intermediates
+    if (L.yt) {
+      FMM_CUDA(cudaFree(L.yt));
+      L.yt = nullptr;
+    }
   FMM_CUDA(cudaMalloc(&T.dM1, M1.size() * sizeof(double)));
   FMM_CUDA(cudaMalloc(&T.dM2, M2.size() * sizeof(double)));
   FMM_CUDA(cudaMalloc(&T.dRowA, rowA.size() * sizeof(int2)));
@@ -483,12 +476,10 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   auto& T = c->m2l;
   const Level& L = c->lv[v];
   if (L.n == 0) return;
-  if (T.yt_cells < L.n) {
-    if (T.dYt) FMM_CUDA(cudaFree(T.dYt));
-    size_t cells = L.n;
-    for (const auto& x : c->lv) cells = std::max<size_t>(cells, x.n);
-    FMM_CUDA(cudaMalloc(&T.dYt, cells * T.ldY * sizeof(double)));
-    T.yt_cells = cells;
+  Level& Lm = c->lv[v];
+  if (!Lm.yt) {  // per-level compressed intermediates; zero = "no source" (see phase B)
+    FMM_CUDA(cudaMallocAsync(&Lm.yt, size_t(L.n) * T.ldY * sizeof(double), s));
+    FMM_CUDA(cudaMemsetAsync(Lm.yt, 0, size_t(L.n) * T.ldY * sizeof(double), s));
   }
   GemmArgs g{};
   g.lv = L.view(v);
@@ -496,7 +487,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   std::copy(L.cls_off, L.cls_off + 9, g.cls_off);
   g.W = L.multipole;
   g.ldE = c->ldE;
-  g.Yt = T.dYt;
+  g.Yt = Lm.yt;
   g.ldY = T.ldY;
   g.rowA = T.dRowA;
   g.rowsA = T.rowsA;

@@ -1,89 +1,171 @@
 // Near field (P2P) on the device: the leaf-level 1/r potential and force of
-// p2p_block / p2p_reduce (direct.cpp:111-200), evaluated one-sided per target so
-// every accumulator has exactly one writer (deterministic, no atomics).
+// p2p_block / p2p_reduce (direct.cpp:111-200; pair kernels direct.cpp:9-20),
+// evaluated one-sided per target so every accumulator has exactly one writer
+// (deterministic, no atomics, no P2PBuffers slots).
 //
-// Mapping: one warp = 32 consecutive Morton-ordered targets (usually 1-2 leaf
-// cells). The warp walks the union of its target cells' 27-neighbourhoods
-// (self included) once, each source cell in a warp-uniform loop; every source
-// particle is a broadcast load and each lane masks the interaction to zero when
-// the source cell is not adjacent to its own cell or when it is the lane's own
-// particle (r^2 == 0; coincident distinct particles are rejected at tree build,
-// geometry.cpp:126-136). Per interaction: 3 DADD + 3 DMUL/DFMA (r^2) + 5 DP ops and
-// one MUFU for 1/sqrt (rsqrt_nr) + 7 DP ops of accumulation.
+// Mapping: one CTA per non-empty parent cell (level leaf-1).
+// Its 2x2x2 children are the target cells; the union of their 27-neighbourhoods
+// is the 4x4x4 block of leaf positions around the parent, whose particles are
+// staged ONCE into shared memory as {x,y,z,w} (8 loads per particle per
+// evaluation instead of 27). Warp w owns child octant w: its targets sit in
+// registers, 32 at a time, and every source is a broadcast LDS.128 pair. When
+// fewer than 32 targets remain, the lanes split the sources of each neighbour
+// cell S ways (S = 32 / remaining) and the S partial sums are combined in a fixed
+// order through shared memory, so a 38-particle leaf costs 1.2 passes, not 2.
+// Neighbourhoods larger than the staging capacity (non-uniform clouds) are
+// streamed through shared memory in chunks; targets then accumulate into HBM per
+// chunk, still single-writer.
+//
+// Per interaction: 3 DADD (d) + 3 DP (r^2) + MUFU.RSQ64H and 4 DP (rsqrt_nr)
+// + 1 DMUL (w/r) + 1 DADD (pot) + 2 DMUL (w/r^3) + 3 DFMA (force) = 18 DP ops.
 #include "common.cuh"
 
 namespace fmmgpu {
 
 namespace {
 
+constexpr int P2P_WARPS = 8;             // one per child octant
+constexpr int P2P_THREADS = P2P_WARPS * 32;
+constexpr int P2P_CAP = 3072;            // staged particles per chunk (96 KB), multiple of 4
+
 struct P2PArgs {
   LevelView leaf;
-  const uint32_t* first;
-  const uint32_t* count;
-  const uint32_t* pcell;
+  const uint64_t* parent_code;  // level leaf-1
+  const uint32_t* first;        // leaf first_particle
+  const uint32_t* count;        // leaf particle_count
   const double4* pw;
-  double* near;  // [4][n]
+  double4* near;  // [n] x {pot, fx, fy, fz}, Morton order
   uint64_t n;
 };
 
-__device__ __forceinline__ bool adjacent(const int a[3], const int b[3]) {
-  return abs(a[0] - b[0]) <= 1 && abs(a[1] - b[1]) <= 1 && abs(a[2] - b[2]) <= 1;
+struct P2PSmem {
+  double4 src[P2P_CAP];
+  double red[P2P_WARPS][4][32];
+  uint32_t first[64];
+  uint32_t cnt[64];
+  uint32_t voff[65];  // virtual offsets of the 64 positions (prefix sum of counts padded to 4)
+};
+
+// A staged source that contributes exactly zero: w = 0 far away (finite r^2, so
+// w/r and w/r^3 are +0 and the accumulators are unchanged bit for bit).
+__device__ __forceinline__ double4 dummy_source() { return make_double4(1e100, 1e100, 1e100, 0.0); }
+
+__device__ __forceinline__ void interact(const double xi, const double yi, const double zi, const double4 pj,
+                                         double& pot, double& fx, double& fy, double& fz) {
+  const double dx = xi - pj.x, dy = yi - pj.y, dz = zi - pj.z;
+  const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+  double inv = rsqrt_nr(r2);
+  // i == j gives r^2 = +0 exactly (coincident distinct particles are rejected at
+  // build): an integer test on the high word keeps the select off the FP64 pipe.
+  inv = __double2hiint(r2) != 0 ? inv : 0.0;
+  const double winv = pj.w * inv;
+  pot += winv;
+  const double s3 = winv * (inv * inv);
+  fx = fma(s3, dx, fx);
+  fy = fma(s3, dy, fy);
+  fz = fma(s3, dz, fz);
 }
 
-__global__ void __launch_bounds__(256) k_p2p(const P2PArgs a) {
-  const uint64_t wid = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint64_t base = wid * 32;
-  if (base >= a.n) return;
-  const uint64_t s = base + lane;
-  const bool valid = s < a.n;
-  const uint64_t sc = valid ? s : a.n - 1;
-  const uint32_t my_cell = a.pcell[sc];
-  int my[3];
-  demorton(a.leaf.code[my_cell], my);
-  const double4 xi = a.pw[sc];
-  const uint32_t c_first = a.pcell[base];
-  const uint32_t c_last = a.pcell[(base + 31 < a.n) ? base + 31 : a.n - 1];
+__global__ void __launch_bounds__(P2P_THREADS, 2) k_p2p(const P2PArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  P2PSmem& sm = *reinterpret_cast<P2PSmem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  double pot = 0, fx = 0, fy = 0, fz = 0;
-  for (uint32_t tc = c_first; tc <= c_last; ++tc) {
-    int t[3];
-    demorton(a.leaf.code[tc], t);
-    for (int o = 0; o < 27; ++o) {
-      const int sx = t[0] + o / 9 - 1, sy = t[1] + (o / 3) % 3 - 1, sz = t[2] + o % 3 - 1;
-      const uint32_t scell = find_ijk(a.leaf, sx, sy, sz);
-      if (scell == NPOS) continue;
-      const int sijk[3] = {sx, sy, sz};
-      bool dup = false;  // already visited through an earlier target cell of this warp
-      for (uint32_t pc = c_first; pc < tc && !dup; ++pc) {
-        int p[3];
-        demorton(a.leaf.code[pc], p);
-        dup = adjacent(p, sijk);
+  int pc[3];
+  demorton(a.parent_code[blockIdx.x], pc);
+  if (tid < 64) {
+    const int qa = tid >> 4, qb = (tid >> 2) & 3, qc = tid & 3;
+    const uint32_t cell = find_ijk(a.leaf, 2 * pc[0] - 1 + qa, 2 * pc[1] - 1 + qb, 2 * pc[2] - 1 + qc);
+    const uint32_t cnt = cell == NPOS ? 0u : a.count[cell];
+    sm.first[tid] = cell == NPOS ? 0u : a.first[cell];
+    sm.cnt[tid] = cnt;
+    // inclusive warp scan over the 64 padded counts (two warps), then fix up
+    uint32_t x = (cnt + 3u) & ~3u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((tid & 31) >= o) x += y;
+    }
+    sm.voff[tid + 1] = x;
+    if (tid == 0) sm.voff[0] = 0;
+  }
+  __syncthreads();
+  if (tid >= 33 && tid <= 64) sm.voff[tid] += sm.voff[32];
+  __syncthreads();
+  const uint32_t total = sm.voff[64];
+
+  // this warp's target cell: child octant `warp` at local position (1+a, 1+b, 1+c)
+  const int ca = (warp >> 2) & 1, cb = (warp >> 1) & 1, cc = warp & 1;
+  const int tpos = ((1 + ca) << 4) | ((1 + cb) << 2) | (1 + cc);
+  const uint32_t nT = sm.cnt[tpos];
+  const uint32_t tfirst = sm.first[tpos];
+
+  for (uint32_t base = 0; base < total; base += P2P_CAP) {
+    const uint32_t clen = min(static_cast<uint32_t>(P2P_CAP), total - base);
+    if (base) __syncthreads();
+    for (uint32_t i = tid; i < clen; i += P2P_THREADS) {
+      const uint32_t v = base + i;
+      int lo = 0, hi = 63;  // last position with voff[pos] <= v
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sm.voff[mid] <= v) lo = mid; else hi = mid - 1;
       }
-      if (dup) continue;
-      const bool use = valid && adjacent(my, sijk);
-      const uint32_t j0 = a.first[scell], j1 = j0 + a.count[scell];
-#pragma unroll 4
-      for (uint32_t j = j0; j < j1; ++j) {
-        const double4 pj = a.pw[j];
-        const double dx = xi.x - pj.x, dy = xi.y - pj.y, dz = xi.z - pj.z;
-        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-        double inv = rsqrt_nr(r2);
-        inv = (use && r2 > 0.0) ? inv : 0.0;
-        const double winv = pj.w * inv;
-        pot += winv;
-        const double s3 = winv * inv * inv;
-        fx = fma(s3, dx, fx);
-        fy = fma(s3, dy, fy);
-        fz = fma(s3, dz, fz);
+      const uint32_t k = v - sm.voff[lo];
+      sm.src[i] = k < sm.cnt[lo] ? a.pw[sm.first[lo] + k] : dummy_source();
+    }
+    __syncthreads();
+
+    for (uint32_t t0 = 0; t0 < nT; t0 += 32) {
+      const uint32_t m = min(32u, nT - t0);
+      const uint32_t S = 32u / m;
+      const uint32_t lt = lane % m, split = lane / m;
+      const bool active = split < S;
+      const uint64_t tg = uint64_t(tfirst) + t0 + lt;
+      const double4 xi = a.pw[tg];
+      double pot = 0, fx = 0, fy = 0, fz = 0;
+      if (active) {
+#pragma unroll 1
+        for (int q = 0; q < 27; ++q) {
+          const int pos = ((ca + q / 9) << 4) | ((cb + (q / 3) % 3) << 2) | (cc + q % 3);
+          // intersection of the position's virtual range with this chunk, chunk-relative
+          // (segments are padded to groups of 4 and chunks are multiples of 4)
+          const uint32_t v0 = max(sm.voff[pos], base), v1 = min(sm.voff[pos + 1], base + clen);
+          const int g1 = static_cast<int>(v1 - base) >> 2;
+          for (int g = (static_cast<int>(v0 - base) >> 2) + static_cast<int>(split); g < g1; g += S) {
+            const double4* sj = sm.src + 4 * g;
+            const double4 p0 = sj[0], p1 = sj[1], p2 = sj[2], p3 = sj[3];
+            interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
+            interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
+            interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
+            interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
+          }
+        }
+      }
+      if (S > 1) {  // combine the S source splits of each target in a fixed order
+        sm.red[warp][0][lane] = pot;
+        sm.red[warp][1][lane] = fx;
+        sm.red[warp][2][lane] = fy;
+        sm.red[warp][3][lane] = fz;
+        __syncwarp();
+        if (lane < m) {
+          for (uint32_t s = 1; s < S; ++s) {
+            pot += sm.red[warp][0][lane + s * m];
+            fx += sm.red[warp][1][lane + s * m];
+            fy += sm.red[warp][2][lane + s * m];
+            fz += sm.red[warp][3][lane + s * m];
+          }
+        }
+        __syncwarp();
+      }
+      if (lane < m) {
+        double4 r = a.near[tg];
+        r.x += pot;
+        r.y += fx;
+        r.z += fy;
+        r.w += fz;
+        a.near[tg] = r;
       }
     }
-  }
-  if (valid) {
-    a.near[s] += pot;
-    a.near[a.n + s] += fx;
-    a.near[2 * a.n + s] += fy;
-    a.near[3 * a.n + s] += fz;
   }
 }
 
@@ -92,10 +174,13 @@ __global__ void __launch_bounds__(256) k_p2p(const P2PArgs a) {
 void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const int leaf = c->height - 1;
   const Level& L = c->lv[leaf];
-  P2PArgs a{L.view(leaf), L.first_particle, L.particle_count, c->d_pcell, c->d_pw, c->d_near, c->n};
-  const uint64_t warps = (c->n + 31) / 32;
-  const unsigned blocks = static_cast<unsigned>((warps * 32 + 255) / 256);
-  k_p2p<<<blocks, 256, 0, s>>>(a);
+  const Level& P = c->lv[leaf - 1];
+  if (P.n == 0) return;
+  P2PArgs a{L.view(leaf), P.code, L.first_particle, L.particle_count, c->d_pw,
+             reinterpret_cast<double4*>(c->d_near), c->n};
+  const int smem = static_cast<int>(sizeof(P2PSmem));
+  FMM_CUDA(cudaFuncSetAttribute(k_p2p, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_p2p<<<P.n, P2P_THREADS, smem, s>>>(a);
   FMM_CUDA(cudaGetLastError());
   ++c->launches;
 }

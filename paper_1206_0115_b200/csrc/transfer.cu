@@ -79,7 +79,7 @@ struct LeafArgs {
   const double* tn;
   double* expansion;       // multipole (P2M) or local_own (L2P)
   const double* down;      // local_down (L2P)
-  double* far;             // [4][n] (L2P)
+  double* far;             // [n] x {pot, fx, fy, fz} (L2P), Morton order
   uint64_t n;
   uint32_t ncells;
   int ldE;
@@ -183,10 +183,13 @@ __global__ void __launch_bounds__(128) k_l2p(LeafArgs a) {
     }
   }
   (void)L3;
-  a.far[s] += pot;
-  a.far[a.n + s] -= inv * dx;
-  a.far[2 * a.n + s] -= inv * dy;
-  a.far[3 * a.n + s] -= inv * dz;
+  double4* f = reinterpret_cast<double4*>(a.far) + s;
+  double4 r = *f;
+  r.x += pot;
+  r.y -= inv * dx;
+  r.z -= inv * dy;
+  r.w -= inv * dz;
+  *f = r;
 }
 
 struct TransArgs {
@@ -264,13 +267,18 @@ __global__ void __launch_bounds__(128) k_transfer(TransArgs a) {
   }
 }
 
-__global__ void k_gather(const double* __restrict__ far, const double* __restrict__ near,
-                         const uint32_t* __restrict__ id, uint64_t n, double* __restrict__ out) {
-  const uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (s >= n) return;
-  const uint32_t o = id[s];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) out[k * n + o] = far[k * n + s] + near[k * n + s];
+// FmmContext::gather (bench.cpp:350-365): input slot o reads its Morton slot
+// inv[o] (one 32-byte sector per field array) and writes the four fields coalesced.
+__global__ void k_gather(const double4* __restrict__ far, const double4* __restrict__ near,
+                         const uint32_t* __restrict__ inv, uint64_t n, double* __restrict__ out) {
+  const uint64_t o = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (o >= n) return;
+  const uint32_t s = inv[o];
+  const double4 f = far[s], e = near[s];
+  out[o] = f.x + e.x;
+  out[n + o] = f.y + e.y;
+  out[2 * n + o] = f.z + e.z;
+  out[3 * n + o] = f.w + e.w;
 }
 
 Geo make_geo(const fmmgpu_ctx* c, int level) {
@@ -438,7 +446,8 @@ void launch_l2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
 }
 
 void launch_gather(fmmgpu_ctx* c, cudaStream_t s) {
-  k_gather<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, s>>>(c->d_far, c->d_near, c->d_id, c->n, c->d_out);
+  k_gather<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<const double4*>(c->d_far), reinterpret_cast<const double4*>(c->d_near), c->d_inv, c->n, c->d_out);
   FMM_CUDA(cudaGetLastError());
   ++c->launches;
 }

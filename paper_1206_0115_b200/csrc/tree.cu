@@ -76,9 +76,13 @@ __global__ void k_keys(const double4* __restrict__ p, uint64_t n, double lo0, do
 }
 
 __global__ void k_permute(const double4* __restrict__ in, const uint32_t* __restrict__ idx, uint64_t n,
-                          double4* __restrict__ out) {
+                          double4* __restrict__ out, uint32_t* __restrict__ inv) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (i < n) out[i] = in[idx[i]];
+  if (i < n) {
+    const uint32_t o = idx[i];
+    out[i] = in[o];
+    inv[o] = static_cast<uint32_t>(i);
+  }
 }
 
 // leaf cell of every Morton slot, and the coincident-particle check
@@ -130,7 +134,7 @@ inline unsigned blocks(uint64_t n, int t) { return static_cast<unsigned>((n + t 
 void free_level(fmmgpu::Level& L, cudaStream_t s) {
   dfree(L.code, s); dfree(L.first_particle, s); dfree(L.particle_count, s); dfree(L.parent, s);
   dfree(L.first_child, s); dfree(L.child_count, s); dfree(L.map, s); dfree(L.cls_cells, s);
-  dfree(L.multipole, s); dfree(L.local_own, s); dfree(L.local_down, s);
+  dfree(L.multipole, s); dfree(L.local_own, s); dfree(L.local_down, s); dfree(L.yt, s);
   dfree(L.far_target, s); dfree(L.far_source, s); dfree(L.far_vec, s); dfree(L.far_group_off, s);
   L.far_pairs = 0;
 }
@@ -150,7 +154,7 @@ void tree_free(fmmgpu_ctx* c) {
   cudaStream_t s = c->s_far;
   for (auto& L : c->lv) free_level(L, s);
   c->lv.clear();
-  dfree(c->d_pw, s); dfree(c->d_id, s); dfree(c->d_pcell, s);
+  dfree(c->d_pw, s); dfree(c->d_id, s); dfree(c->d_inv, s); dfree(c->d_pcell, s);
   dfree(c->d_near, s); dfree(c->d_far, s); dfree(c->d_out, s);
   c->have_tree = false;
 }
@@ -231,7 +235,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
                                            std::max(1, 3 * leaf), s));
   c->d_pw = dalloc<double4>(n, s);
-  k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw);
+  c->d_inv = dalloc<uint32_t>(n, s);
+  k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw, c->d_inv);
   FMM_CUDA(cudaGetLastError());
 
   // leaf cells = runs of equal keys (geometry.cpp:113-122)

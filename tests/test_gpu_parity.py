@@ -235,12 +235,23 @@ def test_edge_cases(fmm):
     c.evaluate()
     g = c.gather()
     assert all(np.all(x == 0) for x in g)
-    # two particles in adjacent leaves: direct interaction only (test_direct.cpp:43-45)
+    # two particles in adjacent leaves of an explicit root cube: direct interaction only
+    # (pair kernels, direct.cpp:9-20; F = w (x - y) / r^3, test_direct.cpp:43-45)
+    two = np.array([[0.1, 0.1, 0.1, 1.0], [0.3, 0.1, 0.1, 1.0]])
+    c.build_tree(two, 3, root=[0.5, 0.5, 0.5, 1.0])
+    c.evaluate()
+    g = c.gather()
+    assert np.allclose(g[0], [5.0, 5.0], rtol=1e-15, atol=0)
+    assert np.allclose(g[1], [-25.0, 25.0], rtol=1e-14, atol=0)
+    assert np.all(g[2] == 0) and np.all(g[3] == 0)
+    # two particles spanning the bounding cube land in leaves 0 and 3 (geometry.cpp:18-36,
+    # 82-94): far field only, so the FMM value (not 1/r) is what the reference returns
     two = np.array([[0.0, 0.0, 0.0, 1.0], [0.5, 0.0, 0.0, 1.0]])
     c.build_tree(two, 3)
     c.evaluate()
     g = c.gather()
-    assert abs(g[0][0] - 2.0) < 1e-15 and abs(g[1][0] + 4.0) < 1e-14
+    of = OracleTree(two, 3).evaluate(OracleOps.cached(3))
+    assert relative_l2_error(g[0], of[0]) <= TOL and force_error(*g[1:], *of[1:]) <= TOL
     # two particles three leaves apart: far field only, as in the reference
     two = np.array([[0.0, 0.0, 0.0, 1.0], [2.0, 0.0, 0.0, 1.0]])
     c.build_tree(two, 3)

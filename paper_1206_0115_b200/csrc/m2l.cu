@@ -223,14 +223,21 @@ struct GemmArgs {
   int ldY;
   const int2* rowA;       // phase A epilogue table [8][rowsA]
   int rowsA;
-  const int* kslot;       // phase B mask table [8][ldY]
+  const int* kslot;       // vector slot per target-stack column [8][ldY] (host tables)
   double* local;          // phase B output (local_own)
+  int ksplit;             // phase B split-K factor (1 = accumulate directly)
+  double* part;           // phase B split-K partials [ksplit][ncells][ldE]
+  uint32_t ncells;
   int l3;
   double scale;
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool PHASE_A>
-__global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
+// Phase B: local_own[t] += scale * M2_q (rowsB x ldY) * Yt[t] for the targets t of
+// parity class q. Optional deterministic split-K for levels too small to fill the
+// GPU: split s writes its partial sums to part[s][t][row] and k_m2l_splitk_reduce
+// adds them in split order.
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
   constexpr int T = WM * WN * 32;
   constexpr int WTM = BM / WM, WTN = BN / WN;
   constexpr int MT = WTM / 8, NT = WTN / 8;
@@ -238,9 +245,8 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
   double* As = smem;                              // [STAGES][BM][SPAD]
   double* Bs = smem + STAGES * BM * SPAD;         // [STAGES][BN][SPAD]
   __shared__ uint32_t col_cell[BN];
-  __shared__ int col_ijk[BN][3];
 
-  const int cls = blockIdx.z;
+  const int cls = blockIdx.z / g.ksplit, split = blockIdx.z % g.ksplit;
   const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
   const uint32_t n0 = blockIdx.y * BN;
   if (n0 >= ncls) return;
@@ -249,45 +255,30 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
   const int wm = warp / WN, wn = warp % WN;
   const int gq = lane >> 2, tq = lane & 3;
 
-  for (int j = tid; j < BN; j += T) {
-    const uint32_t cell = (n0 + j < ncls) ? g.cls_cells[g.cls_off[cls] + n0 + j] : NPOS;
-    col_cell[j] = cell;
-    int ijk[3] = {0, 0, 0};
-    if (cell != NPOS) demorton(g.lv.code[cell], ijk);
-    col_ijk[j][0] = ijk[0];
-    col_ijk[j][1] = ijk[1];
-    col_ijk[j][2] = ijk[2];
-  }
+  for (int j = tid; j < BN; j += T) col_cell[j] = (n0 + j < ncls) ? g.cls_cells[g.cls_off[cls] + n0 + j] : NPOS;
   __syncthreads();
 
   const double* A = g.A + cls * g.a_class_stride + size_t(m0) * g.lda;
-  const int KT = g.K / BK;
+  const int KTALL = g.K / BK;
+  const int per = (KTALL + g.ksplit - 1) / g.ksplit;
+  const int kt0 = split * per;
+  const int KT = max(0, min(KTALL, kt0 + per) - kt0);
 
   auto load_tile = [&](int stage, int kt) {
-    const int k0 = kt * BK;
+    const int k0 = (kt0 + kt) * BK;
     double* as = As + stage * BM * SPAD;
     double* bs = Bs + stage * BN * SPAD;
-    // A: BM rows x 16 doubles as 16-byte chunks
     for (int ch = tid; ch < BM * 8; ch += T) {
       const int r = ch >> 3, q = (ch & 7) * 2;
       cp16(as + r * SPAD + q, A + size_t(r) * g.lda + k0 + q);
     }
-    if (PHASE_A) {
-      for (int ch = tid; ch < BN * 8; ch += T) {
-        const int j = ch >> 3, q = (ch & 7) * 2;
-        const uint32_t cell = col_cell[j];
-        const bool ok = cell != NPOS;
-        cp16z(bs + j * SPAD + q, g.W + (ok ? size_t(cell) * g.ldE + k0 + q : 0), ok);
-      }
-    } else {
-      // Yt rows of absent sources are never written by phase A and stay zero from
-      // the allocation (one Yt per level), so the operand is a plain copy.
-      for (int ch = tid; ch < BN * 8; ch += T) {
-        const int j = ch >> 3, q = (ch & 7) * 2;
-        const uint32_t cell = col_cell[j];
-        const bool ok = cell != NPOS;
-        cp16z(bs + j * SPAD + q, g.Yt + (ok ? size_t(cell) * g.ldY + k0 + q : 0), ok);
-      }
+    // Yt blocks of absent sources were never written by phase A and stay zero from
+    // the allocation (one Yt per level), so the operand is a plain copy.
+    for (int ch = tid; ch < BN * 8; ch += T) {
+      const int j = ch >> 3, q = (ch & 7) * 2;
+      const uint32_t cell = col_cell[j];
+      const bool ok = cell != NPOS;
+      cp16z(bs + j * SPAD + q, g.Yt + (ok ? size_t(cell) * g.ldY + k0 + q : 0), ok);
     }
   };
 
@@ -298,8 +289,8 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_tile(s, s);
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < KT) load_tile(st, st);
     cp_commit();
   }
   for (int kt = 0; kt < KT; ++kt) {
@@ -329,36 +320,153 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_gemm(const GemmArgs g) {
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
     const int row = m0 + wm * WTM + i * 8 + gq;
-    if (PHASE_A) {
-      const int2 info = g.rowA[cls * g.rowsA + row];
-      if (info.x < 0) continue;
-      const int vx = info.x / 49 - 3, vy = (info.x / 7) % 7 - 3, vz = info.x % 7 - 3;
+    if (row >= g.l3) continue;
 #pragma unroll
-      for (int j = 0; j < NT; ++j)
+    for (int j = 0; j < NT; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = wn * WTN + j * 8 + 2 * tq + e;
-          if (col_cell[col] == NPOS) continue;
-          const uint32_t t = find_ijk(g.lv, col_ijk[col][0] - vx, col_ijk[col][1] - vy, col_ijk[col][2] - vz);
-          if (t != NPOS) g.Yt[size_t(t) * g.ldY + info.y] = acc[i][j][e];
-        }
-    } else {
-      if (row >= g.l3) continue;
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = wn * WTN + j * 8 + 2 * tq + e;
-          const uint32_t t = col_cell[col];
-          if (t == NPOS) continue;
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * WTN + j * 8 + 2 * tq + e;
+        const uint32_t t = col_cell[col];
+        if (t == NPOS) continue;
+        if (g.ksplit == 1) {
           double* out = g.local + size_t(t) * g.ldE + row;
           *out += g.scale * acc[i][j][e];
+        } else {
+          g.part[(size_t(split) * g.ncells + t) * g.ldE + row] = acc[i][j][e];
         }
-    }
+      }
   }
 }
 
-constexpr int A_BM = 64, A_BN = 64, A_WM = 2, A_WN = 2, A_ST = 3;
+__global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit, uint32_t ncells, int ldE, int l3,
+                                    double scale, double* __restrict__ local) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= uint64_t(ncells) * ldE) return;
+  if (static_cast<int>(i % ldE) >= l3) return;
+  double s = part[i];
+  for (int k = 1; k < ksplit; ++k) s += part[k * uint64_t(ncells) * ldE + i];
+  local[i] += scale * s;
+}
+
+// Phase A, W-resident: one CTA owns BN source columns of one parity class. Their
+// multipoles (BN x K) are staged ONCE in shared memory and the whole stacked operator
+// M1_p (R rows) streams past them in BM x BK slices through a cp.async ring that
+// runs across M-tile boundaries, so the scatter epilogue of one M-tile overlaps the
+// loads of the next and no CTA pays a pipeline ramp per 64 x 64 tile.
+constexpr int PA_BM = 64, PA_BK = 16, PA_ST = 4, PA_THREADS = 256;
+
+template <int BN, int WM, int WN>
+__global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g) {
+  static_assert(WM * WN * 32 == PA_THREADS, "8 warps");
+  constexpr int WTM = PA_BM / WM, WTN = BN / WN;
+  constexpr int MT = WTM / 8, NT = WTN / 8;
+  extern __shared__ __align__(16) double smem[];
+  const int wpad = g.K + 4;                       // == 4 (mod 16): conflict-free fragments
+  double* Ws = smem;                              // [BN][wpad]
+  double* As = smem + BN * wpad;                  // [PA_ST][PA_BM][SPAD]
+  __shared__ uint32_t col_cell[BN];
+  __shared__ int col_ijk[BN][3];
+
+  const int cls = blockIdx.y;
+  const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
+  const uint32_t n0 = blockIdx.x * BN;
+  if (n0 >= ncls) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / WN, wn = warp % WN;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  for (int j = tid; j < BN; j += PA_THREADS) {
+    const uint32_t cell = (n0 + j < ncls) ? g.cls_cells[g.cls_off[cls] + n0 + j] : NPOS;
+    col_cell[j] = cell;
+    int ijk[3] = {0, 0, 0};
+    if (cell != NPOS) demorton(g.lv.code[cell], ijk);
+    col_ijk[j][0] = ijk[0];
+    col_ijk[j][1] = ijk[1];
+    col_ijk[j][2] = ijk[2];
+  }
+  __syncthreads();
+  // resident operand: the BN multipoles (zero columns past the end of the class)
+  const int kc = g.K / 2;  // 16-byte chunks per column
+  for (int ch = tid; ch < BN * kc; ch += PA_THREADS) {
+    const int j = ch / kc, q = (ch % kc) * 2;
+    const uint32_t cell = col_cell[j];
+    const bool ok = cell != NPOS;
+    cp16z(Ws + j * wpad + q, g.W + (ok ? size_t(cell) * g.ldE + q : 0), ok);
+  }
+  cp_commit();
+
+  const double* A = g.A + cls * g.a_class_stride;
+  const int KT = g.K / PA_BK;
+  const int MTILES = g.rowsA / PA_BM;
+  const int TOTAL = MTILES * KT;
+  auto load_a = [&](int t) {
+    const int mt = t / KT, kt = t % KT;
+    double* as = As + (t % PA_ST) * PA_BM * SPAD;
+    const double* src = A + size_t(mt * PA_BM) * g.lda + kt * PA_BK;
+    for (int ch = tid; ch < PA_BM * (PA_BK / 2); ch += PA_THREADS) {
+      const int r = ch / (PA_BK / 2), q = (ch % (PA_BK / 2)) * 2;
+      cp16(as + r * SPAD + q, src + size_t(r) * g.lda + q);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < PA_ST - 1; ++s) {
+    if (s < TOTAL) load_a(s);
+    cp_commit();
+  }
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int t = 0; t < TOTAL; ++t) {
+    cp_wait<PA_ST - 2>();
+    __syncthreads();
+    if (t + PA_ST - 1 < TOTAL) load_a(t + PA_ST - 1);
+    cp_commit();
+    const int mt = t / KT, kt = t % KT;
+    const double* as = As + (t % PA_ST) * PA_BM * SPAD + (wm * WTM + gq) * SPAD + tq;
+    const double* bs = Ws + (wn * WTN + gq) * wpad + kt * PA_BK + tq;
+#pragma unroll
+    for (int kk = 0; kk < PA_BK; kk += 4) {
+      double a[MT], b[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[i] = as[i * 8 * SPAD + kk];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = bs[j * 8 * wpad + kk];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    if (kt == KT - 1) {
+      // scatter block v of source s to target s - v, target-side column info.y
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int row = mt * PA_BM + wm * WTM + i * 8 + gq;
+        const int2 info = __ldg(g.rowA + cls * g.rowsA + row);
+        if (info.x >= 0) {
+          const int vx = info.x / 49 - 3, vy = (info.x / 7) % 7 - 3, vz = info.x % 7 - 3;
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = wn * WTN + j * 8 + 2 * tq + e;
+              if (col_cell[col] == NPOS) continue;
+              const uint32_t tcell =
+                  find_ijk(g.lv, col_ijk[col][0] - vx, col_ijk[col][1] - vy, col_ijk[col][2] - vz);
+              if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + info.y] = acc[i][j][e];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
 constexpr int B_BM = 128, B_BN = 64, B_WM = 4, B_WN = 2, B_ST = 3;
 
 }  // namespace
@@ -422,7 +530,7 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   }
   T.R = R;
   T.ldY = round_up(R, 16);
-  T.rowsA = round_up(R, A_BM);
+  T.rowsA = round_up(R, PA_BM);
   T.rowsB = round_up(n3, B_BM);
   std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
   std::vector<int2> rowA(size_t(8) * T.rowsA, make_int2(-1, 0));
@@ -503,24 +611,45 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.lda = c->ldE;
     g.a_class_stride = size_t(T.rowsA) * c->ldE;
     g.K = c->ldE;
-    const size_t smem = sizeof(double) * A_ST * (A_BM + A_BN) * SPAD;
-    auto kern = k_m2l_gemm<A_BM, A_BN, A_WM, A_WN, A_ST, true>;
-    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    dim3 grid(T.rowsA / A_BM, (maxcls + A_BN - 1) / A_BN, 8);
-    kern<<<grid, A_WM * A_WN * 32, smem, s>>>(g);
-    FMM_CUDA(cudaGetLastError());
+    // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
+    auto launch = [&](auto kern, int bn) {
+      const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * SPAD);
+      FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      dim3 grid((maxcls + bn - 1) / bn, 8);
+      kern<<<grid, PA_THREADS, smem, s>>>(g);
+      FMM_CUDA(cudaGetLastError());
+    };
+    if (c->ldE <= 128) launch(k_m2l_phase_a<64, 2, 4>, 64);
+    else if (c->ldE <= 352) launch(k_m2l_phase_a<32, 4, 2>, 32);
+    else launch(k_m2l_phase_a<16, 8, 1>, 16);
   }
   {
     g.A = T.dM2;
     g.lda = T.ldY;
     g.a_class_stride = size_t(T.rowsB) * T.ldY;
     g.K = T.ldY;
+    g.ncells = L.n;
+    // deterministic split-K when the level has too few column tiles to fill 2 CTAs/SM
+    const int mtiles = T.rowsB / B_BM;
+    const uint32_t ctas = 8u * ((maxcls + B_BN - 1) / B_BN) * mtiles;
+    const int kt = T.ldY / BK;
+    int ks = 1;
+    while (ks < 16 && ctas * ks < 2u * 148u && kt / (2 * ks) >= 8) ks *= 2;
+    g.ksplit = ks;
+    g.part = ks > 1 ? static_cast<double*>(scratch(c, sizeof(double) * ks * size_t(L.n) * c->ldE)) : nullptr;
     const size_t smem = sizeof(double) * B_ST * (B_BM + B_BN) * SPAD;
-    auto kern = k_m2l_gemm<B_BM, B_BN, B_WM, B_WN, B_ST, false>;
+    auto kern = k_m2l_phase_b<B_BM, B_BN, B_WM, B_WN, B_ST>;
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    dim3 grid(T.rowsB / B_BM, (maxcls + B_BN - 1) / B_BN, 8);
+    dim3 grid(mtiles, (maxcls + B_BN - 1) / B_BN, 8 * ks);
     kern<<<grid, B_WM * B_WN * 32, smem, s>>>(g);
     FMM_CUDA(cudaGetLastError());
+    if (ks > 1) {
+      const uint64_t tot = uint64_t(L.n) * c->ldE;
+      k_m2l_splitk_reduce<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(g.part, ks, L.n, c->ldE, c->l3,
+                                                                                     g.scale, L.local_own);
+      FMM_CUDA(cudaGetLastError());
+      ++c->launches;
+    }
   }
   c->launches += 2;
 }

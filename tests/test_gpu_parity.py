@@ -24,6 +24,11 @@ CASES = [
     (5000, 5, 4, "sphere", 7, False),
     (3000, 4, 3, "uniform", 11, True),
     (20000, 5, 5, "uniform", 3, True),
+    # ~470 particles per leaf: the P2P neighbourhood (30000 particles) streams through
+    # shared memory in 10 chunks, and every target cell takes >= 15 passes
+    (30000, 3, 3, "uniform", 5, True),
+    # surface cloud: ragged leaves from 1 to ~300 particles (source splits S = 1..32)
+    (20000, 4, 4, "sphere", 9, True),
 ]
 
 

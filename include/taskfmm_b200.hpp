@@ -1,0 +1,212 @@
+// taskfmm_b200.hpp — header-only C++ mirror of the reference's operator API over the
+// C ABI of fmmgpu.h (libfmmgpu.so, CUDA sm_100a). A C++ caller of the reference
+// ("taskfmm", /root/reference/proj/include/taskfmm/*.hpp) switches its FMM evaluation
+// path by replacing `taskfmm::` with `taskfmm_b200::` for the names below; the
+// semantics (accumulate contract, input-order fields, exception classes) are the
+// reference's. See INTEGRATION.md.
+//
+//   Particle, Cube                     geometry.hpp:16-24
+//   TaskKind, Task                     taskflow.hpp:15-31
+//   RunConfig, Distribution            bench.hpp:19-35
+//   generate_particles                 bench.cpp:29-61 (same mt19937_64 stream)
+//   relative_l2_error                  bench.cpp:91-100
+//   FmmContext (ctor, reset, run_task, gather, setup_seconds)   bench.hpp:86-121
+//   run_fmm (no oracle check, no writers)                       bench.cpp:415-469
+//
+// Granularity: the device runs one launch per (operator, level). run_task(task)
+// executes the level launch of (task.kind, task.level) on the first task of that pair
+// since the last reset() and is a no-op for the remaining blocks, so executing a whole
+// reference TaskGraph (any valid order) reproduces one evaluation. P2PReduce is folded
+// into P2P (one-sided owner-computes, no slot buffers).
+#pragma once
+
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fmmgpu.h"
+
+namespace taskfmm_b200 {
+
+struct Particle {
+  std::array<double, 3> position;
+  double weight;
+};
+
+struct Cube {
+  std::array<double, 3> center{0.5, 0.5, 0.5};
+  double width = 1.0;
+};
+
+enum class TaskKind : std::uint8_t { P2M, M2M, M2L, L2L, L2P, P2P, P2PReduce };
+inline constexpr int TASK_KIND_COUNT = 7;
+
+struct Task {
+  std::uint32_t id = 0;
+  TaskKind kind = TaskKind::P2M;
+  std::int16_t level = 0;
+  std::uint32_t block = 0;
+  std::uint64_t work = 0;
+};
+
+enum class Distribution { Uniform, Sphere };
+
+struct RunConfig {
+  std::uint64_t n = 10000;
+  Distribution dist = Distribution::Uniform;
+  int height = 4;
+  int acc = 5;  // interpolation order l = acc, svd eps = 10^-acc
+  int group_size = 250;
+  std::uint64_t seed = 42;
+  int device = 0;
+};
+
+// status code -> the reference's exception class
+inline void check(int rc, const char* msg) {
+  switch (rc) {
+    case FMMGPU_OK: return;
+    case FMMGPU_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case FMMGPU_DOMAIN_ERROR: throw std::domain_error(msg);
+    case FMMGPU_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case FMMGPU_LOGIC_ERROR: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+inline std::vector<Particle> generate_particles(std::uint64_t n, Distribution dist, std::uint64_t seed) {
+  std::vector<double> xyzw(4 * n);
+  fmmgpu_generate_particles(n, dist == Distribution::Uniform ? 0 : 1, seed, xyzw.data());
+  std::vector<Particle> out(n);
+  for (std::uint64_t i = 0; i < n; ++i)
+    out[i] = Particle{{xyzw[4 * i], xyzw[4 * i + 1], xyzw[4 * i + 2]}, xyzw[4 * i + 3]};
+  return out;
+}
+
+inline double relative_l2_error(std::span<const double> estimate, std::span<const double> reference) {
+  if (estimate.size() != reference.size()) throw std::invalid_argument("relative_l2_error: size mismatch");
+  double num = 0, den = 0;
+  for (std::size_t i = 0; i < estimate.size(); ++i) {
+    const double d = estimate[i] - reference[i];
+    num += d * d;
+    den += reference[i] * reference[i];
+  }
+  return den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+}
+
+class FmmContext {
+ public:
+  struct Fields {
+    std::vector<double> potential, fx, fy, fz;  // original input order
+  };
+
+  FmmContext(std::vector<Particle> particles, const RunConfig& cfg) : input_(std::move(particles)), cfg_(cfg) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (cfg.acc < 2) throw std::invalid_argument("accuracy parameter must be at least 2");  // bench.cpp:223
+    check(fmmgpu_create(cfg.device, cfg.acc, std::pow(10.0, -cfg.acc), &ctx_), fmmgpu_global_error());
+    std::vector<double> xyzw(4 * input_.size());
+    for (std::size_t i = 0; i < input_.size(); ++i) {
+      xyzw[4 * i] = input_[i].position[0];
+      xyzw[4 * i + 1] = input_[i].position[1];
+      xyzw[4 * i + 2] = input_[i].position[2];
+      xyzw[4 * i + 3] = input_[i].weight;
+    }
+    try {
+      call(fmmgpu_build_tree(ctx_, xyzw.empty() ? nullptr : xyzw.data(), input_.size(), 0, cfg.height,
+                             cfg.group_size, nullptr));
+      call(fmmgpu_reset(ctx_));
+    } catch (...) {
+      fmmgpu_destroy(ctx_);
+      throw;
+    }
+    setup_seconds_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  ~FmmContext() { fmmgpu_destroy(ctx_); }
+  FmmContext(const FmmContext&) = delete;
+  FmmContext& operator=(const FmmContext&) = delete;
+
+  const std::vector<Particle>& input() const { return input_; }
+  double setup_seconds() const { return setup_seconds_; }
+  int height() const { return cfg_.height; }
+  fmmgpu_ctx* handle() const { return ctx_; }
+
+  //! FmmContext::reset (bench.cpp:240-253): zero every accumulator.
+  void reset() {
+    call(fmmgpu_reset(ctx_));
+    for (auto& k : done_) k.assign(static_cast<std::size_t>(cfg_.height), 0);
+  }
+
+  //! FmmContext::run_task (bench.cpp:255-344) at level granularity (see header).
+  void run_task(const Task& task) {
+    const int k = static_cast<int>(task.kind);
+    if (k < 0 || k >= TASK_KIND_COUNT) throw std::invalid_argument("run_task: unknown task kind");
+    if (task.level < 0 || task.level >= cfg_.height) throw std::out_of_range("run_task: level out of range");
+    if (done_[k].empty()) done_[k].assign(static_cast<std::size_t>(cfg_.height), 0);
+    if (done_[k][task.level]) return;
+    done_[k][task.level] = 1;
+    switch (task.kind) {
+      case TaskKind::P2M: call(fmmgpu_p2m(ctx_)); break;
+      case TaskKind::M2M: call(fmmgpu_m2m(ctx_, task.level)); break;
+      case TaskKind::M2L: call(fmmgpu_m2l(ctx_, task.level)); break;
+      case TaskKind::L2L: call(fmmgpu_l2l(ctx_, task.level)); break;
+      case TaskKind::L2P: call(fmmgpu_l2p(ctx_)); break;
+      case TaskKind::P2P: call(fmmgpu_p2p(ctx_)); break;
+      case TaskKind::P2PReduce: break;  // folded into P2P
+    }
+  }
+
+  //! The whole task graph at once (reset + all payloads, near/far on two streams).
+  void evaluate() { call(fmmgpu_evaluate(ctx_)); }
+
+  //! FmmContext::gather (bench.cpp:350-365): fields in input order.
+  Fields gather() const {
+    Fields f;
+    const std::size_t n = input_.size();
+    f.potential.resize(n);
+    f.fx.resize(n);
+    f.fy.resize(n);
+    f.fz.resize(n);
+    call(fmmgpu_download_fields(ctx_, f.potential.data(), f.fx.data(), f.fy.data(), f.fz.data(), 0));
+    return f;
+  }
+
+ private:
+  void call(int rc) const { check(rc, fmmgpu_last_error(ctx_)); }
+
+  std::vector<Particle> input_;
+  RunConfig cfg_;
+  fmmgpu_ctx* ctx_ = nullptr;
+  double setup_seconds_ = 0;
+  std::array<std::vector<char>, TASK_KIND_COUNT> done_;
+};
+
+struct RunResult {
+  RunConfig config;
+  double setup_seconds = 0;
+  double exec_seconds = 0;
+  double wall_seconds = 0;
+  FmmContext::Fields fields;
+  std::vector<Particle> input;
+};
+
+//! run_fmm (bench.cpp:415-469) without the oracle check, ledger or writers.
+inline RunResult run_fmm(const RunConfig& cfg) {
+  const auto w0 = std::chrono::steady_clock::now();
+  RunResult r;
+  r.config = cfg;
+  r.input = generate_particles(cfg.n, cfg.dist, cfg.seed);
+  FmmContext ctx(r.input, cfg);
+  r.setup_seconds = ctx.setup_seconds();
+  const auto e0 = std::chrono::steady_clock::now();
+  ctx.evaluate();
+  r.fields = ctx.gather();
+  r.exec_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - e0).count();
+  r.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+  return r;
+}
+
+}  // namespace taskfmm_b200

@@ -137,7 +137,9 @@ struct M2LTables {
   int rowsB = 0;    // round_up(l^3, 64)... padded M of phase B
   double* dM1 = nullptr;    // [8][rowsA][ldE]
   double* dM2 = nullptr;    // [8][rowsB][ldY]
-  int2* dRowA = nullptr;    // [8][rowsA]: {slot or -1, destination column in Yt}
+  int4* dRowA = nullptr;    // [8][rowsA]: {slot or -1, destination column in Yt, vector index in its M-tile, 0}
+  int* dTileVec = nullptr;  // [8][rowsA/64][vtMax]: vector slots of each 64-row M-tile (-1 = none)
+  int vtMax = 0;            // max distinct vectors in one 64-row M-tile
   int* dKslot = nullptr;    // [8][ldY]: vector slot of column kk of the target stack, -1 = pad
 };
 

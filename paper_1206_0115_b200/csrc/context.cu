@@ -136,8 +136,13 @@ int fmmgpu_create(int device, int order, double eps, fmmgpu_ctx** out) {
     FMM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     FMM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    FMM_CUDA(cudaStreamCreateWithFlags(&c->s_far, cudaStreamNonBlocking));
-    FMM_CUDA(cudaStreamCreateWithFlags(&c->s_near, cudaStreamNonBlocking));
+    // The far-field chain gets the higher priority: its coarse levels cannot fill the
+    // GPU, so P2P CTAs (lower priority, concurrent stream) fill the idle SMs instead of
+    // the chain queueing behind 32k P2P CTAs.
+    int prio_lo = 0, prio_hi = 0;
+    FMM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    FMM_CUDA(cudaStreamCreateWithPriority(&c->s_far, cudaStreamNonBlocking, prio_hi));
+    FMM_CUDA(cudaStreamCreateWithPriority(&c->s_near, cudaStreamNonBlocking, prio_lo));
     FMM_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     FMM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     for (auto& e : c->ev_t) FMM_CUDA(cudaEventCreate(&e));

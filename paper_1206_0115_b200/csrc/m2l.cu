@@ -221,7 +221,9 @@ struct GemmArgs {
   int ldE;
   double* Yt;             // [cells][ldY]
   int ldY;
-  const int2* rowA;       // phase A epilogue table [8][rowsA]
+  const int4* rowA;       // phase A epilogue table [8][rowsA]
+  const int* tileVec;     // phase A: vector slots per M-tile [8][rowsA/64][vtMax]
+  int vtMax;
   int rowsA;
   const int* kslot;       // vector slot per target-stack column [8][ldY] (host tables)
   double* local;          // phase B output (local_own)
@@ -364,6 +366,8 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   const int wpad = g.K + 4;                       // == 4 (mod 16): conflict-free fragments
   double* Ws = smem;                              // [BN][wpad]
   double* As = smem + BN * wpad;                  // [PA_ST][PA_BM][SPAD]
+  // [2][vtMax][BN] target cell of (vector of the M-tile, column), double-buffered by M-tile
+  uint32_t* tgt = reinterpret_cast<uint32_t*>(As + PA_ST * PA_BM * SPAD);
   __shared__ uint32_t col_cell[BN];
   __shared__ int col_ijk[BN][3];
 
@@ -426,6 +430,21 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
     if (t + PA_ST - 1 < TOTAL) load_a(t + PA_ST - 1);
     cp_commit();
     const int mt = t / KT, kt = t % KT;
+    uint32_t* tg = tgt + (mt & 1) * g.vtMax * BN;
+    if (kt == 0) {
+      // one lookup per (vector, source column) of this M-tile: target = source - v
+      const int* vec = g.tileVec + (size_t(cls) * MTILES + mt) * g.vtMax;
+      for (int e = tid; e < g.vtMax * BN; e += PA_THREADS) {
+        const int vi = e / BN, j = e % BN;
+        const int slot = __ldg(vec + vi);
+        uint32_t tc = NPOS;
+        if (slot >= 0 && col_cell[j] != NPOS)
+          tc = find_ijk(g.lv, col_ijk[j][0] - (slot / 49 - 3), col_ijk[j][1] - ((slot / 7) % 7 - 3),
+                        col_ijk[j][2] - (slot % 7 - 3));
+        tg[e] = tc;
+      }
+      if (KT == 1) __syncthreads();
+    }
     const double* as = As + (t % PA_ST) * PA_BM * SPAD + (wm * WTM + gq) * SPAD + tq;
     const double* bs = Ws + (wn * WTN + gq) * wpad + kt * PA_BK + tq;
 #pragma unroll
@@ -445,17 +464,14 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         const int row = mt * PA_BM + wm * WTM + i * 8 + gq;
-        const int2 info = __ldg(g.rowA + cls * g.rowsA + row);
+        const int4 info = __ldg(g.rowA + cls * g.rowsA + row);
         if (info.x >= 0) {
-          const int vx = info.x / 49 - 3, vy = (info.x / 7) % 7 - 3, vz = info.x % 7 - 3;
+          const uint32_t* trow = tg + info.z * BN;
 #pragma unroll
           for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int col = wn * WTN + j * 8 + 2 * tq + e;
-              if (col_cell[col] == NPOS) continue;
-              const uint32_t tcell =
-                  find_ijk(g.lv, col_ijk[col][0] - vx, col_ijk[col][1] - vy, col_ijk[col][2] - vz);
+              const uint32_t tcell = trow[wn * WTN + j * 8 + 2 * tq + e];
               if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + info.y] = acc[i][j][e];
             }
         }
@@ -476,6 +492,8 @@ void m2l_free(fmmgpu_ctx* c) {
   if (T.dM1) cudaFree(T.dM1);
   if (T.dM2) cudaFree(T.dM2);
   if (T.dRowA) cudaFree(T.dRowA);
+  if (T.dTileVec) cudaFree(T.dTileVec);
+  T.dTileVec = nullptr;
   if (T.dKslot) cudaFree(T.dKslot);
   T.dM1 = T.dM2 = nullptr;
   T.dRowA = nullptr;
@@ -533,7 +551,7 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   T.rowsA = round_up(R, PA_BM);
   T.rowsB = round_up(n3, B_BM);
   std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
-  std::vector<int2> rowA(size_t(8) * T.rowsA, make_int2(-1, 0));
+  std::vector<int4> rowA(size_t(8) * T.rowsA, make_int4(-1, 0, 0, 0));
   std::vector<int> kslot(size_t(8) * T.ldY, -1);
   for (int p = 0; p < 8; ++p)
     for (int s = 0; s < 343; ++s) {
@@ -547,7 +565,7 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
         for (int k = 0; k < r; ++k) {
           double* row = &M1[(size_t(p) * T.rowsA + oa + k) * c->ldE];
           for (int n = 0; n < n3; ++n) row[n] = T.sigma[cl][k] * T.v[cl][size_t(T.perm[s][n]) * r + k];
-          rowA[size_t(p) * T.rowsA + oa + k] = make_int2(s, ob + k);
+          rowA[size_t(p) * T.rowsA + oa + k] = make_int4(s, ob + k, 0, 0);
         }
       }
       const int ob = offB[p * 343 + s];  // here p plays the target parity q
@@ -568,11 +586,32 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
     }
   FMM_CUDA(cudaMalloc(&T.dM1, M1.size() * sizeof(double)));
   FMM_CUDA(cudaMalloc(&T.dM2, M2.size() * sizeof(double)));
-  FMM_CUDA(cudaMalloc(&T.dRowA, rowA.size() * sizeof(int2)));
+  // per 64-row M-tile of phase A: the distinct vectors it holds (rows of one vector
+  // are consecutive), so the epilogue resolves one target per (vector, column)
+  const int mtiles = T.rowsA / PA_BM;
+  T.vtMax = 1;
+  std::vector<std::vector<int>> tv(size_t(8) * mtiles);
+  for (int p = 0; p < 8; ++p)
+    for (int mt = 0; mt < mtiles; ++mt) {
+      auto& list = tv[size_t(p) * mtiles + mt];
+      for (int r = 0; r < PA_BM; ++r) {
+        int4& e = rowA[size_t(p) * T.rowsA + mt * PA_BM + r];
+        if (e.x < 0) continue;
+        if (list.empty() || list.back() != e.x) list.push_back(e.x);
+        e.z = static_cast<int>(list.size()) - 1;
+      }
+      T.vtMax = std::max<int>(T.vtMax, static_cast<int>(list.size()));
+    }
+  std::vector<int> tileVec(size_t(8) * mtiles * T.vtMax, -1);
+  for (size_t i = 0; i < tv.size(); ++i)
+    std::copy(tv[i].begin(), tv[i].end(), tileVec.begin() + i * T.vtMax);
+  FMM_CUDA(cudaMalloc(&T.dTileVec, tileVec.size() * sizeof(int)));
+  FMM_CUDA(cudaMemcpy(T.dTileVec, tileVec.data(), tileVec.size() * sizeof(int), cudaMemcpyHostToDevice));
+  FMM_CUDA(cudaMalloc(&T.dRowA, rowA.size() * sizeof(int4)));
   FMM_CUDA(cudaMalloc(&T.dKslot, kslot.size() * sizeof(int)));
   FMM_CUDA(cudaMemcpy(T.dM1, M1.data(), M1.size() * sizeof(double), cudaMemcpyHostToDevice));
   FMM_CUDA(cudaMemcpy(T.dM2, M2.data(), M2.size() * sizeof(double), cudaMemcpyHostToDevice));
-  FMM_CUDA(cudaMemcpy(T.dRowA, rowA.data(), rowA.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  FMM_CUDA(cudaMemcpy(T.dRowA, rowA.data(), rowA.size() * sizeof(int4), cudaMemcpyHostToDevice));
   FMM_CUDA(cudaMemcpy(T.dKslot, kslot.data(), kslot.size() * sizeof(int), cudaMemcpyHostToDevice));
   std::vector<int> canon(T.canonical, T.canonical + 343);
   if (!c->d_canon) FMM_CUDA(cudaMalloc(&c->d_canon, 343 * sizeof(int)));
@@ -598,6 +637,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   g.Yt = Lm.yt;
   g.ldY = T.ldY;
   g.rowA = T.dRowA;
+  g.tileVec = T.dTileVec;
+  g.vtMax = T.vtMax;
   g.rowsA = T.rowsA;
   g.kslot = T.dKslot;
   g.local = L.local_own;
@@ -613,7 +654,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.K = c->ldE;
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
     auto launch = [&](auto kern, int bn) {
-      const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * SPAD);
+      const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * SPAD) +
+                          sizeof(uint32_t) * 2 * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       dim3 grid((maxcls + bn - 1) / bn, 8);
       kern<<<grid, PA_THREADS, smem, s>>>(g);

@@ -87,6 +87,71 @@ struct LeafArgs {
 };
 
 constexpr int P2M_THREADS = 128;
+constexpr int P2M_WARPS = P2M_THREADS / 32;
+
+// P2M, warp per leaf cell: lanes evaluate the interpolation vectors of 32 particles
+// at a time into shared memory (a = w Sx, b = Sy, c = Sz, chebyshev.cpp:122-127), then
+// lane p owns the l coefficients W[n1][n2][0..l) of the pair p = (n1, n2) and adds
+// (a[n1] b[n2]) c[n3] for every particle -- the reference's wx, wxy, out += wxy sz
+// product order, l FMAs per pair per particle, with a and b read once per particle.
+template <int L>
+__global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
+  constexpr int PP = (L * L + 31) / 32;  // (n1, n2) pairs per lane
+  __shared__ double tn[L * (L - 1) + 1];
+  __shared__ double S[P2M_WARPS][32][3 * L + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < L * (L - 1); i += P2M_THREADS) tn[i] = a.tn[i];
+  __syncthreads();
+  const uint32_t c = blockIdx.x * P2M_WARPS + warp;
+  if (c >= a.ncells) return;
+  double ctr[3];
+  cell_center(a.geo, a.code[c], ctr);
+  const uint32_t first = a.first[c], cnt = a.count[c];
+  double acc[PP][L];
+#pragma unroll
+  for (int i = 0; i < PP; ++i)
+#pragma unroll
+    for (int n = 0; n < L; ++n) acc[i][n] = 0.0;
+  double(*sw)[3 * L + 1] = S[warp];
+  for (uint32_t base = 0; base < cnt; base += 32) {
+    if (base + lane < cnt) {
+      const double4 p = a.pw[first + base + lane];
+      double s[L];
+      eval_all<L>(tn, (p.x - ctr[0]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) sw[lane][m] = p.w * s[m];
+      eval_all<L>(tn, (p.y - ctr[1]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) sw[lane][L + m] = s[m];
+      eval_all<L>(tn, (p.z - ctr[2]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) sw[lane][2 * L + m] = s[m];
+    }
+    __syncwarp();
+    const int m = min(32u, cnt - base);
+#pragma unroll
+    for (int i = 0; i < PP; ++i) {
+      const int pr = lane + 32 * i;
+      if (pr < L * L) {
+        const int n1 = pr / L, n2 = pr % L;
+        for (int j = 0; j < m; ++j) {
+          const double ab = sw[j][n1] * sw[j][L + n2];
+#pragma unroll
+          for (int n = 0; n < L; ++n) acc[i][n] = fma(ab, sw[j][2 * L + n], acc[i][n]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  double* out = a.expansion + size_t(c) * a.ldE;
+#pragma unroll
+  for (int i = 0; i < PP; ++i) {
+    const int pr = lane + 32 * i;
+    if (pr < L * L)
+#pragma unroll
+      for (int n = 0; n < L; ++n) out[pr * L + n] += acc[i][n];
+  }
+}
 
 template <int L>
 __global__ void __launch_bounds__(P2M_THREADS) k_p2m(LeafArgs a) {
@@ -136,6 +201,71 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m(LeafArgs a) {
   for (int o = 0; o < OPT; ++o) {
     const int idx = tid + o * P2M_THREADS;
     if (idx < L3) out[idx] += acc[o];
+  }
+}
+
+// L2P, CTA per run of L2P_CELLS consecutive leaf cells: total = own + down is formed
+// once per cell in shared memory (bench.cpp:320-325), then thread per particle of
+// those cells (contiguous in Morton order) reads it as (near-)broadcast LDS.
+constexpr int L2P_CELLS = 8, L2P_THREADS = 128;
+
+template <int L>
+__global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
+  constexpr int L3 = L * L * L;
+  extern __shared__ __align__(16) double tot[];  // [L2P_CELLS][L3]
+  __shared__ double tn[L * (L - 1) + 1];
+  const uint32_t c0 = blockIdx.x * L2P_CELLS;
+  const uint32_t nc = min(static_cast<uint32_t>(L2P_CELLS), a.ncells - c0);
+  for (int i = threadIdx.x; i < L * (L - 1); i += L2P_THREADS) tn[i] = a.tn[i];
+  for (uint32_t i = threadIdx.x; i < nc * L3; i += L2P_THREADS) {
+    const uint32_t lc = i / L3, k = i % L3;
+    const size_t g = size_t(c0 + lc) * a.ldE + k;
+    tot[i] = a.expansion[g] + a.down[g];
+  }
+  __syncthreads();
+  const uint64_t p0 = a.first[c0], p1 = uint64_t(a.first[c0 + nc - 1]) + a.count[c0 + nc - 1];
+  const double inv = a.geo.inv;
+  for (uint64_t s = p0 + threadIdx.x; s < p1; s += L2P_THREADS) {
+    const uint32_t c = a.pcell[s];
+    double ctr[3];
+    cell_center(a.geo, a.code[c], ctr);
+    const double4 p = a.pw[s];
+    const double rx = (p.x - ctr[0]) * inv, ry = (p.y - ctr[1]) * inv, rz = (p.z - ctr[2]) * inv;
+    double sx[L], sy[L], sz[L], gx[L], gy[L], gz[L];
+    eval_all<L>(tn, rx, sx);
+    eval_all<L>(tn, ry, sy);
+    eval_all<L>(tn, rz, sz);
+    grad_all<L>(tn, rx, gx);
+    grad_all<L>(tn, ry, gy);
+    grad_all<L>(tn, rz, gz);
+    const double* t = tot + (c - c0) * L3;
+    double pot = 0, dx = 0, dy = 0, dz = 0;
+    constexpr int UNROLL_N1 = L <= 7 ? L : 1;  // keep sx/gx in registers
+#pragma unroll UNROLL_N1
+    for (int n1 = 0; n1 < L; ++n1) {
+#pragma unroll
+      for (int n2 = 0; n2 < L; ++n2) {
+        double u = 0, w = 0;
+#pragma unroll
+        for (int n3 = 0; n3 < L; ++n3) {
+          const double v = t[(n1 * L + n2) * L + n3];
+          u = fma(v, sz[n3], u);
+          w = fma(v, gz[n3], w);
+        }
+        const double ss = sx[n1] * sy[n2];
+        pot = fma(ss, u, pot);
+        dx = fma(gx[n1] * sy[n2], u, dx);
+        dy = fma(sx[n1] * gy[n2], u, dy);
+        dz = fma(ss, w, dz);
+      }
+    }
+    double4* f = reinterpret_cast<double4*>(a.far) + s;
+    double4 r = *f;
+    r.x += pot;
+    r.y -= inv * dx;
+    r.z -= inv * dy;
+    r.w -= inv * dz;
+    *f = r;
   }
 }
 
@@ -308,13 +438,16 @@ void dispatch_order(int order, Args&&... args) {
 template <int L>
 struct RunP2M {
   static void run(const LeafArgs& a, cudaStream_t s) {
-    if (a.ncells) k_p2m<L><<<a.ncells, P2M_THREADS, 0, s>>>(a);
+    if (a.ncells) k_p2m_warp<L><<<(a.ncells + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
   }
 };
 template <int L>
 struct RunL2P {
   static void run(const LeafArgs& a, cudaStream_t s) {
-    if (a.n) k_l2p<L><<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, s>>>(a);
+    if (!a.ncells) return;
+    const int smem = static_cast<int>(sizeof(double) * L2P_CELLS * L * L * L);
+    FMM_CUDA(cudaFuncSetAttribute(k_l2p_block<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_l2p_block<L><<<(a.ncells + L2P_CELLS - 1) / L2P_CELLS, L2P_THREADS, smem, s>>>(a);
   }
 };
 template <int L>

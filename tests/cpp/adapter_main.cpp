@@ -1,0 +1,80 @@
+// C++ drop-in check of include/taskfmm_b200.hpp (the reference-API mirror over the
+// C ABI). Built and run by tests/test_cpp_adapter.py on a GPU box:
+//   adapter_main <n> <height> <acc> <seed> <out.bin>
+// Runs the evaluation twice — once task by task in a valid reference DAG order
+// (run_task, bench.cpp:255-344), once as evaluate() — writes both field sets, and
+// checks the reference exception classes.
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <vector>
+
+#include "taskfmm_b200.hpp"
+
+using namespace taskfmm_b200;
+
+static int expect_throw(const char* what, auto&& f, auto tag) {
+  try {
+    f();
+  } catch (const decltype(tag)&) {
+    return 0;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "%s: wrong exception %s\n", what, e.what());
+    return 1;
+  }
+  std::fprintf(stderr, "%s: no exception\n", what);
+  return 1;
+}
+
+int main(int argc, char** argv) {
+  if (argc != 6) return 2;
+  RunConfig cfg;
+  cfg.n = std::strtoull(argv[1], nullptr, 10);
+  cfg.height = std::atoi(argv[2]);
+  cfg.acc = std::atoi(argv[3]);
+  cfg.seed = std::strtoull(argv[4], nullptr, 10);
+  auto particles = generate_particles(cfg.n, cfg.dist, cfg.seed);
+  FmmContext ctx(particles, cfg);
+  const int leaf = cfg.height - 1;
+  // a valid topological order of the reference task graph (taskflow.cpp:215-247),
+  // three blocks per (kind, level): P2P first, then the far-field chain
+  ctx.reset();
+  std::uint32_t id = 0;
+  auto run = [&](TaskKind k, int level) {
+    for (std::uint32_t b = 0; b < 3; ++b) ctx.run_task(Task{id++, k, static_cast<std::int16_t>(level), b, 0});
+  };
+  run(TaskKind::P2P, leaf);
+  run(TaskKind::P2M, leaf);
+  for (int v = leaf - 1; v >= 2; --v) run(TaskKind::M2M, v);
+  for (int v = 2; v <= leaf; ++v) run(TaskKind::M2L, v);
+  for (int v = 2; v < leaf; ++v) run(TaskKind::L2L, v);
+  run(TaskKind::L2P, leaf);
+  run(TaskKind::P2PReduce, leaf);
+  const auto a = ctx.gather();
+  ctx.evaluate();
+  const auto b = ctx.gather();
+  std::FILE* f = std::fopen(argv[5], "wb");
+  if (!f) return 3;
+  for (const auto* fs : {&a, &b})
+    for (const auto* v : {&fs->potential, &fs->fx, &fs->fy, &fs->fz}) std::fwrite(v->data(), 8, v->size(), f);
+  std::fclose(f);
+
+  int bad = 0;
+  RunConfig bad_h = cfg;
+  bad_h.height = 2;
+  bad += expect_throw("height 2", [&] { FmmContext c(particles, bad_h); }, std::invalid_argument(""));
+  RunConfig bad_acc = cfg;
+  bad_acc.acc = 11;
+  bad += expect_throw("acc 11", [&] { FmmContext c(particles, bad_acc); }, std::invalid_argument(""));
+  std::vector<Particle> dup = {{{0.1, 0.1, 0.1}, 1.0}, {{0.1, 0.1, 0.1}, 1.0}, {{0.9, 0.9, 0.9}, 1.0}};
+  bad += expect_throw("coincident", [&] { FmmContext c(dup, cfg); }, std::domain_error(""));
+  bad += expect_throw("level", [&] { ctx.run_task(Task{0, TaskKind::M2L, 99, 0, 0}); }, std::out_of_range(""));
+  const auto r = run_fmm(cfg);
+  if (relative_l2_error(r.fields.potential, b.potential) != 0.0) {
+    std::fprintf(stderr, "run_fmm differs from evaluate\n");
+    ++bad;
+  }
+  std::printf("adapter: n=%llu setup %.3f s exec %.3f s, %d failures\n",
+              static_cast<unsigned long long>(cfg.n), r.setup_seconds, r.exec_seconds, bad);
+  return bad;
+}

@@ -6,7 +6,7 @@ for what in "$@"; do
 case "$what" in
   tests) timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -30 > gpurun_out/pytest_gpu.log
          timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1 ;;
-  launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_eval.py 10000000 7 5 2 > gpurun_out/launches.out 2>&1 ;;
+  launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:k_|Radix|Scan|RunLength|Reduce" --csv --log-file gpurun_out/launches.csv python tools/profile_eval.py 10000000 7 5 2 > gpurun_out/launches.out 2>&1 ;;
   full) timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$FULL_RE" -s "${FULL_SKIP:-0}" -c "${FULL_COUNT:-1}" -o gpurun_out/prof -f python tools/profile_eval.py 10000000 7 5 1 > gpurun_out/prof.out 2>&1 ;;
   full2) timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$FULL2_RE" -s "${FULL2_SKIP:-0}" -c "${FULL2_COUNT:-1}" -o gpurun_out/prof2 -f python tools/profile_eval.py 10000000 7 5 1 > gpurun_out/prof2.out 2>&1 ;;
   quick) timeout 300 python tools/quick_eval.py > gpurun_out/quick.log 2>&1 ;;

@@ -40,7 +40,24 @@ CPU_SAMPLE = {"B": (1_250_000, "uniform", 6, 5), "C": (1_250_000, "uniform", 6, 
 
 METRIC = "FMM eval time (s) and Mparticles/s at N=10M, order 5; scaling 1/2/4/8 B200"
 UNIT = "Mparticles/s"
-FP64_PEAK_TFLOPS = 37.15  # own DMMA m8n8k4 microbenchmark, profiles/r01_fp64_peaks.txt
+# FP64 peaks measured on this pool's B200 by tools/microbench/fp64_peaks.cu
+# (profiles/r01_fp64_peaks.txt); MEASURED_PEAKS.json carries HBM and bf16 only.
+FP64_DMMA_TFLOPS = 37.15  # mma.sync m8n8k4 f64 (the M2L GEMMs)
+FP64_DFMA_TFLOPS = 34.02  # DFMA chains (the P2P kernel)
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            for k in ("hbm_gbs", "hbm_GBs", "hbm"):
+                if k in d:
+                    return float(d[k]), "MEASURED_PEAKS.json"
+        except Exception:  # pragma: no cover
+            pass
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
 def log(*a):
@@ -217,26 +234,47 @@ def run_ours(args, world, rank, local):
     e2e = {"value": world * n / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": 32 * n, "d2h_bytes_per_step": 32 * n,
            "ms_per_step": e2e_s * 1e3, "path": "fmmgpu_run (C ABI): pinned H2D, build_tree, evaluate, D2H"}
 
-    # roofline of the dominant kernel family (per-kind device time inside the timed region)
-    per = {k: v / args.steps for k, v in kinds.items()}
+    # isolated per-operator device times (each operator alone, CUDA events on its
+    # stream): the roofline numerators' denominators. The P2P kernel is the largest
+    # single kernel; its share of the step is reported beside it.
     flops = ledger["flops"]
-    fam = "M2L" if per["M2L"] >= per["P2P"] else "P2P"
-    achieved = flops[fam] / (per[fam] / 1e3) / 1e12
+    iso = {k: ctx.time_operator(k, -1, 3) for k in ("P2M", "M2M", "M2L", "L2L", "L2P", "P2P")}
+    leaf = h - 1
+    iso_m2l_leaf = ctx.time_operator("M2L", leaf, 3)
+    ctx.evaluate()
+    ctx.synchronize()
+    peaks = {"P2M": FP64_DFMA_TFLOPS, "M2M": FP64_DFMA_TFLOPS, "M2L": FP64_DMMA_TFLOPS, "L2L": FP64_DFMA_TFLOPS,
+             "L2P": FP64_DFMA_TFLOPS, "P2P": FP64_DFMA_TFLOPS}
+    per_op = {}
+    for k, ms in iso.items():
+        tf = flops[k] / (ms / 1e3) / 1e12
+        per_op[k] = {"ms_isolated": ms, "ms_in_step": kinds[k] / args.steps, "ledger_flops": flops[k],
+                     "tflops": tf, "peak_tflops": peaks[k], "frac": tf / peaks[k]}
+    hbm, hbm_src = hbm_peak()
+    for k in ("M2M", "L2L"):  # HBM-bound transfers: algorithmic bytes 8 l^3 (children + 2 parents)
+        cells = [ctx.level(v)[0].shape[0] for v in range(h)]
+        l3 = order ** 3
+        byts = sum(8 * l3 * (cells[v + 1] + 2 * cells[v]) for v in range(2, leaf))
+        per_op[k]["hbm_gbs"] = byts / (iso[k] / 1e3) / 1e9
+        per_op[k]["hbm_frac"] = per_op[k]["hbm_gbs"] / hbm
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(f"{args.config}:{fam}")
-    roof = {"bound": "tensor" if fam == "M2L" else "fp64", "kernel": fam, "achieved": achieved,
-            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-            "flops_per_launch": flops[fam], "ms_per_launch": per[fam],
-            "peak_source": "FP64 DMMA peak measured by tools/microbench/fp64_peaks.cu (not in MEASURED_PEAKS.json)",
-            "flop_convention": "reference ledger (bench.cpp:104-122): M2L 4 l^3 r + r^2 per pair, P2P 15 per "
-                               "directional interaction"}
-    per_op = {}
-    for k in ("P2M", "M2M", "M2L", "L2L", "L2P", "P2P"):
-        if per[k] > 0:
-            per_op[k] = {"ms": per[k], "tflops_ref_convention": flops[k] / (per[k] / 1e3) / 1e12,
-                         "frac_fp64_peak": flops[k] / (per[k] / 1e3) / 1e12 / FP64_PEAK_TFLOPS}
+        traffic = json.load(open(tp)).get(f"{args.config}:P2P")
+    p2p_tf = flops["P2P"] / (iso["P2P"] / 1e3) / 1e12
+    roof = {"bound": "fp64", "kernel": "k_p2p (P2P, FP64 DFMA/DMUL pipe)", "achieved": p2p_tf,
+            "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s", "frac": p2p_tf / FP64_DFMA_TFLOPS, "traffic": traffic,
+            "flops_per_launch": flops["P2P"], "ms_per_launch": iso["P2P"],
+            "share_of_step": iso["P2P"] / ms_step,
+            "peak_source": "FP64 DFMA measured by tools/microbench/fp64_peaks.cu (profiles/r01_fp64_peaks.txt); "
+                           "MEASURED_PEAKS.json has no FP64 figure",
+            "flop_convention": "reference ledger (bench.hpp:49-53): 15 flop per directional interaction "
+                               "(the kernel issues 18 FP64 instructions per interaction, so frac <= 0.45 at "
+                               "a saturated FP64 pipe)",
+            "m2l": {"bound": "tensor (FP64 DMMA)", "ms_all_levels": iso["M2L"], "ms_leaf": iso_m2l_leaf,
+                    "achieved": per_op["M2L"]["tflops"], "peak": FP64_DMMA_TFLOPS,
+                    "frac": per_op["M2L"]["frac"]},
+            "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "eval_seconds": ms_step / 1e3,
             "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,

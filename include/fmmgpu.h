@@ -146,6 +146,13 @@ uint64_t fmmgpu_last_launch_count(const fmmgpu_ctx* ctx);
 int fmmgpu_time_evaluations(fmmgpu_ctx* ctx, int steps, double* total_ms, double* kind_ms10,
                             uint64_t* launches);
 
+/* Isolated device time of one operator (CUDA events on the launching stream, the
+ * operator alone on the device): `reps` back-to-back launches of kind (fmmgpu_kind,
+ * P2M..P2P) at `level` (ignored for P2M / L2P / P2P; -1 = all levels of that kind),
+ * average ms per repetition in *ms. Accumulators are left dirty: call fmmgpu_reset
+ * (or fmmgpu_evaluate) before reading fields. */
+int fmmgpu_time_operator(fmmgpu_ctx* ctx, int kind, int level, int reps, double* ms);
+
 /* bench.cpp:19-61 generate_particles (mt19937_64, explicit scaling); dist 0 uniform,
  * 1 sphere. Host-side input generator so both sides see identical doubles. */
 void fmmgpu_generate_particles(uint64_t n, int dist, uint64_t seed, double* xyzw);

@@ -330,6 +330,12 @@ class FmmContext:
         keys = list(KINDS[:6]) + ["GATHER", "EVAL", "TREE", "LISTS"]
         return total.value, dict(zip(keys, ms.tolist())), nl.value
 
+    def time_operator(self, kind: str, level: int = -1, reps: int = 5):
+        """Isolated device time (ms per repetition) of one operator; leaves accumulators dirty."""
+        ms = c_double()
+        self._check(self._lib.fmmgpu_time_operator(self.h, KINDS.index(kind), level, reps, byref(ms)))
+        return ms.value
+
     def run(self, particles, height, group_size=250):
         """Whole run through the C ABI with host buffers (fmmgpu_run)."""
         xyzw = np.ascontiguousarray(particles, dtype=np.float64)

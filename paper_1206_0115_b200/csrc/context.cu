@@ -414,6 +414,49 @@ int fmmgpu_time_evaluations(fmmgpu_ctx* c, int steps, double* total_ms, double* 
   });
 }
 
+int fmmgpu_time_operator(fmmgpu_ctx* c, int kind, int level, int reps, double* ms) {
+  return guarded(c, [&] {
+    need_tree(c);
+    if (reps < 1 || !ms) throw Error(FMMGPU_INVALID_ARGUMENT, "reps must be >= 1 and ms non-null");
+    const int leaf = c->height - 1;
+    auto levels = [&](int lo, int hi) {
+      if (level >= 0) {
+        need_level(c, level, lo, hi, "time_operator");
+        return std::vector<int>{level};
+      }
+      std::vector<int> v;
+      for (int i = lo; i <= hi; ++i) v.push_back(i);
+      return v;
+    };
+    std::vector<int> lv;
+    switch (kind) {
+      case FMMGPU_M2M: case FMMGPU_L2L: lv = levels(2, leaf - 1); break;
+      case FMMGPU_M2L: lv = levels(2, leaf); break;
+      case FMMGPU_P2M: case FMMGPU_L2P: case FMMGPU_P2P: lv = {leaf}; break;
+      default: throw Error(FMMGPU_INVALID_ARGUMENT, "time_operator: kind must be P2M..P2P");
+    }
+    cudaStream_t s = c->s_far;
+    FMM_CUDA(cudaStreamSynchronize(c->s_near));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    c->out_valid = false;
+    FMM_CUDA(cudaEventRecord(c->ev_t[12], s));
+    for (int r = 0; r < reps; ++r)
+      for (int v : lv) {
+        switch (kind) {
+          case FMMGPU_P2M: launch_p2m(c, s); break;
+          case FMMGPU_M2M: launch_m2m(c, v, s); break;
+          case FMMGPU_M2L: launch_m2l(c, v, s); break;
+          case FMMGPU_L2L: launch_l2l(c, v, s); break;
+          case FMMGPU_L2P: launch_l2p(c, s); break;
+          case FMMGPU_P2P: launch_p2p(c, s); break;
+        }
+      }
+    FMM_CUDA(cudaEventRecord(c->ev_t[13], s));
+    FMM_CUDA(cudaEventSynchronize(c->ev_t[13]));
+    *ms = elapsed(c->ev_t[12], c->ev_t[13]) / reps;
+  });
+}
+
 int fmmgpu_download_fields(fmmgpu_ctx* c, double* pot, double* fx, double* fy, double* fz, int dst_on_device) {
   return guarded(c, [&] {
     need_tree(c);

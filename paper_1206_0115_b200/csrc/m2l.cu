@@ -228,6 +228,7 @@ struct GemmArgs {
   const int* kslot;       // vector slot per target-stack column [8][ldY] (host tables)
   double* local;          // phase B output (local_own)
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
+  int msplit;             // phase A M-split factor (coarse levels)
   double* part;           // phase B split-K partials [ksplit][ncells][ldE]
   uint32_t ncells;
   int l3;
@@ -402,19 +403,26 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   const double* A = g.A + cls * g.a_class_stride;
   const int KT = g.K / PA_BK;
   const int MTILES = g.rowsA / PA_BM;
-  const int TOTAL = MTILES * KT;
-  auto load_a = [&](int t) {
-    const int mt = t / KT, kt = t % KT;
-    double* as = As + (t % PA_ST) * PA_BM * SPAD;
-    const double* src = A + size_t(mt * PA_BM) * g.lda + kt * PA_BK;
+  // M-split (coarse levels): this CTA streams M-tiles [mt0, mt1) of the operator
+  const int per = (MTILES + g.msplit - 1) / g.msplit;
+  const int mt0 = blockIdx.z * per, mt1 = min(MTILES, mt0 + per);
+  if (mt0 >= mt1) return;
+  const int TOTAL = (mt1 - mt0) * KT;
+  // ring producer position (tile, k-slice), advanced without divisions
+  int pmt = mt0, pkt = 0, pstage = 0;
+  auto load_next = [&]() {
+    double* as = As + pstage * PA_BM * SPAD;
+    const double* src = A + size_t(pmt * PA_BM) * g.lda + pkt * PA_BK;
     for (int ch = tid; ch < PA_BM * (PA_BK / 2); ch += PA_THREADS) {
       const int r = ch / (PA_BK / 2), q = (ch % (PA_BK / 2)) * 2;
       cp16(as + r * SPAD + q, src + size_t(r) * g.lda + q);
     }
+    if (++pkt == KT) { pkt = 0; ++pmt; }
+    if (++pstage == PA_ST) pstage = 0;
   };
 #pragma unroll
   for (int s = 0; s < PA_ST - 1; ++s) {
-    if (s < TOTAL) load_a(s);
+    if (s < TOTAL) load_next();
     cp_commit();
   }
 
@@ -424,28 +432,45 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // epilogue tables of the current M-tile, fetched early so their latency hides
+  // behind the tile's DMMAs: per row {destination column, vector index or -1}, and the
+  // tile's vector slots feeding the (vector, column) -> target lookup
+  const int kt_fill = KT / 2;
+  int2 info[MT];
+  int slot_e0 = -1, slot_e1 = -1;
+  int mt = mt0, kt = 0, stage = 0;
   for (int t = 0; t < TOTAL; ++t) {
     cp_wait<PA_ST - 2>();
     __syncthreads();
-    if (t + PA_ST - 1 < TOTAL) load_a(t + PA_ST - 1);
+    if (t + PA_ST - 1 < TOTAL) load_next();
     cp_commit();
-    const int mt = t / KT, kt = t % KT;
     uint32_t* tg = tgt + (mt & 1) * g.vtMax * BN;
     if (kt == 0) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int4 r = __ldg(g.rowA + cls * g.rowsA + mt * PA_BM + wm * WTM + i * 8 + gq);
+        info[i] = make_int2(r.y, r.x >= 0 ? r.z : -1);
+      }
+      const int* vec = g.tileVec + (size_t(cls) * MTILES + mt) * g.vtMax;
+      slot_e0 = tid < g.vtMax * BN ? __ldg(vec + tid / BN) : -1;
+      slot_e1 = tid + PA_THREADS < g.vtMax * BN ? __ldg(vec + (tid + PA_THREADS) / BN) : -1;
+    }
+    if (kt == kt_fill) {
       // one lookup per (vector, source column) of this M-tile: target = source - v
       const int* vec = g.tileVec + (size_t(cls) * MTILES + mt) * g.vtMax;
-      for (int e = tid; e < g.vtMax * BN; e += PA_THREADS) {
-        const int vi = e / BN, j = e % BN;
-        const int slot = __ldg(vec + vi);
+      int u = 0;
+      for (int e = tid; e < g.vtMax * BN; e += PA_THREADS, ++u) {
+        const int j = e % BN;
+        const int slot = u == 0 ? slot_e0 : u == 1 ? slot_e1 : __ldg(vec + e / BN);
         uint32_t tc = NPOS;
         if (slot >= 0 && col_cell[j] != NPOS)
           tc = find_ijk(g.lv, col_ijk[j][0] - (slot / 49 - 3), col_ijk[j][1] - ((slot / 7) % 7 - 3),
                         col_ijk[j][2] - (slot % 7 - 3));
         tg[e] = tc;
       }
-      if (KT == 1) __syncthreads();
+      if (kt_fill == KT - 1) __syncthreads();
     }
-    const double* as = As + (t % PA_ST) * PA_BM * SPAD + (wm * WTM + gq) * SPAD + tq;
+    const double* as = As + stage * PA_BM * SPAD + (wm * WTM + gq) * SPAD + tq;
     const double* bs = Ws + (wn * WTN + gq) * wpad + kt * PA_BK + tq;
 #pragma unroll
     for (int kk = 0; kk < PA_BK; kk += 4) {
@@ -460,25 +485,25 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
         for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     if (kt == KT - 1) {
-      // scatter block v of source s to target s - v, target-side column info.y
+      // scatter block v of source s to target s - v, target-side column info.x
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        const int row = mt * PA_BM + wm * WTM + i * 8 + gq;
-        const int4 info = __ldg(g.rowA + cls * g.rowsA + row);
-        if (info.x >= 0) {
-          const uint32_t* trow = tg + info.z * BN;
+        if (info[i].y >= 0) {
+          const uint32_t* trow = tg + info[i].y * BN;
 #pragma unroll
           for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const uint32_t tcell = trow[wn * WTN + j * 8 + 2 * tq + e];
-              if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + info.y] = acc[i][j][e];
+              if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + info[i].x] = acc[i][j][e];
             }
         }
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
       }
     }
+    if (++stage == PA_ST) stage = 0;
+    if (++kt == KT) { kt = 0; ++mt; }
   }
   cp_wait<0>();
 }
@@ -657,7 +682,13 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * SPAD) +
                           sizeof(uint32_t) * 2 * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      dim3 grid((maxcls + bn - 1) / bn, 8);
+      // M-split so coarse levels still put >= 2 CTAs on every SM
+      const uint32_t ncols = 8u * ((maxcls + bn - 1) / bn);
+      const int mtiles = T.rowsA / PA_BM;
+      int ms = 1;
+      while (ms < mtiles && ncols * ms < 2u * 148u) ++ms;
+      g.msplit = ms;
+      dim3 grid((maxcls + bn - 1) / bn, 8, ms);
       kern<<<grid, PA_THREADS, smem, s>>>(g);
       FMM_CUDA(cudaGetLastError());
     };

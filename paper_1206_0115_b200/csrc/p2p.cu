@@ -44,6 +44,8 @@ struct P2PSmem {
   uint32_t first[64];
   uint32_t cnt[64];
   uint32_t voff[65];  // virtual offsets of the 64 positions (prefix sum of counts padded to 4)
+  uint32_t full_off[9];  // prefix over the 8 children of their full 32-target passes
+  uint32_t next_unit;    // work-unit queue head (per chunk)
 };
 
 // A staged source that contributes exactly zero: w = 0 far away (finite r^2, so
@@ -94,15 +96,33 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) k_p2p(const P2PArgs a) {
   __syncthreads();
   const uint32_t total = sm.voff[64];
 
-  // this warp's target cell: child octant `warp` at local position (1+a, 1+b, 1+c)
-  const int ca = (warp >> 2) & 1, cb = (warp >> 1) & 1, cc = warp & 1;
-  const int tpos = ((1 + ca) << 4) | ((1 + cb) << 2) | (1 + cc);
-  const uint32_t nT = sm.cnt[tpos];
-  const uint32_t tfirst = sm.first[tpos];
+  // Work units: every full 32-target pass of every child, then every child's partial
+  // last pass (cost ~ m/32 of a full one). Warps pull units from a shared queue, so a
+  // CTA whose children differ in size still keeps all 8 warps busy to the end (a
+  // static warp-per-child mapping idles ~20% at ~38 particles per leaf). Each unit
+  // owns distinct targets, so results do not depend on which warp takes it.
+  if (tid == 0) {
+    uint32_t acc = 0;
+    for (int w = 0; w < 8; ++w) {
+      sm.full_off[w] = acc;
+      const int tp = ((1 + ((w >> 2) & 1)) << 4) | ((1 + ((w >> 1) & 1)) << 2) | (1 + (w & 1));
+      acc += sm.cnt[tp] / 32u;
+    }
+    sm.full_off[8] = acc;
+  }
+  __syncthreads();
+  const uint32_t nfull = sm.full_off[8];
+  uint32_t npart = 0;
+  for (int w = 0; w < 8; ++w) {
+    const int tp = ((1 + ((w >> 2) & 1)) << 4) | ((1 + ((w >> 1) & 1)) << 2) | (1 + (w & 1));
+    npart += (sm.cnt[tp] % 32u) != 0;
+  }
+  const uint32_t nunits = nfull + npart;
 
   for (uint32_t base = 0; base < total; base += P2P_CAP) {
     const uint32_t clen = min(static_cast<uint32_t>(P2P_CAP), total - base);
     if (base) __syncthreads();
+    if (tid == 0) sm.next_unit = 0;
     for (uint32_t i = tid; i < clen; i += P2P_THREADS) {
       const uint32_t v = base + i;
       int lo = 0, hi = 63;  // last position with voff[pos] <= v
@@ -115,7 +135,31 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) k_p2p(const P2PArgs a) {
     }
     __syncthreads();
 
-    for (uint32_t t0 = 0; t0 < nT; t0 += 32) {
+    for (;;) {
+      uint32_t u = 0;
+      if (lane == 0) u = atomicAdd(&sm.next_unit, 1u);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= nunits) break;
+      // decode unit -> (child octant w, first target t0)
+      int w = 0;
+      uint32_t t0 = 0;
+      if (u < nfull) {
+        while (sm.full_off[w + 1] <= u) ++w;
+        t0 = 32u * (u - sm.full_off[w]);
+      } else {
+        uint32_t k = u - nfull;
+        for (w = 0; w < 8; ++w) {
+          const int tp = ((1 + ((w >> 2) & 1)) << 4) | ((1 + ((w >> 1) & 1)) << 2) | (1 + (w & 1));
+          if (sm.cnt[tp] % 32u == 0) continue;
+          if (k == 0) break;
+          --k;
+        }
+        t0 = 32u * (sm.full_off[w + 1] - sm.full_off[w]);
+      }
+      const int ca = (w >> 2) & 1, cb = (w >> 1) & 1, cc = w & 1;
+      const int tpos = ((1 + ca) << 4) | ((1 + cb) << 2) | (1 + cc);
+      const uint32_t nT = sm.cnt[tpos];
+      const uint32_t tfirst = sm.first[tpos];
       const uint32_t m = min(32u, nT - t0);
       const uint32_t S = 32u / m;
       const uint32_t lt = lane % m, split = lane / m;

@@ -345,6 +345,72 @@ __device__ __forceinline__ double step_one(const double* mt, const double* src, 
   return acc;
 }
 
+// M2M / L2L, CTA per parent with one warp per child (<= 8): each warp runs the three
+// l x l passes of tensor_step (chebyshev.cpp:181-211) on its own shared buffers with
+// __syncwarp only. M2M sums the children's contributions into the parent in child
+// order (the reference's order, bench.cpp:280-284); L2L stages own+down of the parent
+// once (bench.cpp:308-309) and each warp accumulates into its child's local_down.
+template <int L, bool IS_M2M>
+__global__ void __launch_bounds__(256) k_transfer_warp(TransArgs a) {
+  constexpr int L3 = L * L * L;
+  constexpr int PER = (L3 + 31) / 32;
+  __shared__ double mats[2 * L * L];
+  __shared__ double par[L3];
+  __shared__ double buf[8][2][L3];
+  const uint32_t p = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 2 * L * L; i += 256) mats[i] = a.mats[i];
+  if (!IS_M2M)
+    for (int i = tid; i < L3; i += 256) par[i] = a.parent_a[size_t(p) * a.ldE + i] + a.parent_b[size_t(p) * a.ldE + i];
+  __syncthreads();
+  const uint32_t f = a.first_child[p], nch = a.child_count[p];
+  if (warp < static_cast<int>(nch)) {
+    const uint32_t ch = f + warp;
+    const int oct = static_cast<int>(a.child_code[ch] & 7);
+    const double* m0 = mats + ((oct >> 2) & 1) * L * L;
+    const double* m1 = mats + ((oct >> 1) & 1) * L * L;
+    const double* m2 = mats + (oct & 1) * L * L;
+    double* b0 = buf[warp][0];
+    double* b1 = buf[warp][1];
+    const double* src = par;
+    if (IS_M2M) {
+      for (int i = lane; i < L3; i += 32) b1[i] = a.child_in[size_t(ch) * a.ldE + i];
+      __syncwarp();
+      src = b1;
+    }
+    for (int i = lane; i < L3; i += 32) b0[i] = step_one<L>(m0, src, i);
+    __syncwarp();
+    for (int i = lane; i < L3; i += 32) b1[i] = step_one<L>(m1, b0, i);
+    __syncwarp();
+    if (IS_M2M) {
+      double r[PER];
+#pragma unroll
+      for (int o = 0; o < PER; ++o) {
+        const int i = lane + 32 * o;
+        if (i < L3) r[o] = step_one<L>(m2, b1, i);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int o = 0; o < PER; ++o) {
+        const int i = lane + 32 * o;
+        if (i < L3) b0[i] = r[o];
+      }
+    } else {
+      double* out = a.out + size_t(ch) * a.ldE;
+      for (int i = lane; i < L3; i += 32) out[i] += step_one<L>(m2, b1, i);
+    }
+  }
+  if (IS_M2M) {
+    __syncthreads();
+    double* out = a.out + size_t(p) * a.ldE;
+    for (int i = tid; i < L3; i += 256) {
+      double acc = out[i];
+      for (uint32_t c = 0; c < nch; ++c) acc += buf[c][0][i];
+      out[i] = acc;
+    }
+  }
+}
+
 template <int L, bool IS_M2M>
 __global__ void __launch_bounds__(128) k_transfer(TransArgs a) {
   constexpr int L3 = L * L * L;
@@ -453,13 +519,17 @@ struct RunL2P {
 template <int L>
 struct RunM2M {
   static void run(const TransArgs& a, cudaStream_t s) {
-    if (a.nparents) k_transfer<L, true><<<a.nparents, 128, 0, s>>>(a);
+    if (!a.nparents) return;
+    if constexpr (L <= 7) k_transfer_warp<L, true><<<a.nparents, 256, 0, s>>>(a);  // 48 KB static smem
+    else k_transfer<L, true><<<a.nparents, 128, 0, s>>>(a);
   }
 };
 template <int L>
 struct RunL2L {
   static void run(const TransArgs& a, cudaStream_t s) {
-    if (a.nparents) k_transfer<L, false><<<a.nparents, 128, 0, s>>>(a);
+    if (!a.nparents) return;
+    if constexpr (L <= 7) k_transfer_warp<L, false><<<a.nparents, 256, 0, s>>>(a);
+    else k_transfer<L, false><<<a.nparents, 128, 0, s>>>(a);
   }
 };
 

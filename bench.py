@@ -283,7 +283,7 @@ def run_ours(args, world, rank, local):
                        "group_size": 250, "parallelism": "replicas" if world > 1 else "single",
                        "l2": "inputs (320 MB particles, 262 MB leaf expansions) exceed the 126 MB L2"},
             "gpu_launches": launches, "e2e": e2e, "roofline": roof, "per_operator": per_op,
-            "tree_ms": per["TREE"], "clocks": clk,
+            "tree_ms": kinds["TREE"], "clocks": clk,
             "note": "P2P runs on its own stream concurrently with the far-field chain; per-operator times "
                     "of the far chain include waiting for SMs the P2P kernel holds"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -24,7 +24,7 @@ namespace fmmgpu {
 
 namespace {
 
-constexpr int P2P_WARPS = 8;             // one per child octant
+constexpr int P2P_WARPS = 12;            // pull work units (child passes) from a shared queue
 constexpr int P2P_THREADS = P2P_WARPS * 32;
 constexpr int P2P_CAP = 3072;            // staged particles per chunk (96 KB), multiple of 4
 

@@ -350,10 +350,25 @@ __device__ __forceinline__ double step_one(const double* mt, const double* src, 
 // __syncwarp only. M2M sums the children's contributions into the parent in child
 // order (the reference's order, bench.cpp:280-284); L2L stages own+down of the parent
 // once (bench.cpp:308-309) and each warp accumulates into its child's local_down.
+// One output row of tensor_step: dst[r*L + n] = sum_k mt[k*L + n] * src[k*L*L + r] for
+// all n -- the L source values are loaded once per row instead of once per output.
+template <int L>
+__device__ __forceinline__ void step_row(const double* mt, const double* src, int r, double* out) {
+  double s[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) s[k] = src[k * L * L + r];
+#pragma unroll
+  for (int n = 0; n < L; ++n) {
+    double acc = 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) acc += mt[k * L + n] * s[k];
+    out[n] = acc;
+  }
+}
+
 template <int L, bool IS_M2M>
 __global__ void __launch_bounds__(256) k_transfer_warp(TransArgs a) {
   constexpr int L3 = L * L * L;
-  constexpr int PER = (L3 + 31) / 32;
   __shared__ double mats[2 * L * L];
   __shared__ double par[L3];
   __shared__ double buf[8][2][L3];
@@ -378,26 +393,32 @@ __global__ void __launch_bounds__(256) k_transfer_warp(TransArgs a) {
       __syncwarp();
       src = b1;
     }
-    for (int i = lane; i < L3; i += 32) b0[i] = step_one<L>(m0, src, i);
+    double o[L];
+    for (int r = lane; r < L * L; r += 32) {
+      step_row<L>(m0, src, r, o);
+#pragma unroll
+      for (int n = 0; n < L; ++n) b0[r * L + n] = o[n];
+    }
     __syncwarp();
-    for (int i = lane; i < L3; i += 32) b1[i] = step_one<L>(m1, b0, i);
+    for (int r = lane; r < L * L; r += 32) {
+      step_row<L>(m1, b0, r, o);
+#pragma unroll
+      for (int n = 0; n < L; ++n) b1[r * L + n] = o[n];
+    }
     __syncwarp();
     if (IS_M2M) {
-      double r[PER];
+      for (int r = lane; r < L * L; r += 32) {
+        step_row<L>(m2, b1, r, o);
 #pragma unroll
-      for (int o = 0; o < PER; ++o) {
-        const int i = lane + 32 * o;
-        if (i < L3) r[o] = step_one<L>(m2, b1, i);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int o = 0; o < PER; ++o) {
-        const int i = lane + 32 * o;
-        if (i < L3) b0[i] = r[o];
+        for (int n = 0; n < L; ++n) b0[r * L + n] = o[n];  // b0 is free again after pass 2
       }
     } else {
       double* out = a.out + size_t(ch) * a.ldE;
-      for (int i = lane; i < L3; i += 32) out[i] += step_one<L>(m2, b1, i);
+      for (int r = lane; r < L * L; r += 32) {
+        step_row<L>(m2, b1, r, o);
+#pragma unroll
+        for (int n = 0; n < L; ++n) out[r * L + n] += o[n];
+      }
     }
   }
   if (IS_M2M) {

@@ -107,15 +107,21 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
   double ctr[3];
   cell_center(a.geo, a.code[c], ctr);
   const uint32_t first = a.first[c], cnt = a.count[c];
+  double* out = a.expansion + size_t(c) * a.ldE;
+  // issue the loads of the first two particle chunks and of the accumulated
+  // coefficients together (one memory round trip instead of three)
+  const double4 zero4 = make_double4(0, 0, 0, 0);
+  const double4 q0 = lane < cnt ? a.pw[first + lane] : zero4;
+  const double4 q1 = lane + 32 < cnt ? a.pw[first + 32 + lane] : zero4;
   double acc[PP][L];
 #pragma unroll
   for (int i = 0; i < PP; ++i)
 #pragma unroll
-    for (int n = 0; n < L; ++n) acc[i][n] = 0.0;
+    for (int n = 0; n < L; ++n) acc[i][n] = (lane + 32 * i < L * L) ? out[(lane + 32 * i) * L + n] : 0.0;
   double(*sw)[3 * L + 1] = S[warp];
   for (uint32_t base = 0; base < cnt; base += 32) {
     if (base + lane < cnt) {
-      const double4 p = a.pw[first + base + lane];
+      const double4 p = base == 0 ? q0 : base == 32 ? q1 : a.pw[first + base + lane];
       double s[L];
       eval_all<L>(tn, (p.x - ctr[0]) * a.geo.inv, s);
 #pragma unroll
@@ -143,13 +149,12 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
     }
     __syncwarp();
   }
-  double* out = a.expansion + size_t(c) * a.ldE;
 #pragma unroll
   for (int i = 0; i < PP; ++i) {
     const int pr = lane + 32 * i;
     if (pr < L * L)
 #pragma unroll
-      for (int n = 0; n < L; ++n) out[pr * L + n] += acc[i][n];
+      for (int n = 0; n < L; ++n) out[pr * L + n] = acc[i][n];
   }
 }
 
@@ -214,8 +219,24 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
   constexpr int L3 = L * L * L;
   extern __shared__ __align__(16) double tot[];  // [L2P_CELLS][L3]
   __shared__ double tn[L * (L - 1) + 1];
+  __shared__ uint32_t cfirst[L2P_CELLS + 1];
+  __shared__ double cctr[L2P_CELLS][3];
   const uint32_t c0 = blockIdx.x * L2P_CELLS;
   const uint32_t nc = min(static_cast<uint32_t>(L2P_CELLS), a.ncells - c0);
+  const uint64_t p0 = a.first[c0], p1 = uint64_t(a.first[c0 + nc - 1]) + a.count[c0 + nc - 1];
+  // the first particle of each thread: position and accumulated fields in flight
+  // while the cells' totals are staged
+  const uint64_t s_first = p0 + threadIdx.x;
+  const double4 zero4 = make_double4(0, 0, 0, 0);
+  const double4 pf = s_first < p1 ? a.pw[s_first] : zero4;
+  double4* far4 = reinterpret_cast<double4*>(a.far);
+  const double4 ff = s_first < p1 ? far4[s_first] : zero4;
+  if (threadIdx.x < nc) {
+    const uint32_t c = c0 + threadIdx.x;
+    cfirst[threadIdx.x] = a.first[c];
+    cell_center(a.geo, a.code[c], cctr[threadIdx.x]);
+  }
+  if (threadIdx.x == 0) cfirst[nc] = static_cast<uint32_t>(p1);
   for (int i = threadIdx.x; i < L * (L - 1); i += L2P_THREADS) tn[i] = a.tn[i];
   for (uint32_t i = threadIdx.x; i < nc * L3; i += L2P_THREADS) {
     const uint32_t lc = i / L3, k = i % L3;
@@ -223,13 +244,13 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
     tot[i] = a.expansion[g] + a.down[g];
   }
   __syncthreads();
-  const uint64_t p0 = a.first[c0], p1 = uint64_t(a.first[c0 + nc - 1]) + a.count[c0 + nc - 1];
   const double inv = a.geo.inv;
-  for (uint64_t s = p0 + threadIdx.x; s < p1; s += L2P_THREADS) {
-    const uint32_t c = a.pcell[s];
-    double ctr[3];
-    cell_center(a.geo, a.code[c], ctr);
-    const double4 p = a.pw[s];
+  for (uint64_t s = s_first; s < p1; s += L2P_THREADS) {
+    uint32_t lc = 0;  // local cell of slot s (cells are contiguous in Morton order)
+    while (lc + 1 < nc && cfirst[lc + 1] <= s) ++lc;
+    const uint32_t c = c0 + lc;
+    const double* ctr = cctr[lc];
+    const double4 p = s == s_first ? pf : a.pw[s];
     const double rx = (p.x - ctr[0]) * inv, ry = (p.y - ctr[1]) * inv, rz = (p.z - ctr[2]) * inv;
     double sx[L], sy[L], sz[L], gx[L], gy[L], gz[L];
     eval_all<L>(tn, rx, sx);
@@ -259,13 +280,12 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
         dz = fma(ss, w, dz);
       }
     }
-    double4* f = reinterpret_cast<double4*>(a.far) + s;
-    double4 r = *f;
+    double4 r = s == s_first ? ff : far4[s];
     r.x += pot;
     r.y -= inv * dx;
     r.z -= inv * dy;
     r.w -= inv * dz;
-    *f = r;
+    far4[s] = r;
   }
 }
 

@@ -132,7 +132,7 @@ struct M2LTables {
   std::vector<uint32_t> perm[343];  // grid permutation per vector slot
   // stacked operators
   int R = 0;        // rows of the source-side stack = columns of the target-side stack
-  int ldY = 0;      // round_up(R, 16): stride of one target's compressed vector
+  int ldY = 0;      // round_up(R, 32): stride of one target's compressed vector
   int rowsA = 0;    // round_up(R, 64): padded M of phase A
   int rowsB = 0;    // round_up(l^3, 64)... padded M of phase B
   double* dM1 = nullptr;    // [8][rowsA][ldE]
@@ -155,7 +155,7 @@ struct fmmgpu_ctx {
   int order = 0;
   double eps = 0;
   int l3 = 0;
-  int ldE = 0;  // padded expansion stride (multiple of 16 doubles)
+  int ldE = 0;  // padded expansion stride (multiple of 32 doubles: whole GEMM k-slices)
   std::string err;
   cudaStream_t s_far = nullptr, s_near = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;

@@ -130,7 +130,7 @@ int fmmgpu_create(int device, int order, double eps, fmmgpu_ctx** out) {
     c->order = order;
     c->eps = eps;
     c->l3 = order * order * order;
-    c->ldE = round_up(c->l3, 16);
+    c->ldE = round_up(c->l3, 32);  // multiple of the GEMM k-slice (32)
     FMM_CUDA(cudaSetDevice(device));
     cudaMemPool_t pool;
     FMM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

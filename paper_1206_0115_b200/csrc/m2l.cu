@@ -184,8 +184,6 @@ void compute_factors(fmmgpu_ctx* c) {
 }
 
 // ------------------------------------------------------------------ GEMM kernels
-constexpr int BK = 16;
-constexpr int SPAD = 20;  // smem row stride in doubles (== 4 mod 16: conflict-free fragments)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -239,11 +237,12 @@ struct GemmArgs {
 // parity class q. Optional deterministic split-K for levels too small to fill the
 // GPU: split s writes its partial sums to part[s][t][row] and k_m2l_splitk_reduce
 // adds them in split order.
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int WM, int WN, int STAGES, int BK>
 __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
   constexpr int T = WM * WN * 32;
   constexpr int WTM = BM / WM, WTN = BN / WN;
   constexpr int MT = WTM / 8, NT = WTN / 8;
+  constexpr int SPAD = BK + 4;  // == 4 (mod 16): conflict-free fragment loads
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                              // [STAGES][BM][SPAD]
   double* Bs = smem + STAGES * BM * SPAD;         // [STAGES][BN][SPAD]
@@ -271,14 +270,14 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
     const int k0 = (kt0 + kt) * BK;
     double* as = As + stage * BM * SPAD;
     double* bs = Bs + stage * BN * SPAD;
-    for (int ch = tid; ch < BM * 8; ch += T) {
-      const int r = ch >> 3, q = (ch & 7) * 2;
+    for (int ch = tid; ch < BM * (BK / 2); ch += T) {
+      const int r = ch / (BK / 2), q = (ch % (BK / 2)) * 2;
       cp16(as + r * SPAD + q, A + size_t(r) * g.lda + k0 + q);
     }
     // Yt blocks of absent sources were never written by phase A and stay zero from
     // the allocation (one Yt per level), so the operand is a plain copy.
-    for (int ch = tid; ch < BN * 8; ch += T) {
-      const int j = ch >> 3, q = (ch & 7) * 2;
+    for (int ch = tid; ch < BN * (BK / 2); ch += T) {
+      const int j = ch / (BK / 2), q = (ch % (BK / 2)) * 2;
       const uint32_t cell = col_cell[j];
       const bool ok = cell != NPOS;
       cp16z(bs + j * SPAD + q, g.Yt + (ok ? size_t(cell) * g.ldY + k0 + q : 0), ok);
@@ -356,7 +355,8 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
 // M1_p (R rows) streams past them in BM x BK slices through a cp.async ring that
 // runs across M-tile boundaries, so the scatter epilogue of one M-tile overlaps the
 // loads of the next and no CTA pays a pipeline ramp per 64 x 64 tile.
-constexpr int PA_BM = 64, PA_BK = 16, PA_ST = 4, PA_THREADS = 256;
+constexpr int PA_BM = 64, PA_BK = 32, PA_ST = 3, PA_THREADS = 256;
+constexpr int PA_SPAD = PA_BK + 4;  // == 4 (mod 16)
 
 template <int BN, int WM, int WN>
 __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g) {
@@ -366,9 +366,9 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   extern __shared__ __align__(16) double smem[];
   const int wpad = g.K + 4;                       // == 4 (mod 16): conflict-free fragments
   double* Ws = smem;                              // [BN][wpad]
-  double* As = smem + BN * wpad;                  // [PA_ST][PA_BM][SPAD]
+  double* As = smem + BN * wpad;                  // [PA_ST][PA_BM][PA_SPAD]
   // [2][vtMax][BN] target cell of (vector of the M-tile, column), double-buffered by M-tile
-  uint32_t* tgt = reinterpret_cast<uint32_t*>(As + PA_ST * PA_BM * SPAD);
+  uint32_t* tgt = reinterpret_cast<uint32_t*>(As + PA_ST * PA_BM * PA_SPAD);
   __shared__ uint32_t col_cell[BN];
   __shared__ int col_ijk[BN][3];
 
@@ -411,11 +411,11 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   // ring producer position (tile, k-slice), advanced without divisions
   int pmt = mt0, pkt = 0, pstage = 0;
   auto load_next = [&]() {
-    double* as = As + pstage * PA_BM * SPAD;
+    double* as = As + pstage * PA_BM * PA_SPAD;
     const double* src = A + size_t(pmt * PA_BM) * g.lda + pkt * PA_BK;
     for (int ch = tid; ch < PA_BM * (PA_BK / 2); ch += PA_THREADS) {
       const int r = ch / (PA_BK / 2), q = (ch % (PA_BK / 2)) * 2;
-      cp16(as + r * SPAD + q, src + size_t(r) * g.lda + q);
+      cp16(as + r * PA_SPAD + q, src + size_t(r) * g.lda + q);
     }
     if (++pkt == KT) { pkt = 0; ++pmt; }
     if (++pstage == PA_ST) pstage = 0;
@@ -470,13 +470,13 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
       }
       if (kt_fill == KT - 1) __syncthreads();
     }
-    const double* as = As + stage * PA_BM * SPAD + (wm * WTM + gq) * SPAD + tq;
+    const double* as = As + stage * PA_BM * PA_SPAD + (wm * WTM + gq) * PA_SPAD + tq;
     const double* bs = Ws + (wn * WTN + gq) * wpad + kt * PA_BK + tq;
 #pragma unroll
     for (int kk = 0; kk < PA_BK; kk += 4) {
       double a[MT], b[NT];
 #pragma unroll
-      for (int i = 0; i < MT; ++i) a[i] = as[i * 8 * SPAD + kk];
+      for (int i = 0; i < MT; ++i) a[i] = as[i * 8 * PA_SPAD + kk];
 #pragma unroll
       for (int j = 0; j < NT; ++j) b[j] = bs[j * 8 * wpad + kk];
 #pragma unroll
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   cp_wait<0>();
 }
 
-constexpr int B_BM = 128, B_BN = 64, B_WM = 4, B_WN = 2, B_ST = 3;
+constexpr int B_BM = 128, B_BN = 64, B_WM = 4, B_WN = 2, B_ST = 2, B_BK = 32;
 
 }  // namespace
 
@@ -572,7 +572,7 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
     if (off != R) throw Error(FMMGPU_LOGIC_ERROR, "M2L source stack size mismatch");
   }
   T.R = R;
-  T.ldY = round_up(R, 16);
+  T.ldY = round_up(R, 32);
   T.rowsA = round_up(R, PA_BM);
   T.rowsB = round_up(n3, B_BM);
   std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
@@ -679,7 +679,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.K = c->ldE;
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
     auto launch = [&](auto kern, int bn) {
-      const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * SPAD) +
+      const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * PA_SPAD) +
                           sizeof(uint32_t) * 2 * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       // M-split so coarse levels still put >= 2 CTAs on every SM
@@ -705,13 +705,13 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     // deterministic split-K when the level has too few column tiles to fill 2 CTAs/SM
     const int mtiles = T.rowsB / B_BM;
     const uint32_t ctas = 8u * ((maxcls + B_BN - 1) / B_BN) * mtiles;
-    const int kt = T.ldY / BK;
+    const int kt = T.ldY / B_BK;
     int ks = 1;
     while (ks < 16 && ctas * ks < 2u * 148u && kt / (2 * ks) >= 8) ks *= 2;
     g.ksplit = ks;
     g.part = ks > 1 ? static_cast<double*>(scratch(c, sizeof(double) * ks * size_t(L.n) * c->ldE)) : nullptr;
-    const size_t smem = sizeof(double) * B_ST * (B_BM + B_BN) * SPAD;
-    auto kern = k_m2l_phase_b<B_BM, B_BN, B_WM, B_WN, B_ST>;
+    const size_t smem = sizeof(double) * B_ST * (B_BM + B_BN) * (B_BK + 4);
+    auto kern = k_m2l_phase_b<B_BM, B_BN, B_WM, B_WN, B_ST, B_BK>;
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     dim3 grid(mtiles, (maxcls + B_BN - 1) / B_BN, 8 * ks);
     kern<<<grid, B_WM * B_WN * 32, smem, s>>>(g);

@@ -153,6 +153,35 @@ int fmmgpu_time_evaluations(fmmgpu_ctx* ctx, int steps, double* total_ms, double
  * (or fmmgpu_evaluate) before reading fields. */
 int fmmgpu_time_operator(fmmgpu_ctx* ctx, int kind, int level, int reps, double* ms);
 
+/* ---- multi-GPU: contiguous Morton ranges of leaves -------------
+ * No reference counterpart (the reference is single-process); added by
+ * the north star. Every rank builds the whole tree from the whole particle set, then
+ * fmmgpu_partition makes this context rank `rank` of `nranks`: leaves are split into
+ * contiguous Morton ranges aligned to the cells of an alignment level and balanced by
+ * estimated work; levels below it are replicated. Evaluations then compute only the
+ * owned targets (gathered fields are zero for other particles), with one exchange per
+ * upward level >= the alignment level: an all-gather of that level's multipoles, done
+ * by an attached NCCL communicator inside fmmgpu_evaluate, or by the host between
+ * fmmgpu_upward_level calls (stepped API). nranks = 1 restores the full evaluation. */
+int fmmgpu_partition(fmmgpu_ctx* ctx, int rank, int nranks);
+/* first owned cell of every rank at `level` (nranks + 1 entries, last = cell count) */
+int fmmgpu_partition_ranges(const fmmgpu_ctx* ctx, int level, uint32_t* begins);
+int fmmgpu_partition_info(const fmmgpu_ctx* ctx, int* rank, int* nranks, int* align_level,
+                          uint64_t* slot_begin, uint64_t* slot_end);
+/* host-only balanced contiguous split of n weighted items: begins[nranks + 1] */
+int fmmgpu_plan_partition(const uint64_t* weights, uint32_t n, int nranks, uint32_t* begins);
+/* NCCL communicator (libnccl.so.2 loaded on first use): rank 0 creates the 128-byte
+ * id, every rank passes it to fmmgpu_comm_init. */
+int fmmgpu_comm_unique_id(char* out128);
+int fmmgpu_comm_init(fmmgpu_ctx* ctx, const char* id128, int nranks, int rank);
+int fmmgpu_comm_destroy(fmmgpu_ctx* ctx);
+/* stepped evaluation: fmmgpu_reset; fmmgpu_upward_level(leaf), (leaf-1), ..., (2)
+ * (P2M at the leaf, M2M above; owned or replicated cells), the caller exchanging each
+ * level >= the alignment level in between; then fmmgpu_downward (M2L, L2L, L2P, P2P,
+ * gather). Synchronous. */
+int fmmgpu_upward_level(fmmgpu_ctx* ctx, int level);
+int fmmgpu_downward(fmmgpu_ctx* ctx);
+
 /* bench.cpp:19-61 generate_particles (mt19937_64, explicit scaling); dist 0 uniform,
  * 1 sphere. Host-side input generator so both sides see identical doubles. */
 void fmmgpu_generate_particles(uint64_t n, int dist, uint64_t seed, double* xyzw);

@@ -84,8 +84,15 @@ def lib():
         for name in ("fmmgpu_reset", "fmmgpu_p2m", "fmmgpu_l2p", "fmmgpu_p2p", "fmmgpu_evaluate",
                      "fmmgpu_synchronize", "fmmgpu_build_lists"):
             getattr(L, name).argtypes = [c_void_p]
-        for name in ("fmmgpu_m2m", "fmmgpu_m2l", "fmmgpu_l2l"):
+        for name in ("fmmgpu_m2m", "fmmgpu_m2l", "fmmgpu_l2l", "fmmgpu_upward_level"):
             getattr(L, name).argtypes = [c_void_p, c_int]
+        L.fmmgpu_downward.argtypes = [c_void_p]
+        L.fmmgpu_partition.argtypes = [c_void_p, c_int, c_int]
+        L.fmmgpu_partition_ranges.argtypes = [c_void_p, c_int, c_void_p]
+        L.fmmgpu_plan_partition.argtypes = [c_void_p, ctypes.c_uint32, c_int, c_void_p]
+        L.fmmgpu_comm_init.argtypes = [c_void_p, ctypes.c_char_p, c_int, c_int]
+        L.fmmgpu_comm_destroy.argtypes = [c_void_p]
+        L.fmmgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
         _lib = L
     return _lib
 
@@ -104,6 +111,25 @@ class RunConfig:
     group_size: int = 250
     seed: int = 42
     device: int = 0
+
+
+def plan_partition(weights, nranks: int) -> np.ndarray:
+    """Balanced contiguous split of weighted items (host only): first item of each rank + end."""
+    w = np.ascontiguousarray(weights, dtype=np.uint64)
+    out = np.zeros(nranks + 1, dtype=np.uint32)
+    rc = lib().fmmgpu_plan_partition(_p(w) if len(w) else None, len(w), nranks, _p(out))
+    if rc:
+        raise _ERRORS.get(rc, FmmError)("plan_partition failed")
+    return out
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id (128 bytes) for fmmgpu_comm_init; create on rank 0 and broadcast."""
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().fmmgpu_comm_unique_id(buf)
+    if rc:
+        raise FmmError("ncclGetUniqueId failed")
+    return buf.raw
 
 
 def generate_particles(n: int, dist: str = "uniform", seed: int = 42) -> np.ndarray:
@@ -329,6 +355,32 @@ class FmmContext:
         self._check(self._lib.fmmgpu_time_evaluations(self.h, steps, byref(total), _p(ms), byref(nl)))
         keys = list(KINDS[:6]) + ["GATHER", "EVAL", "TREE", "LISTS"]
         return total.value, dict(zip(keys, ms.tolist())), nl.value
+
+    # -- multi-GPU partition
+    def partition(self, rank: int, nranks: int):
+        """Own a contiguous Morton range of leaves (rank of nranks); nranks=1 undoes it."""
+        self._check(self._lib.fmmgpu_partition(self.h, rank, nranks))
+
+    def partition_info(self):
+        r, n, a = c_int(), c_int(), c_int()
+        s0, s1 = c_uint64(), c_uint64()
+        self._check(self._lib.fmmgpu_partition_info(self.h, byref(r), byref(n), byref(a), byref(s0), byref(s1)))
+        return {"rank": r.value, "nranks": n.value, "align_level": a.value, "slots": (s0.value, s1.value)}
+
+    def partition_ranges(self, level: int):
+        n = self.partition_info()["nranks"]
+        out = np.zeros(n + 1, dtype=np.uint32)
+        self._check(self._lib.fmmgpu_partition_ranges(self.h, level, _p(out)))
+        return out
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        self._check(self._lib.fmmgpu_comm_init(self.h, uid, nranks, rank))
+
+    def upward_level(self, level: int):
+        self._check(self._lib.fmmgpu_upward_level(self.h, level))
+
+    def downward(self):
+        self._check(self._lib.fmmgpu_downward(self.h))
 
     def time_operator(self, kind: str, level: int = -1, reps: int = 5):
         """Isolated device time (ms per repetition) of one operator; leaves accumulators dirty."""

@@ -112,6 +112,14 @@ struct Level {
   uint32_t* map = nullptr;         // dense code -> index (sparse levels <= DENSE_MAP_MAX_LEVEL)
   uint32_t* cls_cells = nullptr;   // cell indices grouped by parity class (code & 7)
   uint32_t cls_off[9] = {};        // class offsets into cls_cells (host copy)
+  // partitioned runs (fmmgpu_partition): owned cells [own0, own1) -- every cell when the
+  // level is replicated -- and the M2L phase A source / phase B target lists per parity
+  // class (nullptr = cls_cells)
+  uint32_t own0 = 0, own1 = 0;
+  uint32_t* srcA = nullptr;
+  uint32_t srcA_off[9] = {};
+  uint32_t* tgtB = nullptr;
+  uint32_t tgtB_off[9] = {};
   double *multipole = nullptr, *local_own = nullptr, *local_down = nullptr;  // n x ldE
   double* yt = nullptr;  // M2L compressed intermediates, n x ldY (zero where no source)
   std::vector<uint32_t> block_offsets;
@@ -182,6 +190,12 @@ struct fmmgpu_ctx {
   double* d_near = nullptr;      // near-field fields [n] x {pot,fx,fy,fz} (Morton order)
   double* d_far = nullptr;       // far-field fields [n] x {pot,fx,fy,fz} (Morton order)
   double* d_out = nullptr;       // gathered fields [4][n] (input order)
+  // partition: this context is rank part_rank of part_n; levels below
+  // part_align are replicated; own_s0..own_s1 = owned Morton particle slots
+  int part_rank = 0, part_n = 1, part_align = 0;
+  uint64_t own_s0 = 0, own_s1 = 0;
+  void* nccl = nullptr;          // ncclComm_t when fmmgpu_comm_init attached one
+  std::vector<std::vector<uint32_t>> part_begin;  // per level: first owned cell of every rank (+ end)
   bool out_valid = false;        // d_out holds near + far of the current arrays
   int* d_flag = nullptr;         // error flags
   // near plan
@@ -213,6 +227,8 @@ void launch_l2p(fmmgpu_ctx* c, cudaStream_t s);
 void launch_m2l(fmmgpu_ctx* c, int level, cudaStream_t s);
 void launch_p2p(fmmgpu_ctx* c, cudaStream_t s);
 void launch_gather(fmmgpu_ctx* c, cudaStream_t s);
+void partition_free(fmmgpu_ctx* c);
+void exchange_level(fmmgpu_ctx* c, int v, cudaStream_t s);
 void* scratch(fmmgpu_ctx* c, size_t bytes);
 uint64_t near_directional_count(fmmgpu_ctx* c);
 int canonicalize_host(const int v[3], int perm[3], int sign[3]);

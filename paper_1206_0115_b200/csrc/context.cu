@@ -166,6 +166,7 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
     cudaStreamSynchronize(c->s_far);
     cudaStreamSynchronize(c->s_near);
     try {
+      partition_free(c);
       lists_free(c);
       tree_free(c);
     } catch (...) {
@@ -175,6 +176,7 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
     cudaStreamSynchronize(c->s_far);
   }
   m2l_free(c);
+  if (c->nccl) fmmgpu_comm_destroy(c);
   if (c->d_interp) cudaFree(c->d_interp);
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_canon) cudaFree(c->d_canon);
@@ -341,8 +343,12 @@ int fmmgpu_evaluate(fmmgpu_ctx* c) {
     FMM_CUDA(cudaEventRecord(e[7], c->s_near));
     FMM_CUDA(cudaEventRecord(e[1], s));
     launch_p2m(c, s);
+    exchange_level(c, leaf, s);  // partitioned runs: all-gather this level's multipoles
     FMM_CUDA(cudaEventRecord(e[2], s));
-    for (int v = leaf - 1; v >= 2; --v) launch_m2m(c, v, s);
+    for (int v = leaf - 1; v >= 2; --v) {
+      launch_m2m(c, v, s);
+      exchange_level(c, v, s);
+    }
     FMM_CUDA(cudaEventRecord(e[3], s));
     for (int v = 2; v <= leaf; ++v) launch_m2l(c, v, s);
     FMM_CUDA(cudaEventRecord(e[4], s));
@@ -356,6 +362,38 @@ int fmmgpu_evaluate(fmmgpu_ctx* c) {
     launch_gather(c, s);
     FMM_CUDA(cudaEventRecord(e[10], s));
     c->out_valid = true;
+  });
+}
+
+// Stepped evaluation for a host-driven exchange (partitioned runs without an attached
+// communicator): fmmgpu_reset, then fmmgpu_upward_level(leaf .. 2) with the host
+// all-gathering each level >= the alignment level between calls, then fmmgpu_downward.
+int fmmgpu_upward_level(fmmgpu_ctx* c, int v) {
+  return guarded(c, [&] {
+    need_level(c, v, 2, c->height - 1, "upward_level");
+    c->out_valid = false;
+    if (v == c->height - 1) launch_p2m(c, c->s_far);
+    else launch_m2m(c, v, c->s_far);
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+  });
+}
+
+int fmmgpu_downward(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    need_tree(c);
+    const int leaf = c->height - 1;
+    cudaStream_t s = c->s_far;
+    FMM_CUDA(cudaEventRecord(c->ev_fork, s));
+    FMM_CUDA(cudaStreamWaitEvent(c->s_near, c->ev_fork, 0));
+    launch_p2p(c, c->s_near);
+    for (int v = 2; v <= leaf; ++v) launch_m2l(c, v, s);
+    for (int v = 2; v < leaf; ++v) launch_l2l(c, v, s);
+    launch_l2p(c, s);
+    FMM_CUDA(cudaEventRecord(c->ev_join, c->s_near));
+    FMM_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+    launch_gather(c, s);
+    c->out_valid = true;
+    FMM_CUDA(cudaStreamSynchronize(s));
   });
 }
 

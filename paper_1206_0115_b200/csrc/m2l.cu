@@ -340,11 +340,15 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
   }
 }
 
+// over the targets of the phase B list only (the partials of other cells are unset)
 __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit, uint32_t ncells, int ldE, int l3,
-                                    double scale, double* __restrict__ local) {
-  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (i >= uint64_t(ncells) * ldE) return;
-  if (static_cast<int>(i % ldE) >= l3) return;
+                                    double scale, const uint32_t* __restrict__ targets, uint32_t ntargets,
+                                    double* __restrict__ local) {
+  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (e >= uint64_t(ntargets) * ldE) return;
+  const int row = static_cast<int>(e % ldE);
+  if (row >= l3) return;
+  const uint64_t i = uint64_t(targets[e / ldE]) * ldE + row;
   double s = part[i];
   for (int k = 1; k < ksplit; ++k) s += part[k * uint64_t(ncells) * ldE + i];
   local[i] += scale * s;
@@ -355,7 +359,7 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
 // M1_p (R rows) streams past them in BM x BK slices through a cp.async ring that
 // runs across M-tile boundaries, so the scatter epilogue of one M-tile overlaps the
 // loads of the next and no CTA pays a pipeline ramp per 64 x 64 tile.
-constexpr int PA_BM = 64, PA_BK = 32, PA_ST = 3, PA_THREADS = 256;
+constexpr int PA_BM = 64, PA_BK = 32, PA_ST = 2, PA_THREADS = 256;  // 2 CTAs/SM: W 68 KB + ring 37 KB
 constexpr int PA_SPAD = PA_BK + 4;  // == 4 (mod 16)
 
 template <int BN, int WM, int WN>
@@ -655,8 +659,10 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   }
   GemmArgs g{};
   g.lv = L.view(v);
-  g.cls_cells = L.cls_cells;
-  std::copy(L.cls_off, L.cls_off + 9, g.cls_off);
+  // phase A runs over the sources (partitioned: those with an owned target), phase B
+  // over the targets (partitioned: the owned ones)
+  g.cls_cells = L.srcA ? L.srcA : L.cls_cells;
+  std::copy(L.srcA ? L.srcA_off : L.cls_off, (L.srcA ? L.srcA_off : L.cls_off) + 9, g.cls_off);
   g.W = L.multipole;
   g.ldE = c->ldE;
   g.Yt = Lm.yt;
@@ -670,9 +676,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   g.l3 = c->l3;
   g.scale = 1.0 / (c->root[3] / static_cast<double>(uint64_t{1} << v));  // bench.cpp:233-234
   uint32_t maxcls = 0;
-  for (int q = 0; q < 8; ++q) maxcls = std::max(maxcls, L.cls_off[q + 1] - L.cls_off[q]);
-  if (maxcls == 0) return;
-  {
+  for (int q = 0; q < 8; ++q) maxcls = std::max(maxcls, g.cls_off[q + 1] - g.cls_off[q]);
+  if (maxcls) {
     g.A = T.dM1;
     g.lda = c->ldE;
     g.a_class_stride = size_t(T.rowsA) * c->ldE;
@@ -696,7 +701,11 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     else if (c->ldE <= 352) launch(k_m2l_phase_a<32, 4, 2>, 32);
     else launch(k_m2l_phase_a<16, 8, 1>, 16);
   }
-  {
+  g.cls_cells = L.tgtB ? L.tgtB : L.cls_cells;
+  std::copy(L.tgtB ? L.tgtB_off : L.cls_off, (L.tgtB ? L.tgtB_off : L.cls_off) + 9, g.cls_off);
+  maxcls = 0;
+  for (int q = 0; q < 8; ++q) maxcls = std::max(maxcls, g.cls_off[q + 1] - g.cls_off[q]);
+  if (maxcls) {
     g.A = T.dM2;
     g.lda = T.ldY;
     g.a_class_stride = size_t(T.rowsB) * T.ldY;
@@ -717,9 +726,10 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     kern<<<grid, B_WM * B_WN * 32, smem, s>>>(g);
     FMM_CUDA(cudaGetLastError());
     if (ks > 1) {
-      const uint64_t tot = uint64_t(L.n) * c->ldE;
-      k_m2l_splitk_reduce<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(g.part, ks, L.n, c->ldE, c->l3,
-                                                                                     g.scale, L.local_own);
+      const uint32_t ntg = g.cls_off[8];
+      const uint64_t tot = uint64_t(ntg) * c->ldE;
+      k_m2l_splitk_reduce<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(
+          g.part, ks, L.n, c->ldE, c->l3, g.scale, g.cls_cells, ntg, L.local_own);
       FMM_CUDA(cudaGetLastError());
       ++c->launches;
     }

@@ -31,6 +31,7 @@ constexpr int P2P_CAP = 3072;            // staged particles per chunk (96 KB), 
 struct P2PArgs {
   LevelView leaf;
   const uint64_t* parent_code;  // level leaf-1
+  uint32_t p0;                  // first parent of the launch (partitioned runs: owned range)
   const uint32_t* first;        // leaf first_particle
   const uint32_t* count;        // leaf particle_count
   const double4* pw;
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) k_p2p(const P2PArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   int pc[3];
-  demorton(a.parent_code[blockIdx.x], pc);
+  demorton(a.parent_code[a.p0 + blockIdx.x], pc);
   if (tid < 64) {
     const int qa = tid >> 4, qb = (tid >> 2) & 3, qc = tid & 3;
     const uint32_t cell = find_ijk(a.leaf, 2 * pc[0] - 1 + qa, 2 * pc[1] - 1 + qb, 2 * pc[2] - 1 + qc);
@@ -219,12 +220,13 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const int leaf = c->height - 1;
   const Level& L = c->lv[leaf];
   const Level& P = c->lv[leaf - 1];
-  if (P.n == 0) return;
-  P2PArgs a{L.view(leaf), P.code, L.first_particle, L.particle_count, c->d_pw,
+  const uint32_t np = P.own1 - P.own0;
+  if (np == 0) return;
+  P2PArgs a{L.view(leaf), P.code, P.own0, L.first_particle, L.particle_count, c->d_pw,
              reinterpret_cast<double4*>(c->d_near), c->n};
   const int smem = static_cast<int>(sizeof(P2PSmem));
   FMM_CUDA(cudaFuncSetAttribute(k_p2p, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_p2p<<<P.n, P2P_THREADS, smem, s>>>(a);
+  k_p2p<<<np, P2P_THREADS, smem, s>>>(a);
   FMM_CUDA(cudaGetLastError());
   ++c->launches;
 }

@@ -81,7 +81,8 @@ struct LeafArgs {
   const double* down;      // local_down (L2P)
   double* far;             // [n] x {pot, fx, fy, fz} (L2P), Morton order
   uint64_t n;
-  uint32_t ncells;
+  uint32_t cell0;   // first leaf cell of the launch (partitioned runs: the owned range)
+  uint32_t ncells;  // one past the last leaf cell of the launch
   int ldE;
   Geo geo;
 };
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < L * (L - 1); i += P2M_THREADS) tn[i] = a.tn[i];
   __syncthreads();
-  const uint32_t c = blockIdx.x * P2M_WARPS + warp;
+  const uint32_t c = a.cell0 + blockIdx.x * P2M_WARPS + warp;
   if (c >= a.ncells) return;
   double ctr[3];
   cell_center(a.geo, a.code[c], ctr);
@@ -158,57 +159,6 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
   }
 }
 
-template <int L>
-__global__ void __launch_bounds__(P2M_THREADS) k_p2m(LeafArgs a) {
-  constexpr int L3 = L * L * L;
-  constexpr int OPT = (L3 + P2M_THREADS - 1) / P2M_THREADS;
-  __shared__ double tn[L * (L - 1) + 1];
-  __shared__ double S[P2M_THREADS][3 * L];
-  const uint32_t c = blockIdx.x;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < L * (L - 1); i += P2M_THREADS) tn[i] = a.tn[i];
-  double ctr[3];
-  cell_center(a.geo, a.code[c], ctr);
-  const uint32_t first = a.first[c], cnt = a.count[c];
-  double acc[OPT];
-#pragma unroll
-  for (int o = 0; o < OPT; ++o) acc[o] = 0.0;
-  for (uint32_t base = 0; base < cnt; base += P2M_THREADS) {
-    __syncthreads();
-    if (tid < cnt - base) {
-      const double4 p = a.pw[first + base + tid];
-      double s[L];
-      eval_all<L>(tn, (p.x - ctr[0]) * a.geo.inv, s);
-#pragma unroll
-      for (int m = 0; m < L; ++m) S[tid][m] = p.w * s[m];
-      eval_all<L>(tn, (p.y - ctr[1]) * a.geo.inv, s);
-#pragma unroll
-      for (int m = 0; m < L; ++m) S[tid][L + m] = s[m];
-      eval_all<L>(tn, (p.z - ctr[2]) * a.geo.inv, s);
-#pragma unroll
-      for (int m = 0; m < L; ++m) S[tid][2 * L + m] = s[m];
-    }
-    __syncthreads();
-    const int m = (cnt - base < P2M_THREADS) ? static_cast<int>(cnt - base) : P2M_THREADS;
-#pragma unroll
-    for (int o = 0; o < OPT; ++o) {
-      const int idx = tid + o * P2M_THREADS;
-      if (idx < L3) {
-        const int n1 = idx / (L * L), n2 = (idx / L) % L, n3 = idx % L;
-        double s = acc[o];
-        for (int j = 0; j < m; ++j) s += (S[j][n1] * S[j][L + n2]) * S[j][2 * L + n3];
-        acc[o] = s;
-      }
-    }
-  }
-  double* out = a.expansion + size_t(c) * a.ldE;
-#pragma unroll
-  for (int o = 0; o < OPT; ++o) {
-    const int idx = tid + o * P2M_THREADS;
-    if (idx < L3) out[idx] += acc[o];
-  }
-}
-
 // L2P, CTA per run of L2P_CELLS consecutive leaf cells: total = own + down is formed
 // once per cell in shared memory (bench.cpp:320-325), then thread per particle of
 // those cells (contiguous in Morton order) reads it as (near-)broadcast LDS.
@@ -221,7 +171,7 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
   __shared__ double tn[L * (L - 1) + 1];
   __shared__ uint32_t cfirst[L2P_CELLS + 1];
   __shared__ double cctr[L2P_CELLS][3];
-  const uint32_t c0 = blockIdx.x * L2P_CELLS;
+  const uint32_t c0 = a.cell0 + blockIdx.x * L2P_CELLS;
   const uint32_t nc = min(static_cast<uint32_t>(L2P_CELLS), a.ncells - c0);
   const uint64_t p0 = a.first[c0], p1 = uint64_t(a.first[c0 + nc - 1]) + a.count[c0 + nc - 1];
   // the first particle of each thread: position and accumulated fields in flight
@@ -289,59 +239,6 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
   }
 }
 
-template <int L>
-__global__ void __launch_bounds__(128) k_l2p(LeafArgs a) {
-  constexpr int L3 = L * L * L;
-  __shared__ double tn[L * (L - 1) + 1];
-  for (int i = threadIdx.x; i < L * (L - 1); i += blockDim.x) tn[i] = a.tn[i];
-  __syncthreads();
-  const uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (s >= a.n) return;
-  const uint32_t c = a.pcell[s];
-  double ctr[3];
-  cell_center(a.geo, a.code[c], ctr);
-  const double4 p = a.pw[s];
-  const double inv = a.geo.inv;
-  const double rx = (p.x - ctr[0]) * inv, ry = (p.y - ctr[1]) * inv, rz = (p.z - ctr[2]) * inv;
-  double sx[L], sy[L], sz[L], gx[L], gy[L], gz[L];
-  eval_all<L>(tn, rx, sx);
-  eval_all<L>(tn, ry, sy);
-  eval_all<L>(tn, rz, sz);
-  grad_all<L>(tn, rx, gx);
-  grad_all<L>(tn, ry, gy);
-  grad_all<L>(tn, rz, gz);
-  const double* own = a.expansion + size_t(c) * a.ldE;
-  const double* down = a.down + size_t(c) * a.ldE;
-  double pot = 0, dx = 0, dy = 0, dz = 0;
-#pragma unroll 1
-  for (int n1 = 0; n1 < L; ++n1) {
-#pragma unroll
-    for (int n2 = 0; n2 < L; ++n2) {
-      double u = 0, w = 0;
-#pragma unroll
-      for (int n3 = 0; n3 < L; ++n3) {
-        const int i = (n1 * L + n2) * L + n3;
-        const double v = __ldg(own + i) + __ldg(down + i);
-        u += v * sz[n3];
-        w += v * gz[n3];
-      }
-      const double ss = sx[n1] * sy[n2];
-      pot += ss * u;
-      dx += gx[n1] * sy[n2] * u;
-      dy += sx[n1] * gy[n2] * u;
-      dz += ss * w;
-    }
-  }
-  (void)L3;
-  double4* f = reinterpret_cast<double4*>(a.far) + s;
-  double4 r = *f;
-  r.x += pot;
-  r.y -= inv * dx;
-  r.z -= inv * dy;
-  r.w -= inv * dz;
-  *f = r;
-}
-
 struct TransArgs {
   const uint64_t* child_code;
   const uint32_t* first_child;
@@ -351,6 +248,7 @@ struct TransArgs {
   const double* parent_b;  // L2L: local_down of parents
   const double* child_in;  // M2M: child multipoles
   double* out;             // M2M: parent multipole; L2L: child local_down
+  uint32_t p0;             // first parent of the launch (partitioned runs: the owned range)
   uint32_t nparents;
   int ldE;
 };
@@ -392,7 +290,7 @@ __global__ void __launch_bounds__(256) k_transfer_warp(TransArgs a) {
   __shared__ double mats[2 * L * L];
   __shared__ double par[L3];
   __shared__ double buf[8][2][L3];
-  const uint32_t p = blockIdx.x;
+  const uint32_t p = a.p0 + blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 2 * L * L; i += 256) mats[i] = a.mats[i];
   if (!IS_M2M)
@@ -458,7 +356,7 @@ __global__ void __launch_bounds__(128) k_transfer(TransArgs a) {
   constexpr int OPT = (L3 + 127) / 128;
   __shared__ double mats[2 * L * L];
   __shared__ double buf0[L3], buf1[L3], par[IS_M2M ? 1 : L3];
-  const uint32_t p = blockIdx.x;
+  const uint32_t p = a.p0 + blockIdx.x;
   const int tid = threadIdx.x;
   for (int i = tid; i < 2 * L * L; i += 128) mats[i] = a.mats[i];
   if (!IS_M2M)
@@ -506,12 +404,16 @@ __global__ void __launch_bounds__(128) k_transfer(TransArgs a) {
 
 // FmmContext::gather (bench.cpp:350-365): input slot o reads its Morton slot
 // inv[o] (one 32-byte sector per field array) and writes the four fields coalesced.
+// Partitioned runs own the Morton slots [s0, s1); other slots are written as zero.
 __global__ void k_gather(const double4* __restrict__ far, const double4* __restrict__ near,
-                         const uint32_t* __restrict__ inv, uint64_t n, double* __restrict__ out) {
+                         const uint32_t* __restrict__ inv, uint64_t n, uint64_t s0, uint64_t s1,
+                         double* __restrict__ out) {
   const uint64_t o = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (o >= n) return;
   const uint32_t s = inv[o];
-  const double4 f = far[s], e = near[s];
+  const bool own = s >= s0 && s < s1;
+  const double4 z = make_double4(0, 0, 0, 0);
+  const double4 f = own ? far[s] : z, e = own ? near[s] : z;
   out[o] = f.x + e.x;
   out[n + o] = f.y + e.y;
   out[2 * n + o] = f.z + e.z;
@@ -545,16 +447,18 @@ void dispatch_order(int order, Args&&... args) {
 template <int L>
 struct RunP2M {
   static void run(const LeafArgs& a, cudaStream_t s) {
-    if (a.ncells) k_p2m_warp<L><<<(a.ncells + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
+    const uint32_t nc = a.ncells - a.cell0;
+    if (nc) k_p2m_warp<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
   }
 };
 template <int L>
 struct RunL2P {
   static void run(const LeafArgs& a, cudaStream_t s) {
-    if (!a.ncells) return;
+    const uint32_t nc = a.ncells - a.cell0;
+    if (!nc) return;
     const int smem = static_cast<int>(sizeof(double) * L2P_CELLS * L * L * L);
     FMM_CUDA(cudaFuncSetAttribute(k_l2p_block<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_l2p_block<L><<<(a.ncells + L2P_CELLS - 1) / L2P_CELLS, L2P_THREADS, smem, s>>>(a);
+    k_l2p_block<L><<<(nc + L2P_CELLS - 1) / L2P_CELLS, L2P_THREADS, smem, s>>>(a);
   }
 };
 template <int L>
@@ -585,7 +489,8 @@ LeafArgs leaf_args(fmmgpu_ctx* c) {
   a.pcell = c->d_pcell;
   a.tn = c->d_interp;
   a.n = c->n;
-  a.ncells = L.n;
+  a.cell0 = L.own0;  // partitioned runs: this rank's leaves only
+  a.ncells = L.own1;
   a.ldE = c->ldE;
   a.geo = make_geo(c, leaf);
   return a;
@@ -665,7 +570,8 @@ void launch_m2m(fmmgpu_ctx* c, int v, cudaStream_t s) {
   a.mats = c->d_interp + 3 * l * l;  // child_t
   a.child_in = c->lv[v + 1].multipole;
   a.out = c->lv[v].multipole;
-  a.nparents = c->lv[v].n;
+  a.p0 = c->lv[v].own0;
+  a.nparents = c->lv[v].own1 - c->lv[v].own0;
   a.ldE = c->ldE;
   dispatch_order<RunM2M>(l, a, s);
   FMM_CUDA(cudaGetLastError());
@@ -682,7 +588,8 @@ void launch_l2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   a.parent_a = c->lv[v].local_own;
   a.parent_b = c->lv[v].local_down;
   a.out = c->lv[v + 1].local_down;
-  a.nparents = c->lv[v].n;
+  a.p0 = c->lv[v].own0;
+  a.nparents = c->lv[v].own1 - c->lv[v].own0;
   a.ldE = c->ldE;
   dispatch_order<RunL2L>(l, a, s);
   FMM_CUDA(cudaGetLastError());
@@ -691,7 +598,8 @@ void launch_l2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
 
 void launch_gather(fmmgpu_ctx* c, cudaStream_t s) {
   k_gather<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, s>>>(
-      reinterpret_cast<const double4*>(c->d_far), reinterpret_cast<const double4*>(c->d_near), c->d_inv, c->n, c->d_out);
+      reinterpret_cast<const double4*>(c->d_far), reinterpret_cast<const double4*>(c->d_near), c->d_inv, c->n,
+      c->own_s0, c->own_s1, c->d_out);
   FMM_CUDA(cudaGetLastError());
   ++c->launches;
 }

@@ -136,6 +136,7 @@ void free_level(fmmgpu::Level& L, cudaStream_t s) {
   dfree(L.first_child, s); dfree(L.child_count, s); dfree(L.map, s); dfree(L.cls_cells, s);
   dfree(L.multipole, s); dfree(L.local_own, s); dfree(L.local_down, s); dfree(L.yt, s);
   dfree(L.far_target, s); dfree(L.far_source, s); dfree(L.far_vec, s); dfree(L.far_group_off, s);
+  dfree(L.srcA, s); dfree(L.tgtB, s);
   L.far_pairs = 0;
 }
 
@@ -168,6 +169,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   if (n >= 0xffffffffull) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: particle count exceeds 32-bit ids");
   if (root4 && !(root4[3] > 0)) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: root cube width must be positive");
   cudaStream_t s = c->s_far;
+  partition_free(c);
   tree_free(c);
   lists_free(c);
 
@@ -326,6 +328,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
       dfree(oct_sorted, s);
       dfree(iota, s);
     }
+    V.own0 = 0;  // unpartitioned: every cell is owned
+    V.own1 = V.n;
     const size_t e = size_t(V.n) * c->ldE;
     V.multipole = dalloc<double>(e, s);
     V.local_own = dalloc<double>(e, s);
@@ -334,6 +338,11 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     FMM_CUDA(cudaMemsetAsync(V.local_own, 0, e * 8, s));
     FMM_CUDA(cudaMemsetAsync(V.local_down, 0, e * 8, s));
   }
+  c->part_rank = 0;
+  c->part_n = 1;
+  c->part_align = 0;
+  c->own_s0 = 0;
+  c->own_s1 = n;
   c->d_near = dalloc<double>(4 * n, s);
   c->d_far = dalloc<double>(4 * n, s);
   c->d_out = dalloc<double>(4 * n, s);

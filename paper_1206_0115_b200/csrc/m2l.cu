@@ -359,7 +359,7 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
 // M1_p (R rows) streams past them in BM x BK slices through a cp.async ring that
 // runs across M-tile boundaries, so the scatter epilogue of one M-tile overlaps the
 // loads of the next and no CTA pays a pipeline ramp per 64 x 64 tile.
-constexpr int PA_BM = 64, PA_BK = 32, PA_ST = 2, PA_THREADS = 256;  // 2 CTAs/SM: W 68 KB + ring 37 KB
+constexpr int PA_BM = 64, PA_BK = 16, PA_ST = 4, PA_THREADS = 256;  // 2 CTAs/SM: W 68 KB + ring 40 KB
 constexpr int PA_SPAD = PA_BK + 4;  // == 4 (mod 16)
 
 template <int BN, int WM, int WN>

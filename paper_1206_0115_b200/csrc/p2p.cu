@@ -18,14 +18,14 @@
 //
 // Per interaction: 3 DADD (d) + 3 DP (r^2) + MUFU.RSQ64H and 4 DP (rsqrt_nr)
 // + 1 DMUL (w/r) + 1 DADD (pot) + 2 DMUL (w/r^3) + 3 DFMA (force) = 18 DP ops.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fmmgpu {
 
 namespace {
 
-constexpr int P2P_WARPS = 12;            // pull work units (child passes) from a shared queue
-constexpr int P2P_THREADS = P2P_WARPS * 32;
 constexpr int P2P_CAP = 3072;            // staged particles per chunk (96 KB), multiple of 4
 
 struct P2PArgs {
@@ -39,9 +39,10 @@ struct P2PArgs {
   uint64_t n;
 };
 
+template <int WARPS>
 struct P2PSmem {
-  double4 src[P2P_CAP];
-  double red[P2P_WARPS][4][32];
+  double4 src[P2P_CAP + 4];  // + one group of zero-weight sources (tail of a 2-group step)
+  double red[WARPS][4][32];
   uint32_t first[64];
   uint32_t cnt[64];
   uint32_t voff[65];  // virtual offsets of the 64 positions (prefix sum of counts padded to 4)
@@ -69,9 +70,12 @@ __device__ __forceinline__ void interact(const double xi, const double yi, const
   fz = fma(s3, dz, fz);
 }
 
-__global__ void __launch_bounds__(P2P_THREADS, 2) k_p2p(const P2PArgs a) {
+// WARPS warps per CTA pull the work units; G groups of 4 sources per inner iteration.
+template <int WARPS, int G>
+__global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
+  constexpr int P2P_THREADS = WARPS * 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  P2PSmem& sm = *reinterpret_cast<P2PSmem*>(smem_raw);
+  P2PSmem<WARPS>& sm = *reinterpret_cast<P2PSmem<WARPS>*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   int pc[3];
@@ -102,6 +106,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) k_p2p(const P2PArgs a) {
   // CTA whose children differ in size still keeps all 8 warps busy to the end (a
   // static warp-per-child mapping idles ~20% at ~38 particles per leaf). Each unit
   // owns distinct targets, so results do not depend on which warp takes it.
+  if (tid < 4) sm.src[P2P_CAP + tid] = dummy_source();
   if (tid == 0) {
     uint32_t acc = 0;
     for (int w = 0; w < 8; ++w) {
@@ -169,20 +174,36 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) k_p2p(const P2PArgs a) {
       const double4 xi = a.pw[tg];
       double pot = 0, fx = 0, fy = 0, fz = 0;
       if (active) {
+        // the 27 neighbour positions as 9 runs of 3 consecutive positions (qc = cc..cc+2),
+        // whose padded segments are contiguous in shared memory
 #pragma unroll 1
-        for (int q = 0; q < 27; ++q) {
-          const int pos = ((ca + q / 9) << 4) | ((cb + (q / 3) % 3) << 2) | (cc + q % 3);
-          // intersection of the position's virtual range with this chunk, chunk-relative
+        for (int q = 0; q < 9; ++q) {
+          const int pos = ((ca + q / 3) << 4) | ((cb + q % 3) << 2) | cc;
+          // intersection of the run's virtual range with this chunk, chunk-relative
           // (segments are padded to groups of 4 and chunks are multiples of 4)
-          const uint32_t v0 = max(sm.voff[pos], base), v1 = min(sm.voff[pos + 1], base + clen);
+          const uint32_t v0 = max(sm.voff[pos], base), v1 = min(sm.voff[pos + 3], base + clen);
           const int g1 = static_cast<int>(v1 - base) >> 2;
-          for (int g = (static_cast<int>(v0 - base) >> 2) + static_cast<int>(split); g < g1; g += S) {
+          const int gs = static_cast<int>(S);
+          for (int g = (static_cast<int>(v0 - base) >> 2) + static_cast<int>(split); g < g1; g += G * gs) {
             const double4* sj = sm.src + 4 * g;
             const double4 p0 = sj[0], p1 = sj[1], p2 = sj[2], p3 = sj[3];
-            interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
-            interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
-            interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
-            interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
+            if constexpr (G == 2) {
+              const double4* sk = (g + gs < g1) ? sm.src + 4 * (g + gs) : sm.src + P2P_CAP;
+              const double4 p4 = sk[0], p5 = sk[1], p6 = sk[2], p7 = sk[3];
+              interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p4, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p5, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p6, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p7, pot, fx, fy, fz);
+            } else {
+              interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
+              interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
+            }
           }
         }
       }
@@ -224,9 +245,21 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   if (np == 0) return;
   P2PArgs a{L.view(leaf), P.code, P.own0, L.first_particle, L.particle_count, c->d_pw,
              reinterpret_cast<double4*>(c->d_near), c->n};
-  const int smem = static_cast<int>(sizeof(P2PSmem));
-  FMM_CUDA(cudaFuncSetAttribute(k_p2p, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_p2p<<<np, P2P_THREADS, smem, s>>>(a);
+  auto run = [&](auto kern, int warps, int smem) {
+    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<np, warps * 32, smem, s>>>(a);
+  };
+  // FMMGPU_P2P_VARIANT (tuning experiments): 0 = 12 warps x 1 group, 1 = 8 x 2, 2 = 16 x 1, 3 = 8 x 1
+  static const int variant = [] {
+    const char* e = std::getenv("FMMGPU_P2P_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  switch (variant) {
+    case 1: run(k_p2p<8, 2>, 8, static_cast<int>(sizeof(P2PSmem<8>))); break;
+    case 2: run(k_p2p<16, 1>, 16, static_cast<int>(sizeof(P2PSmem<16>))); break;
+    case 3: run(k_p2p<8, 1>, 8, static_cast<int>(sizeof(P2PSmem<8>))); break;
+    default: run(k_p2p<12, 1>, 12, static_cast<int>(sizeof(P2PSmem<12>))); break;
+  }
   FMM_CUDA(cudaGetLastError());
   ++c->launches;
 }

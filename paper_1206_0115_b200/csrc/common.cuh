@@ -147,8 +147,6 @@ struct M2LTables {
   double* dM2 = nullptr;    // [8][rowsB][ldY]
   int4* dRowA = nullptr;    // [8][rowsA]: {slot or -1, destination column in Yt, vector index in its M-tile, 0}
   int* dTileVec = nullptr;  // [8][rowsA/64][vtMax]: vector slots of each 64-row M-tile (-1 = none)
-  int2* dKsrc = nullptr;    // [8][ldY]: {vector slot or -1, row of the source-side stack} (gather variant)
-  int variant = 0;          // 0: scatter in phase A; 1: dense phase A, gather in phase B
   int vtMax = 0;            // max distinct vectors in one 64-row M-tile
   int* dKslot = nullptr;    // [8][ldY]: vector slot of column kk of the target stack, -1 = pad
 };

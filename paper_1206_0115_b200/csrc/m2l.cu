@@ -225,8 +225,6 @@ struct GemmArgs {
   int vtMax;
   int rowsA;
   const int* kslot;       // vector slot per target-stack column [8][ldY] (host tables)
-  const int2* ksrc;       // gather variant: {slot, source-stack row} per target-stack column [8][ldY]
-  int R;                  // rows of the stacked operators (unpadded)
   double* local;          // phase B output (local_own)
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
   int msplit;             // phase A M-split factor (coarse levels)
@@ -339,218 +337,6 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
         } else {
           g.part[(size_t(split) * g.ncells + t) * g.ldE + row] = acc[i][j][e];
         }
-      }
-  }
-}
-
-// ---- gather variant: phase A writes each source's stacked vector Ys[s][0..R) densely;
-// phase B gathers, for target t of parity q and target-stack column k (vector v), the
-// element Ys[t + v][row_q(k)] (zero when the source t + v does not exist). No scatter,
-// no per-level zeroing, and phase A's epilogue is a plain coalesced store.
-template <int BN, int WM, int WN>
-__global__ void __launch_bounds__(256, 2) k_m2l_phase_a_dense(const GemmArgs g) {
-  constexpr int BM = 64, BK = 16, ST = 4, SP = BK + 4, T = 256;
-  static_assert(WM * WN * 32 == T, "8 warps");
-  constexpr int WTM = BM / WM, WTN = BN / WN;
-  constexpr int MT = WTM / 8, NT = WTN / 8;
-  extern __shared__ __align__(16) double smem[];
-  const int wpad = g.K + 4;
-  double* Ws = smem;                // [BN][wpad]
-  double* As = smem + BN * wpad;    // [ST][BM][SP]
-  __shared__ uint32_t col_cell[BN];
-  const int cls = blockIdx.y;
-  const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
-  const uint32_t n0 = blockIdx.x * BN;
-  if (n0 >= ncls) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = warp / WN, wn = warp % WN;
-  const int gq = lane >> 2, tq = lane & 3;
-  for (int j = tid; j < BN; j += T) col_cell[j] = (n0 + j < ncls) ? g.cls_cells[g.cls_off[cls] + n0 + j] : NPOS;
-  __syncthreads();
-  const int kc = g.K / 2;
-  for (int ch = tid; ch < BN * kc; ch += T) {
-    const int j = ch / kc, q = (ch % kc) * 2;
-    const uint32_t cell = col_cell[j];
-    const bool ok = cell != NPOS;
-    cp16z(Ws + j * wpad + q, g.W + (ok ? size_t(cell) * g.ldE + q : 0), ok);
-  }
-  cp_commit();
-  const double* A = g.A + cls * g.a_class_stride;
-  const int KT = g.K / BK, MTILES = g.rowsA / BM;
-  const int per = (MTILES + g.msplit - 1) / g.msplit;
-  const int mt0 = blockIdx.z * per, mt1 = min(MTILES, mt0 + per);
-  if (mt0 >= mt1) return;
-  const int TOTAL = (mt1 - mt0) * KT;
-  int pmt = mt0, pkt = 0, pstage = 0;
-  auto load_next = [&]() {
-    double* as = As + pstage * BM * SP;
-    const double* src = A + size_t(pmt * BM) * g.lda + pkt * BK;
-    for (int ch = tid; ch < BM * (BK / 2); ch += T) {
-      const int r = ch / (BK / 2), q = (ch % (BK / 2)) * 2;
-      cp16(as + r * SP + q, src + size_t(r) * g.lda + q);
-    }
-    if (++pkt == KT) { pkt = 0; ++pmt; }
-    if (++pstage == ST) pstage = 0;
-  };
-#pragma unroll
-  for (int s = 0; s < ST - 1; ++s) {
-    if (s < TOTAL) load_next();
-    cp_commit();
-  }
-  double acc[MT][NT][2];
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  int mt = mt0, kt = 0, stage = 0;
-  for (int t = 0; t < TOTAL; ++t) {
-    cp_wait<ST - 2>();
-    __syncthreads();
-    if (t + ST - 1 < TOTAL) load_next();
-    cp_commit();
-    const double* as = As + stage * BM * SP + (wm * WTM + gq) * SP + tq;
-    const double* bs = Ws + (wn * WTN + gq) * wpad + kt * BK + tq;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double a[MT], b[NT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) a[i] = as[i * 8 * SP + kk];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = bs[j * 8 * wpad + kk];
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-    }
-    if (kt == KT - 1) {
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const int row = mt * BM + wm * WTM + i * 8 + gq;
-        if (row < g.R) {
-#pragma unroll
-          for (int j = 0; j < NT; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const uint32_t cell = col_cell[wn * WTN + j * 8 + 2 * tq + e];
-              if (cell != NPOS) g.Yt[size_t(cell) * g.ldY + row] = acc[i][j][e];
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      }
-    }
-    if (++stage == ST) stage = 0;
-    if (++kt == KT) { kt = 0; ++mt; }
-  }
-  cp_wait<0>();
-}
-
-template <int BM, int BN, int WM, int WN, int STAGES, int BK>
-__global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b_gather(const GemmArgs g) {
-  constexpr int T = WM * WN * 32;
-  constexpr int WTM = BM / WM, WTN = BN / WN;
-  constexpr int MT = WTM / 8, NT = WTN / 8;
-  constexpr int SPAD = BK + 4;
-  static_assert(BN * BK / 8 == T, "one 8-column octet of one target per thread and k-slice");
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
-  double* Bs = smem + STAGES * BM * SPAD;
-  __shared__ uint32_t col_cell[BN];
-  __shared__ int col_ijk[BN][3];
-  const int cls = blockIdx.z / g.ksplit, split = blockIdx.z % g.ksplit;
-  const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
-  const uint32_t n0 = blockIdx.y * BN;
-  if (n0 >= ncls) return;
-  const int m0 = blockIdx.x * BM;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = warp / WN, wn = warp % WN;
-  const int gq = lane >> 2, tq = lane & 3;
-  for (int j = tid; j < BN; j += T) {
-    const uint32_t cell = (n0 + j < ncls) ? g.cls_cells[g.cls_off[cls] + n0 + j] : NPOS;
-    col_cell[j] = cell;
-    int ijk[3] = {0, 0, 0};
-    if (cell != NPOS) demorton(g.lv.code[cell], ijk);
-    col_ijk[j][0] = ijk[0];
-    col_ijk[j][1] = ijk[1];
-    col_ijk[j][2] = ijk[2];
-  }
-  __syncthreads();
-  const double* A = g.A + cls * g.a_class_stride + size_t(m0) * g.lda;
-  const int2* ks = g.ksrc + cls * g.ldY;
-  const int KTALL = g.K / BK;
-  const int per = (KTALL + g.ksplit - 1) / g.ksplit;
-  const int kt0 = split * per;
-  const int KT = max(0, min(KTALL, kt0 + per) - kt0);
-  const int bj = tid / (BK / 8), bo = (tid % (BK / 8)) * 8;  // this thread's target / octet
-  const uint32_t tcell = col_cell[bj];
-  const int ti = col_ijk[bj][0], tj = col_ijk[bj][1], tk = col_ijk[bj][2];
-  auto load_tile = [&](int stage, int kt) {
-    const int k0 = (kt0 + kt) * BK;
-    double* as = As + stage * BM * SPAD;
-    double* bs = Bs + stage * BN * SPAD;
-    for (int ch = tid; ch < BM * (BK / 2); ch += T) {
-      const int r = ch / (BK / 2), q = (ch % (BK / 2)) * 2;
-      cp16(as + r * SPAD + q, A + size_t(r) * g.lda + k0 + q);
-    }
-    int last = -2;
-    uint32_t src = NPOS;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int2 e = __ldg(ks + k0 + bo + u);
-      if (e.x != last) {
-        last = e.x;
-        src = (e.x >= 0 && tcell != NPOS)
-                  ? find_ijk(g.lv, ti + (e.x / 49 - 3), tj + ((e.x / 7) % 7 - 3), tk + (e.x % 7 - 3))
-                  : NPOS;
-      }
-      const bool ok = src != NPOS;
-      cp8z(bs + bj * SPAD + bo + u, g.Yt + (ok ? size_t(src) * g.ldY + e.y : 0), ok);
-    }
-  };
-  double acc[MT][NT][2];
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < KT) load_tile(st, st);
-    cp_commit();
-  }
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_wait<STAGES - 2>();
-    __syncthreads();
-    const int pf = kt + STAGES - 1;
-    if (pf < KT) load_tile(pf % STAGES, pf);
-    cp_commit();
-    const double* as = As + (kt % STAGES) * BM * SPAD + (wm * WTM + gq) * SPAD + tq;
-    const double* bs = Bs + (kt % STAGES) * BN * SPAD + (wn * WTN + gq) * SPAD + tq;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double a[MT], b[NT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) a[i] = as[i * 8 * SPAD + kk];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = bs[j * 8 * SPAD + kk];
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-    }
-  }
-  cp_wait<0>();
-#pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int row = m0 + wm * WTM + i * 8 + gq;
-    if (row >= g.l3) continue;
-#pragma unroll
-    for (int j = 0; j < NT; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const uint32_t t = col_cell[wn * WTN + j * 8 + 2 * tq + e];
-        if (t == NPOS) continue;
-        if (g.ksplit == 1) g.local[size_t(t) * g.ldE + row] += g.scale * acc[i][j][e];
-        else g.part[(size_t(split) * g.ncells + t) * g.ldE + row] = acc[i][j][e];
       }
   }
 }
@@ -737,8 +523,6 @@ void m2l_free(fmmgpu_ctx* c) {
   if (T.dM2) cudaFree(T.dM2);
   if (T.dRowA) cudaFree(T.dRowA);
   if (T.dTileVec) cudaFree(T.dTileVec);
-  if (T.dKsrc) cudaFree(T.dKsrc);
-  T.dKsrc = nullptr;
   T.dTileVec = nullptr;
   if (T.dKslot) cudaFree(T.dKslot);
   T.dM1 = T.dM2 = nullptr;
@@ -799,7 +583,6 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
   std::vector<int4> rowA(size_t(8) * T.rowsA, make_int4(-1, 0, 0, 0));
   std::vector<int> kslot(size_t(8) * T.ldY, -1);
-  std::vector<int2> ksrc(size_t(8) * T.ldY, make_int2(-1, 0));
   for (int p = 0; p < 8; ++p)
     for (int s = 0; s < 343; ++s) {
       const int oa = offA[p * 343 + s];
@@ -813,7 +596,6 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
           double* row = &M1[(size_t(p) * T.rowsA + oa + k) * c->ldE];
           for (int n = 0; n < n3; ++n) row[n] = T.sigma[cl][k] * T.v[cl][size_t(T.perm[s][n]) * r + k];
           rowA[size_t(p) * T.rowsA + oa + k] = make_int4(s, ob + k, 0, 0);
-          ksrc[size_t(q) * T.ldY + ob + k] = make_int2(s, oa + k);
         }
       }
       const int ob = offB[p * 343 + s];  // here p plays the target parity q
@@ -857,9 +639,6 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   FMM_CUDA(cudaMemcpy(T.dTileVec, tileVec.data(), tileVec.size() * sizeof(int), cudaMemcpyHostToDevice));
   FMM_CUDA(cudaMalloc(&T.dRowA, rowA.size() * sizeof(int4)));
   FMM_CUDA(cudaMalloc(&T.dKslot, kslot.size() * sizeof(int)));
-  FMM_CUDA(cudaMalloc(&T.dKsrc, ksrc.size() * sizeof(int2)));
-  FMM_CUDA(cudaMemcpy(T.dKsrc, ksrc.data(), ksrc.size() * sizeof(int2), cudaMemcpyHostToDevice));
-  if (const char* e = std::getenv("FMMGPU_M2L_VARIANT")) T.variant = std::atoi(e);
   FMM_CUDA(cudaMemcpy(T.dM1, M1.data(), M1.size() * sizeof(double), cudaMemcpyHostToDevice));
   FMM_CUDA(cudaMemcpy(T.dM2, M2.data(), M2.size() * sizeof(double), cudaMemcpyHostToDevice));
   FMM_CUDA(cudaMemcpy(T.dRowA, rowA.data(), rowA.size() * sizeof(int4), cudaMemcpyHostToDevice));
@@ -890,8 +669,6 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   g.Yt = Lm.yt;
   g.ldY = T.ldY;
   g.rowA = T.dRowA;
-  g.ksrc = T.dKsrc;
-  g.R = T.R;
   g.tileVec = T.dTileVec;
   g.vtMax = T.vtMax;
   g.rowsA = T.rowsA;
@@ -921,22 +698,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       kern<<<grid, PA_THREADS, smem, s>>>(g);
       FMM_CUDA(cudaGetLastError());
     };
-    if (T.variant == 1) {
-      auto launch_d = [&](auto kern, int bn) {
-        const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(4) * 64 * 20);
-        FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        const uint32_t ncols = 8u * ((maxcls + bn - 1) / bn);
-        const int mtiles = T.rowsA / PA_BM;
-        int ms = 1;
-        while (ms < mtiles && ncols * ms < 2u * 148u) ++ms;
-        g.msplit = ms;
-        kern<<<dim3((maxcls + bn - 1) / bn, 8, ms), 256, smem, s>>>(g);
-        FMM_CUDA(cudaGetLastError());
-      };
-      if (c->ldE <= 128) launch_d(k_m2l_phase_a_dense<64, 2, 4>, 64);
-      else if (c->ldE <= 352) launch_d(k_m2l_phase_a_dense<32, 4, 2>, 32);
-      else launch_d(k_m2l_phase_a_dense<16, 8, 1>, 16);
-    } else if (c->ldE <= 128) launch(k_m2l_phase_a<64, 2, 4>, 64);
+    if (c->ldE <= 128) launch(k_m2l_phase_a<64, 2, 4>, 64);
     else if (c->ldE <= 352) launch(k_m2l_phase_a<32, 4, 2>, 32);
     else launch(k_m2l_phase_a<16, 8, 1>, 16);
   }
@@ -959,8 +721,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.ksplit = ks;
     g.part = ks > 1 ? static_cast<double*>(scratch(c, sizeof(double) * ks * size_t(L.n) * c->ldE)) : nullptr;
     const size_t smem = sizeof(double) * B_ST * (B_BM + B_BN) * (B_BK + 4);
-    auto kern = T.variant == 1 ? k_m2l_phase_b_gather<B_BM, B_BN, B_WM, B_WN, B_ST, B_BK>
-                               : k_m2l_phase_b<B_BM, B_BN, B_WM, B_WN, B_ST, B_BK>;
+    auto kern = k_m2l_phase_b<B_BM, B_BN, B_WM, B_WN, B_ST, B_BK>;
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     dim3 grid(mtiles, (maxcls + B_BN - 1) / B_BN, 8 * ks);
     kern<<<grid, B_WM * B_WN * 32, smem, s>>>(g);

@@ -33,10 +33,15 @@ CONFIGS = {
     "A": (100_000, "uniform", 4, 5, "uniform cube N=100k, height 4, order 5"),
     "B": (10_000_000, "uniform", 7, 5, "uniform cube N=10M, height 7, order 5"),
     "C": (10_000_000, "uniform", 7, 7, "uniform cube N=10M, height 7, order 7"),
+    "D": (20_000_000, "ellipsoid", 8, 5, "ellipsoid surface (semi-axes 0.5, 0.35, 0.2) N=20M, height 8, order 5"),
+    "E": (100_000_000, "uniform", 8, 5, "uniform cube N=100M, height 8, order 5"),
 }
 # Bounded CPU sample of config B: same particles per leaf (~38) and order, one level
 # shallower (1/8 of the particles): the reference's per-particle work is the same.
-CPU_SAMPLE = {"B": (1_250_000, "uniform", 6, 5), "C": (1_250_000, "uniform", 6, 7), "A": (100_000, "uniform", 4, 5)}
+CPU_SAMPLE = {"B": (1_250_000, "uniform", 6, 5), "C": (1_250_000, "uniform", 6, 7), "A": (100_000, "uniform", 4, 5),
+              "D": (1_250_000, "ellipsoid", 6, 5), "E": (1_562_500, "uniform", 6, 5)}
+# (volume clouds keep N / 8^h, the surface cloud N / 4^h: same particles per leaf as the
+# full configuration, so the reference's per-particle work is the same)
 
 METRIC = "FMM eval time (s) and Mparticles/s at N=10M, order 5; scaling 1/2/4/8 B200"
 UNIT = "Mparticles/s"
@@ -168,9 +173,9 @@ def reference_sample(cfg_name, workers, warmup, steps):
         kind, workers, setup = "port", 1, None
     rates = [n / t / 1e6 for t in times]
     info = {"kind": kind, "cores": workers,
-            "sample": f"N={n} {dist}, height {h}, order {order} (config {cfg_name} at the same ~38 particles "
-                      f"per leaf, 1/8 of the particles); timed = the reference's execute() of the whole task "
-                      f"graph ({'%d workers' % workers}), setup ({setup and round(setup, 2)} s) excluded"}
+            "sample": f"N={n} {dist}, height {h}, order {order} (config {cfg_name} at the same particles per "
+                      f"leaf, 1/{CONFIGS[cfg_name][0] // n} of the particles); timed = the reference's execute() of "
+                      f"the whole task graph ({'%d workers' % workers}), setup ({setup and round(setup, 2)} s) excluded"}
     return rates, info
 
 

@@ -183,7 +183,8 @@ int fmmgpu_upward_level(fmmgpu_ctx* ctx, int level);
 int fmmgpu_downward(fmmgpu_ctx* ctx);
 
 /* bench.cpp:19-61 generate_particles (mt19937_64, explicit scaling); dist 0 uniform,
- * 1 sphere. Host-side input generator so both sides see identical doubles. */
+ * 1 sphere, 2 ellipsoid surface (config D: the sphere's directions on semi-axes
+ * 0.5, 0.35, 0.2). Host-side input generator so both sides see identical doubles. */
 void fmmgpu_generate_particles(uint64_t n, int dist, uint64_t seed, double* xyzw);
 
 #ifdef __cplusplus

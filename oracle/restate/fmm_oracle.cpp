@@ -953,9 +953,13 @@ void orc_generate_particles(u64 n, int dist, u64 seed, double* xyzw) {
       normal_pair(gz, spare);
       norm = std::sqrt(gx * gx + gy * gy + gz * gz);
     } while (norm < 1e-12);
-    xyzw[4 * i] = 0.5 + 0.5 * gx / norm;
-    xyzw[4 * i + 1] = 0.5 + 0.5 * gy / norm;
-    xyzw[4 * i + 2] = 0.5 + 0.5 * gz / norm;
+    // dist 1: the reference's sphere (bench.cpp:40-59); dist 2: BASELINE.json config D's
+    // "ellipsoid surface", defined as the same directions on semi-axes
+    // (0.5, 0.35, 0.2) about (1/2, 1/2, 1/2)
+    const double ax = 0.5, ay = dist == 2 ? 0.35 : 0.5, az = dist == 2 ? 0.2 : 0.5;
+    xyzw[4 * i] = 0.5 + ax * gx / norm;
+    xyzw[4 * i + 1] = 0.5 + ay * gy / norm;
+    xyzw[4 * i + 2] = 0.5 + az * gz / norm;
     xyzw[4 * i + 3] = 1.0;
   }
 }

@@ -28,6 +28,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfmmgpu.so")
 
 KINDS = ("P2M", "M2M", "M2L", "L2L", "L2P", "P2P", "P2PREDUCE")
+DISTS = {"uniform": 0, "sphere": 1, "ellipsoid": 2}
 CELL_DTYPE = np.dtype(
     [("code", "<u8"), ("first_particle", "<u4"), ("particle_count", "<u4"), ("parent", "<u4"),
      ("first_child", "<u4"), ("child_count", "<u4"), ("_pad", "<u4")])
@@ -133,9 +134,10 @@ def comm_unique_id() -> bytes:
 
 
 def generate_particles(n: int, dist: str = "uniform", seed: int = 42) -> np.ndarray:
-    """bench.cpp:29-61: (n, 4) array of x, y, z, w (unit weights)."""
+    """bench.cpp:29-61: (n, 4) array of x, y, z, w (unit weights); dist uniform, sphere or
+    ellipsoid (config D: the sphere's directions on semi-axes 0.5, 0.35, 0.2)."""
     out = np.zeros((n, 4), dtype=np.float64)
-    lib().fmmgpu_generate_particles(n, 0 if dist == "uniform" else 1, seed, _p(out))
+    lib().fmmgpu_generate_particles(n, DISTS[dist], seed, _p(out))
     return out
 
 

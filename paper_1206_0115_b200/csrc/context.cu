@@ -711,9 +711,11 @@ void fmmgpu_generate_particles(uint64_t n, int dist, uint64_t seed, double* xyzw
       normal_pair(gz, spare);
       norm = std::sqrt(gx * gx + gy * gy + gz * gz);
     } while (norm < 1e-12);
-    xyzw[4 * i] = 0.5 + 0.5 * gx / norm;
-    xyzw[4 * i + 1] = 0.5 + 0.5 * gy / norm;
-    xyzw[4 * i + 2] = 0.5 + 0.5 * gz / norm;
+    // dist 2: config D's ellipsoid surface, semi-axes (0.5, 0.35, 0.2)
+    const double ax = 0.5, ay = dist == 2 ? 0.35 : 0.5, az = dist == 2 ? 0.2 : 0.5;
+    xyzw[4 * i] = 0.5 + ax * gx / norm;
+    xyzw[4 * i + 1] = 0.5 + ay * gy / norm;
+    xyzw[4 * i + 2] = 0.5 + az * gz / norm;
     xyzw[4 * i + 3] = 1.0;
   }
 }

@@ -188,19 +188,38 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
   }
   if (threadIdx.x == 0) cfirst[nc] = static_cast<uint32_t>(p1);
   for (int i = threadIdx.x; i < L * (L - 1); i += L2P_THREADS) tn[i] = a.tn[i];
-  for (uint32_t i = threadIdx.x; i < nc * L3; i += L2P_THREADS) {
-    const uint32_t lc = i / L3, k = i % L3;
-    const size_t g = size_t(c0 + lc) * a.ldE + k;
-    tot[i] = a.expansion[g] + a.down[g];
+  // staged 4 elements at a time so the loads of a thread are in flight together
+  for (uint32_t i0 = threadIdx.x; i0 < nc * L3; i0 += 4 * L2P_THREADS) {
+    double e[4], d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * L2P_THREADS;
+      if (i < nc * L3) {
+        const size_t g = size_t(c0 + i / L3) * a.ldE + i % L3;
+        e[u] = a.expansion[g];
+        d[u] = a.down[g];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * L2P_THREADS;
+      if (i < nc * L3) tot[i] = e[u] + d[u];
+    }
   }
   __syncthreads();
   const double inv = a.geo.inv;
+  double4 pnext = pf, fnext = ff;
   for (uint64_t s = s_first; s < p1; s += L2P_THREADS) {
     uint32_t lc = 0;  // local cell of slot s (cells are contiguous in Morton order)
     while (lc + 1 < nc && cfirst[lc + 1] <= s) ++lc;
     const uint32_t c = c0 + lc;
     const double* ctr = cctr[lc];
-    const double4 p = s == s_first ? pf : a.pw[s];
+    const double4 p = pnext;
+    const double4 fprev = fnext;
+    if (s + L2P_THREADS < p1) {  // next particle's loads overlap this one's arithmetic
+      pnext = a.pw[s + L2P_THREADS];
+      fnext = far4[s + L2P_THREADS];
+    }
     const double rx = (p.x - ctr[0]) * inv, ry = (p.y - ctr[1]) * inv, rz = (p.z - ctr[2]) * inv;
     double sx[L], sy[L], sz[L], gx[L], gy[L], gz[L];
     eval_all<L>(tn, rx, sx);
@@ -230,7 +249,7 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
         dz = fma(ss, w, dz);
       }
     }
-    double4 r = s == s_first ? ff : far4[s];
+    double4 r = fprev;
     r.x += pot;
     r.y -= inv * dx;
     r.z -= inv * dy;

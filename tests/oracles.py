@@ -69,7 +69,7 @@ class Oracle:
     @classmethod
     def generate_particles(cls, n, dist="uniform", seed=42):
         out = np.zeros((n, 4))
-        cls.lib().orc_generate_particles(c_uint64(n), 0 if dist == "uniform" else 1, c_uint64(seed), _p(out))
+        cls.lib().orc_generate_particles(c_uint64(n), {"uniform": 0, "sphere": 1, "ellipsoid": 2}[dist], c_uint64(seed), _p(out))
         return out
 
 

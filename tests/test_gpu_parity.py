@@ -29,6 +29,8 @@ CASES = [
     (30000, 3, 3, "uniform", 5, True),
     # surface cloud: ragged leaves from 1 to ~300 particles (source splits S = 1..32)
     (20000, 4, 4, "sphere", 9, True),
+    # config D's ellipsoid surface (sparse levels: dense code maps, empty parents)
+    (40000, 6, 5, "ellipsoid", 4, False),
 ]
 
 

@@ -13,3 +13,9 @@ case "$what" in
   bench) timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err ;;
 esac
 done
+# configs: every BASELINE.json config through bench.py (short runs)
+if [ "${ALLCONFIGS:-0}" = "1" ]; then
+  for cfgname in A B C D E; do
+    timeout 900 python bench.py --config $cfgname --steps 5 --warmup 3 > gpurun_out/bench_$cfgname.json 2> gpurun_out/bench_$cfgname.err
+  done
+fi

@@ -65,6 +65,15 @@ def hbm_peak():
     return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
+def config_dict(name, world=1):
+    """The workload description shared by both arms' JSON lines."""
+    n, dist, h, order, desc = CONFIGS[name]
+    return {"workload": desc, "n": n, "height": h, "order": order, "eps": 10.0 ** -order, "group_size": 250,
+            "parallelism": f"morton-range partition x{world}, NCCL multipole all-gather per upward level"
+                           if world > 1 else "single",
+            "l2": "inputs (32 B/particle + 1 KB per leaf expansion array) exceed the 126 MB L2"}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -188,9 +197,9 @@ def run_reference(args, world, rank):
     n = CONFIGS[args.config][0]
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": CPU_SAMPLE[args.config][0] / v / 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator, seed 42)", "impl": "reference",
-            "config": {"workload": CONFIGS[args.config][4], "n": n, "sample_n": CPU_SAMPLE[args.config][0]},
+            "config": dict(config_dict(args.config), sample_n=CPU_SAMPLE[args.config][0]),
             "cpu_baseline": dict(info, value=v, unit=UNIT),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -308,11 +317,7 @@ def run_ours(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": ms_step, "eval_seconds": ms_step / 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (reference generator bench.cpp:29-39, seed 42, unit weights)",
-            "config": {"workload": desc, "n": n, "height": h, "order": order, "eps": 10.0 ** -order,
-                       "group_size": 250,
-                       "parallelism": f"morton-range partition x{world}, NCCL multipole all-gather per upward "
-                                      f"level" if world > 1 else "single",
-                       "l2": "inputs (320 MB particles, 262 MB leaf expansions) exceed the 126 MB L2"},
+            "config": config_dict(args.config, world),
             "gpu_launches": launches, "e2e": e2e, "roofline": roof, "per_operator": per_op,
             "tree_ms": kinds["TREE"], "clocks": clk,
             "note": "P2P runs on its own stream concurrently with the far-field chain; per-operator times "

@@ -32,6 +32,7 @@ struct P2PArgs {
   LevelView leaf;
   const uint64_t* parent_code;  // level leaf-1
   uint32_t p0;                  // first parent of the launch (partitioned runs: owned range)
+  uint32_t usplit;              // CTAs per parent: CTA y takes the units u = y (mod usplit)
   const uint32_t* first;        // leaf first_particle
   const uint32_t* count;        // leaf particle_count
   const double4* pw;
@@ -79,7 +80,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   int pc[3];
-  demorton(a.parent_code[a.p0 + blockIdx.x], pc);
+  demorton(a.parent_code[a.p0 + blockIdx.x / a.usplit], pc);
+  const uint32_t ysplit = blockIdx.x % a.usplit;
   if (tid < 64) {
     const int qa = tid >> 4, qb = (tid >> 2) & 3, qc = tid & 3;
     const uint32_t cell = find_ijk(a.leaf, 2 * pc[0] - 1 + qa, 2 * pc[1] - 1 + qb, 2 * pc[2] - 1 + qc);
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
     for (;;) {
       uint32_t u = 0;
       if (lane == 0) u = atomicAdd(&sm.next_unit, 1u);
-      u = __shfl_sync(0xffffffffu, u, 0);
+      u = __shfl_sync(0xffffffffu, u, 0) * a.usplit + ysplit;
       if (u >= nunits) break;
       // decode unit -> (child octant w, first target t0)
       int w = 0;
@@ -243,11 +245,15 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const Level& P = c->lv[leaf - 1];
   const uint32_t np = P.own1 - P.own0;
   if (np == 0) return;
-  P2PArgs a{L.view(leaf), P.code, P.own0, L.first_particle, L.particle_count, c->d_pw,
+  // few parents (shallow trees, big leaves): several CTAs per parent share its units
+  // (each re-stages the neighbourhood) so the grid still covers 2 CTAs per SM
+  uint32_t usplit = 1;
+  while (np * usplit < 2u * 148u && usplit < 16u) usplit *= 2;
+  P2PArgs a{L.view(leaf), P.code, P.own0, usplit, L.first_particle, L.particle_count, c->d_pw,
              reinterpret_cast<double4*>(c->d_near), c->n};
   auto run = [&](auto kern, int warps, int smem) {
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<np, warps * 32, smem, s>>>(a);
+    kern<<<np * usplit, warps * 32, smem, s>>>(a);
   };
   // FMMGPU_P2P_VARIANT (tuning experiments): 0 = 12 warps x 1 group, 1 = 8 x 2, 2 = 16 x 1, 3 = 8 x 1
   static const int variant = [] {

@@ -141,7 +141,8 @@ struct M2LTables {
   // stacked operators
   int R = 0;        // rows of the source-side stack = columns of the target-side stack
   int ldY = 0;      // round_up(R, 32): stride of one target's compressed vector
-  int rowsA = 0;    // round_up(R, 64): padded M of phase A
+  int rowsA = 0;    // round_up(R, bmA): padded M of phase A
+  int bmA = 64;     // phase A M-tile rows (64 for l <= 5, 128 above)
   int rowsB = 0;    // round_up(l^3, 64)... padded M of phase B
   double* dM1 = nullptr;    // [8][rowsA][ldE]
   double* dM2 = nullptr;    // [8][rowsB][ldY]

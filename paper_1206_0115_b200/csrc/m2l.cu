@@ -360,10 +360,13 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
 // M1_p (R rows) streams past them in BM x BK slices through a cp.async ring that
 // runs across M-tile boundaries, so the scatter epilogue of one M-tile overlaps the
 // loads of the next and no CTA pays a pipeline ramp per 64 x 64 tile.
-constexpr int PA_BM = 64, PA_BK = 16, PA_ST = 4, PA_THREADS = 256;  // 2 CTAs/SM: W 68 KB + ring 40 KB
+// Tiles: l <= 5: 64-row M-tiles, 4-stage ring, 64 resident columns (W 68 KB + ring 40 KB);
+// larger orders: 128-row M-tiles, 3 stages, 16 columns (l = 7: W 46 KB + ring 61 KB), so
+// two CTAs still fit on an SM. The epilogue tables are built for the M-tile in use.
+constexpr int PA_BK = 16, PA_THREADS = 256;
 constexpr int PA_SPAD = PA_BK + 4;  // == 4 (mod 16)
 
-template <int BN, int WM, int WN>
+template <int PA_BM, int PA_ST, int BN, int WM, int WN>
 __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g) {
   static_assert(WM * WN * 32 == PA_THREADS, "8 warps");
   constexpr int WTM = PA_BM / WM, WTN = BN / WN;
@@ -578,7 +581,8 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   }
   T.R = R;
   T.ldY = round_up(R, 32);
-  T.rowsA = round_up(R, PA_BM);
+  T.bmA = c->ldE <= 128 ? 64 : 128;
+  T.rowsA = round_up(R, T.bmA);
   T.rowsB = round_up(n3, B_BM);
   std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
   std::vector<int4> rowA(size_t(8) * T.rowsA, make_int4(-1, 0, 0, 0));
@@ -618,6 +622,7 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   FMM_CUDA(cudaMalloc(&T.dM2, M2.size() * sizeof(double)));
   // per 64-row M-tile of phase A: the distinct vectors it holds (rows of one vector
   // are consecutive), so the epilogue resolves one target per (vector, column)
+  const int PA_BM = T.bmA;
   const int mtiles = T.rowsA / PA_BM;
   T.vtMax = 1;
   std::vector<std::vector<int>> tv(size_t(8) * mtiles);
@@ -684,7 +689,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.a_class_stride = size_t(T.rowsA) * c->ldE;
     g.K = c->ldE;
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
-    auto launch = [&](auto kern, int bn) {
+    auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST) {
       const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * PA_SPAD) +
                           sizeof(uint32_t) * 2 * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -698,9 +703,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       kern<<<grid, PA_THREADS, smem, s>>>(g);
       FMM_CUDA(cudaGetLastError());
     };
-    if (c->ldE <= 128) launch(k_m2l_phase_a<64, 2, 4>, 64);
-    else if (c->ldE <= 352) launch(k_m2l_phase_a<32, 4, 2>, 32);
-    else launch(k_m2l_phase_a<16, 8, 1>, 16);
+    if (T.bmA == 64) launch(k_m2l_phase_a<64, 4, 64, 2, 4>, 64, 64, 4);
+    else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
   }
   g.cls_cells = L.tgtB ? L.tgtB : L.cls_cells;
   std::copy(L.tgtB ? L.tgtB_off : L.cls_off, (L.tgtB ? L.tgtB_off : L.cls_off) + 9, g.cls_off);

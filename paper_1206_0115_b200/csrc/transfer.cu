@@ -159,93 +159,6 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
   }
 }
 
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
-// P2M on the FP64 tensor path (l <= 8), warp per leaf cell: the multipole is the
-// product W (l^2 x l) = AB (l^2 x n) . C (n x l) with AB[n1 l + n2][j] = (w_j Sx_j[n1])
-// Sy_j[n2] and C[j][n3] = Sz_j[n3] (chebyshev.cpp:128-134). Per 4 particles a lane
-// loads one C and 2 * ceil(l^2/8) AB operands for ceil(l^2/8) DMMA m8n8k4 -- about a
-// third of the shared-memory traffic of the FMA formulation, which was LDS-bound.
-template <int L>
-__global__ void __launch_bounds__(P2M_THREADS) k_p2m_dmma(LeafArgs a) {
-  constexpr int MT = (L * L + 7) / 8;
-  constexpr int RW = 3 * L + 1;
-  __shared__ double tn[L * (L - 1) + 1];
-  __shared__ double S[P2M_WARPS][32][RW];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gq = lane >> 2, tq = lane & 3;
-  for (int i = threadIdx.x; i < L * (L - 1); i += P2M_THREADS) tn[i] = a.tn[i];
-  __syncthreads();
-  const uint32_t c = a.cell0 + blockIdx.x * P2M_WARPS + warp;
-  if (c >= a.ncells) return;
-  double ctr[3];
-  cell_center(a.geo, a.code[c], ctr);
-  const uint32_t first = a.first[c], cnt = a.count[c];
-  double* out = a.expansion + size_t(c) * a.ldE;
-  const double4 zero4 = make_double4(0, 0, 0, 0);
-  const double4 q0 = lane < cnt ? a.pw[first + lane] : zero4;
-  // fragment row of this lane in each m-tile: (n1, n2) or padding
-  int rn1[MT], rn2[MT];
-#pragma unroll
-  for (int m = 0; m < MT; ++m) {
-    const int r = m * 8 + gq;
-    rn1[m] = r < L * L ? r / L : -1;
-    rn2[m] = r < L * L ? r % L : 0;
-  }
-  double acc[MT][2];
-#pragma unroll
-  for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
-  double(*sw)[RW] = S[warp];
-  for (uint32_t base = 0; base < cnt; base += 32) {
-    const uint32_t nb = min(32u, cnt - base);
-    {
-      double* row = sw[lane];
-      if (lane < nb) {
-        const double4 p = base == 0 ? q0 : a.pw[first + base + lane];
-        double s[L];
-        eval_all<L>(tn, (p.x - ctr[0]) * a.geo.inv, s);
-#pragma unroll
-        for (int m = 0; m < L; ++m) row[m] = p.w * s[m];
-        eval_all<L>(tn, (p.y - ctr[1]) * a.geo.inv, s);
-#pragma unroll
-        for (int m = 0; m < L; ++m) row[L + m] = s[m];
-        eval_all<L>(tn, (p.z - ctr[2]) * a.geo.inv, s);
-#pragma unroll
-        for (int m = 0; m < L; ++m) row[2 * L + m] = s[m];
-      } else {  // zero particles pad the last k-step
-#pragma unroll
-        for (int m = 0; m < 3 * L; ++m) row[m] = 0.0;
-      }
-    }
-    __syncwarp();
-    for (uint32_t j0 = 0; j0 < nb; j0 += 4) {
-      const double* pj = sw[j0 + tq];
-      const double bfr = gq < L ? pj[2 * L + gq] : 0.0;
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        const double afr = rn1[m] >= 0 ? pj[rn1[m]] * pj[L + rn2[m]] : 0.0;
-        dmma884(acc[m][0], acc[m][1], afr, bfr);
-      }
-    }
-    __syncwarp();
-  }
-  // lane holds W[m*8 + gq][2 tq + e]
-#pragma unroll
-  for (int m = 0; m < MT; ++m) {
-    const int r = m * 8 + gq;
-    if (r >= L * L) continue;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int n3 = 2 * tq + e;
-      if (n3 < L) out[r * L + n3] += acc[m][e];
-    }
-  }
-}
-
 // L2P, CTA per run of L2P_CELLS consecutive leaf cells: total = own + down is formed
 // once per cell in shared memory (bench.cpp:320-325), then thread per particle of
 // those cells (contiguous in Morton order) reads it as (near-)broadcast LDS.
@@ -555,8 +468,7 @@ struct RunP2M {
   static void run(const LeafArgs& a, cudaStream_t s) {
     const uint32_t nc = a.ncells - a.cell0;
     if (!nc) return;
-    if constexpr (L <= 8) k_p2m_dmma<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
-    else k_p2m_warp<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
+    k_p2m_warp<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
   }
 };
 template <int L>

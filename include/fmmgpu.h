@@ -153,6 +153,13 @@ int fmmgpu_time_evaluations(fmmgpu_ctx* ctx, int steps, double* total_ms, double
  * (or fmmgpu_evaluate) before reading fields. */
 int fmmgpu_time_operator(fmmgpu_ctx* ctx, int kind, int level, int reps, double* ms);
 
+/* ---- accuracy check: direct_oracle (direct.cpp:202-226) on the device ------------
+ * Exact sums over all n input particles (self excluded) for the k sampled input indices
+ * `targets` (host array), as run_fmm's check (bench.cpp:366-398) uses them; outputs
+ * are host arrays of k doubles (any may be NULL). Deterministic. */
+int fmmgpu_direct(fmmgpu_ctx* ctx, const uint32_t* targets, uint64_t k, double* potential,
+                  double* fx, double* fy, double* fz);
+
 /* ---- multi-GPU: contiguous Morton ranges of leaves -------------
  * No reference counterpart (the reference is single-process); added by
  * the north star. Every rank builds the whole tree from the whole particle set, then

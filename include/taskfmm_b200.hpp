@@ -11,7 +11,7 @@
 //   generate_particles                 bench.cpp:29-61 (same mt19937_64 stream)
 //   relative_l2_error                  bench.cpp:91-100
 //   FmmContext (ctor, reset, run_task, gather, setup_seconds)   bench.hpp:86-121
-//   run_fmm (no oracle check, no writers)                       bench.cpp:415-469
+//   run_fmm (oracle check on the device, no writers)            bench.cpp:415-469
 //
 // Granularity: the device runs one launch per (operator, level). run_task(task)
 // executes the level launch of (task.kind, task.level) on the first task of that pair
@@ -23,7 +23,9 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
+#include <limits>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -63,6 +65,7 @@ struct RunConfig {
   int acc = 5;  // interpolation order l = acc, svd eps = 10^-acc
   int group_size = 250;
   std::uint64_t seed = 42;
+  std::uint64_t check = 1000;  // oracle sample size, 0 disables (exact sums on the device)
   int device = 0;
 };
 
@@ -95,7 +98,8 @@ inline double relative_l2_error(std::span<const double> estimate, std::span<cons
     num += d * d;
     den += reference[i] * reference[i];
   }
-  return den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+  if (den == 0) return num == 0 ? 0.0 : std::numeric_limits<double>::infinity();  // bench.cpp:97-98
+  return std::sqrt(num / den);
 }
 
 class FmmContext {
@@ -189,11 +193,23 @@ struct RunResult {
   double setup_seconds = 0;
   double exec_seconds = 0;
   double wall_seconds = 0;
+  double eps_l2_potential = -1;  // -1 when not checked
+  double eps_l2_force = -1;
   FmmContext::Fields fields;
   std::vector<Particle> input;
 };
 
-//! run_fmm (bench.cpp:415-469) without the oracle check, ledger or writers.
+//! bench.cpp:368-376
+inline std::vector<std::uint32_t> check_targets(std::uint64_t n, std::uint64_t check) {
+  std::vector<std::uint32_t> t;
+  for (std::uint64_t k = 0; k < check; ++k) t.push_back(static_cast<std::uint32_t>(k * n / check));
+  std::sort(t.begin(), t.end());
+  t.erase(std::unique(t.begin(), t.end()), t.end());
+  return t;
+}
+
+//! run_fmm (bench.cpp:415-469) without the ledger or writers; the oracle check
+//! (bench.cpp:378-398) runs on the device (fmmgpu_direct).
 inline RunResult run_fmm(const RunConfig& cfg) {
   const auto w0 = std::chrono::steady_clock::now();
   RunResult r;
@@ -205,6 +221,20 @@ inline RunResult run_fmm(const RunConfig& cfg) {
   ctx.evaluate();
   r.fields = ctx.gather();
   r.exec_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - e0).count();
+  if (cfg.check > 0 && !r.input.empty()) {
+    const auto t = check_targets(r.input.size(), std::min<std::uint64_t>(cfg.check, r.input.size()));
+    std::vector<double> pot(t.size()), fx(t.size()), fy(t.size()), fz(t.size());
+    check(fmmgpu_direct(ctx.handle(), t.data(), t.size(), pot.data(), fx.data(), fy.data(), fz.data()),
+          fmmgpu_last_error(ctx.handle()));
+    std::vector<double> ep(t.size()), ef, rf;
+    for (std::size_t i = 0; i < t.size(); ++i) {
+      ep[i] = r.fields.potential[t[i]];
+      ef.insert(ef.end(), {r.fields.fx[t[i]], r.fields.fy[t[i]], r.fields.fz[t[i]]});
+      rf.insert(rf.end(), {fx[i], fy[i], fz[i]});
+    }
+    r.eps_l2_potential = relative_l2_error(ep, pot);
+    r.eps_l2_force = relative_l2_error(ef, rf);
+  }
   r.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
   return r;
 }

@@ -89,6 +89,7 @@ def lib():
             getattr(L, name).argtypes = [c_void_p, c_int]
         L.fmmgpu_downward.argtypes = [c_void_p]
         L.fmmgpu_partition.argtypes = [c_void_p, c_int, c_int]
+        L.fmmgpu_direct.argtypes = [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]
         L.fmmgpu_partition_ranges.argtypes = [c_void_p, c_int, c_void_p]
         L.fmmgpu_plan_partition.argtypes = [c_void_p, ctypes.c_uint32, c_int, c_void_p]
         L.fmmgpu_comm_init.argtypes = [c_void_p, ctypes.c_char_p, c_int, c_int]
@@ -358,6 +359,14 @@ class FmmContext:
         keys = list(KINDS[:6]) + ["GATHER", "EVAL", "TREE", "LISTS"]
         return total.value, dict(zip(keys, ms.tolist())), nl.value
 
+    # -- accuracy check (direct.cpp:202-226 on the device)
+    def direct(self, targets):
+        """Exact potential / force at the given input indices (sum over all particles)."""
+        t = np.ascontiguousarray(targets, dtype=np.uint32)
+        out = [np.zeros(len(t)) for _ in range(4)]
+        self._check(self._lib.fmmgpu_direct(self.h, _p(t), len(t), *[_p(a) for a in out]))
+        return out
+
     # -- multi-GPU partition (SURVEY.md §8e)
     def partition(self, rank: int, nranks: int):
         """Own a contiguous Morton range of leaves (rank of nranks); nranks=1 undoes it."""
@@ -400,8 +409,32 @@ class FmmContext:
         return out
 
 
-def run_fmm(cfg: RunConfig, particles=None):
-    """run_fmm (bench.cpp:415-469) minus the oracle check: returns fields in input order."""
+def check_targets(n: int, check: int) -> np.ndarray:
+    """bench.cpp:368-376: k * n / check for k < check, sorted, unique."""
+    k = np.arange(check, dtype=np.uint64)
+    return np.unique((k * np.uint64(n) // np.uint64(check)).astype(np.uint32))
+
+
+def relative_l2_error(estimate, reference) -> float:
+    """bench.cpp:91-100: sqrt(sum (est-ref)^2 / sum ref^2); 0 or inf when the reference is 0."""
+    e, r = np.asarray(estimate, dtype=np.float64), np.asarray(reference, dtype=np.float64)
+    num, den = float(np.sum((e - r) ** 2)), float(np.sum(r * r))
+    if den == 0:
+        return 0.0 if num == 0 else float("inf")
+    return float(np.sqrt(num / den))
+
+
+def run_fmm(cfg: RunConfig, particles=None, check: int = 0):
+    """run_fmm (bench.cpp:415-469): fields in input order; with check > 0 also the
+    accuracy against the exact sum at `check` sampled targets (bench.cpp:378-398),
+    computed on the device. Returns (fields, eps_potential, eps_force)."""
     xyzw = generate_particles(cfg.n, cfg.dist, cfg.seed) if particles is None else particles
     with FmmContext(None, cfg) as ctx:
-        return ctx.run(xyzw, cfg.height, cfg.group_size)
+        fields = ctx.run(xyzw, cfg.height, cfg.group_size)
+        if check <= 0:
+            return fields, -1.0, -1.0
+        t = check_targets(len(xyzw), min(check, len(xyzw)))
+        ref = ctx.direct(t)
+    est_f = np.stack([fields[1][t], fields[2][t], fields[3][t]], axis=1).ravel()
+    ref_f = np.stack(ref[1:], axis=1).ravel()
+    return fields, relative_l2_error(fields[0][t], ref[0]), relative_l2_error(est_f, ref_f)

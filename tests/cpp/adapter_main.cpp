@@ -69,12 +69,17 @@ int main(int argc, char** argv) {
   std::vector<Particle> dup = {{{0.1, 0.1, 0.1}, 1.0}, {{0.1, 0.1, 0.1}, 1.0}, {{0.9, 0.9, 0.9}, 1.0}};
   bad += expect_throw("coincident", [&] { FmmContext c(dup, cfg); }, std::domain_error(""));
   bad += expect_throw("level", [&] { ctx.run_task(Task{0, TaskKind::M2L, 99, 0, 0}); }, std::out_of_range(""));
-  const auto r = run_fmm(cfg);
+  const auto r = run_fmm(cfg);  // includes the device-side oracle check (cfg.check = 1000)
+  if (!(r.eps_l2_potential > 0 && r.eps_l2_potential < 1e-4 && r.eps_l2_force > 0 && r.eps_l2_force < 1e-2)) {
+    std::fprintf(stderr, "run_fmm accuracy out of range: %g %g\n", r.eps_l2_potential, r.eps_l2_force);
+    ++bad;
+  }
   if (relative_l2_error(r.fields.potential, b.potential) != 0.0) {
     std::fprintf(stderr, "run_fmm differs from evaluate\n");
     ++bad;
   }
-  std::printf("adapter: n=%llu setup %.3f s exec %.3f s, %d failures\n",
-              static_cast<unsigned long long>(cfg.n), r.setup_seconds, r.exec_seconds, bad);
+  std::printf("adapter: n=%llu setup %.3f s exec %.3f s eps_l2 %.3e / %.3e, %d failures\n",
+              static_cast<unsigned long long>(cfg.n), r.setup_seconds, r.exec_seconds, r.eps_l2_potential,
+              r.eps_l2_force, bad);
   return bad;
 }

@@ -325,3 +325,33 @@ def test_accuracy_against_direct_sum(fmm):
     ep = relative_l2_error(g[0][targets], out[0])
     ef = force_error(g[1][targets], g[2][targets], g[3][targets], *out[1:])
     assert ep < 1e-5 and ef < 1e-3, (ep, ef)
+
+
+def test_direct_checker_matches_oracle(fmm):
+    """fmmgpu_direct (direct_oracle on the device, direct.cpp:202-226) vs the CPU loop."""
+    import ctypes
+    xyzw = make_particles(20000, "uniform", 5, True)
+    c = ctx_for(fmm, xyzw, 5, 4)
+    targets = fmm.check_targets(len(xyzw), 300)
+    got = c.direct(targets)
+    ref = [np.zeros(len(targets)) for _ in range(4)]
+    Oracle.lib().orc_direct(xyzw.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint64(len(xyzw)),
+                            targets.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint64(len(targets)),
+                            *[a.ctypes.data_as(ctypes.c_void_p) for a in ref])
+    for a, b in zip(got, ref):
+        assert relative_l2_error(a, b) <= 1e-14
+    with pytest.raises(fmm.OutOfRange):
+        c.direct([len(xyzw)])
+
+
+def test_run_fmm_check_reproduces_recorded_accuracy(fmm):
+    """proj/test_output.txt:7 through the GPU path and the GPU checker: eps_L2 of the
+    potential at N=1e4 uniform seed 42, h=4, 1000 sampled targets = 1.242e-04 / 1.051e-06
+    / 1.150e-08 for orders 3 / 5 / 7 (4 significant digits)."""
+    got = []
+    for acc in (3, 5, 7):
+        cfg = fmm.RunConfig(n=10000, height=4, acc=acc, seed=42)
+        _, ep, ef = fmm.run_fmm(cfg, check=1000)
+        assert 0 < ef < 1e-2
+        got.append("%.3e" % ep)
+    assert got == ["1.242e-04", "1.051e-06", "1.150e-08"]

@@ -197,6 +197,13 @@ struct fmmgpu_ctx {
   uint64_t own_s0 = 0, own_s1 = 0;
   void* nccl = nullptr;          // ncclComm_t when fmmgpu_comm_init attached one
   std::vector<std::vector<uint32_t>> part_begin;  // per level: first owned cell of every rank (+ end)
+  // captured evaluation (fmmgpu_evaluate): replayed while tree / partition / operators hold
+  cudaGraphExec_t graph_exec = nullptr;
+  bool graph_warm = false;   // one eager evaluation done since the last invalidation
+  bool capturing = false;
+  uint64_t graph_launches = 0;
+  double* d_splitk = nullptr;  // M2L phase B split-K partials
+  size_t splitk_cap = 0;
   bool out_valid = false;        // d_out holds near + far of the current arrays
   int* d_flag = nullptr;         // error flags
   // near plan
@@ -229,6 +236,9 @@ void launch_m2l(fmmgpu_ctx* c, int level, cudaStream_t s);
 void launch_p2p(fmmgpu_ctx* c, cudaStream_t s);
 void launch_gather(fmmgpu_ctx* c, cudaStream_t s);
 void partition_free(fmmgpu_ctx* c);
+}  // namespace fmmgpu
+extern "C" void fmmgpu_invalidate_graph(fmmgpu_ctx* c);
+namespace fmmgpu {
 void exchange_level(fmmgpu_ctx* c, int v, cudaStream_t s);
 void* scratch(fmmgpu_ctx* c, size_t bytes);
 uint64_t near_directional_count(fmmgpu_ctx* c);

@@ -176,6 +176,8 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
     cudaStreamSynchronize(c->s_far);
   }
   m2l_free(c);
+  fmmgpu_invalidate_graph(c);
+  if (c->d_splitk) cudaFree(c->d_splitk);
   if (c->nccl) fmmgpu_comm_destroy(c);
   if (c->d_interp) cudaFree(c->d_interp);
   if (c->d_flag) cudaFree(c->d_flag);
@@ -326,43 +328,102 @@ int fmmgpu_p2p(fmmgpu_ctx* c) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Timing events must stay visible outside a captured graph (cudaEventRecordExternal).
+void record(fmmgpu_ctx* c, cudaEvent_t e, cudaStream_t s) {
+  if (c->capturing) FMM_CUDA(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+  else FMM_CUDA(cudaEventRecord(e, s));
+}
+
+// One evaluation: reset, then the DAG as a level-synchronous two-stream schedule.
+void enqueue_evaluation(fmmgpu_ctx* c) {
+  const int leaf = c->height - 1;
+  cudaStream_t s = c->s_far;
+  c->launches = 0;
+  cudaEvent_t* e = c->ev_t;
+  record(c, e[0], s);
+  reset_arrays(c, s);
+  FMM_CUDA(cudaEventRecord(c->ev_fork, s));
+  FMM_CUDA(cudaStreamWaitEvent(c->s_near, c->ev_fork, 0));
+  record(c, e[6], c->s_near);
+  launch_p2p(c, c->s_near);
+  record(c, e[7], c->s_near);
+  record(c, e[1], s);
+  launch_p2m(c, s);
+  exchange_level(c, leaf, s);  // partitioned runs: all-gather this level's multipoles
+  record(c, e[2], s);
+  for (int v = leaf - 1; v >= 2; --v) {
+    launch_m2m(c, v, s);
+    exchange_level(c, v, s);
+  }
+  record(c, e[3], s);
+  for (int v = 2; v <= leaf; ++v) launch_m2l(c, v, s);
+  record(c, e[4], s);
+  for (int v = 2; v < leaf; ++v) launch_l2l(c, v, s);
+  record(c, e[5], s);
+  launch_l2p(c, s);
+  record(c, e[8], s);
+  FMM_CUDA(cudaEventRecord(c->ev_join, c->s_near));
+  FMM_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
+  record(c, e[9], s);
+  launch_gather(c, s);
+  record(c, e[10], s);
+}
+
+}  // namespace
+
+extern "C" {
+
+// The evaluation's ~25 launches are captured once into a CUDA graph (after one eager
+// run, so every lazy allocation has happened) and replayed while the tree, partition
+// and operators are unchanged (the stream/event schedule as a
+// graph). FMMGPU_NO_GRAPH=1 keeps eager launches. Partitioned runs with an NCCL
+// communicator stay eager.
 int fmmgpu_evaluate(fmmgpu_ctx* c) {
   return guarded(c, [&] {
     need_tree(c);
     FMM_CUDA(cudaSetDevice(c->device));
-    const int leaf = c->height - 1;
-    cudaStream_t s = c->s_far;
-    c->launches = 0;
-    cudaEvent_t* e = c->ev_t;
-    FMM_CUDA(cudaEventRecord(e[0], s));
-    reset_arrays(c, s);
-    FMM_CUDA(cudaEventRecord(c->ev_fork, s));
-    FMM_CUDA(cudaStreamWaitEvent(c->s_near, c->ev_fork, 0));
-    FMM_CUDA(cudaEventRecord(e[6], c->s_near));
-    launch_p2p(c, c->s_near);
-    FMM_CUDA(cudaEventRecord(e[7], c->s_near));
-    FMM_CUDA(cudaEventRecord(e[1], s));
-    launch_p2m(c, s);
-    exchange_level(c, leaf, s);  // partitioned runs: all-gather this level's multipoles
-    FMM_CUDA(cudaEventRecord(e[2], s));
-    for (int v = leaf - 1; v >= 2; --v) {
-      launch_m2m(c, v, s);
-      exchange_level(c, v, s);
+    static const bool no_graph = std::getenv("FMMGPU_NO_GRAPH") != nullptr;
+    const bool graphable = !no_graph && !(c->part_n > 1 && c->nccl);
+    if (graphable && c->graph_exec) {
+      FMM_CUDA(cudaGraphLaunch(c->graph_exec, c->s_far));
+      c->launches = c->graph_launches;
+      c->out_valid = true;
+      return;
     }
-    FMM_CUDA(cudaEventRecord(e[3], s));
-    for (int v = 2; v <= leaf; ++v) launch_m2l(c, v, s);
-    FMM_CUDA(cudaEventRecord(e[4], s));
-    for (int v = 2; v < leaf; ++v) launch_l2l(c, v, s);
-    FMM_CUDA(cudaEventRecord(e[5], s));
-    launch_l2p(c, s);
-    FMM_CUDA(cudaEventRecord(e[8], s));
-    FMM_CUDA(cudaEventRecord(c->ev_join, c->s_near));
-    FMM_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
-    FMM_CUDA(cudaEventRecord(e[9], s));
-    launch_gather(c, s);
-    FMM_CUDA(cudaEventRecord(e[10], s));
+    enqueue_evaluation(c);
     c->out_valid = true;
+    if (!graphable || !c->graph_warm) {  // first run eager: lazy allocations happen here
+      c->graph_warm = graphable;
+      return;
+    }
+    cudaGraph_t g = nullptr;
+    FMM_CUDA(cudaStreamBeginCapture(c->s_far, cudaStreamCaptureModeRelaxed));
+    c->capturing = true;
+    try {
+      enqueue_evaluation(c);
+    } catch (...) {
+      c->capturing = false;
+      cudaStreamEndCapture(c->s_far, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    c->capturing = false;
+    FMM_CUDA(cudaStreamEndCapture(c->s_far, &g));
+    FMM_CUDA(cudaGraphInstantiate(&c->graph_exec, g, 0));
+    FMM_CUDA(cudaGraphDestroy(g));
+    c->graph_launches = c->launches;
   });
+}
+
+void fmmgpu_invalidate_graph(fmmgpu_ctx* c) {
+  if (!c) return;
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  c->graph_exec = nullptr;
+  c->graph_warm = false;
 }
 
 // Stepped evaluation for a host-driven exchange (partitioned runs without an attached

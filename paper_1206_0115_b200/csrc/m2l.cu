@@ -613,6 +613,7 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
       }
     }
   m2l_free(c);
+  fmmgpu_invalidate_graph(c);
   for (auto& L : c->lv)  // the Yt layout depends on the ranks: drop stale intermediates
     if (L.yt) {
       FMM_CUDA(cudaFree(L.yt));
@@ -723,7 +724,17 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     int ks = 1;
     while (ks < 16 && ctas * ks < 2u * 148u && kt / (2 * ks) >= 8) ks *= 2;
     g.ksplit = ks;
-    g.part = ks > 1 ? static_cast<double*>(scratch(c, sizeof(double) * ks * size_t(L.n) * c->ldE)) : nullptr;
+    if (ks > 1) {  // own buffer (not the shared scratch): captured graphs keep this pointer
+      const size_t bytes = sizeof(double) * ks * size_t(L.n) * c->ldE;
+      if (bytes > c->splitk_cap) {
+        if (c->capturing) throw Error(FMMGPU_LOGIC_ERROR, "split-K buffer growth during graph capture");
+        if (c->d_splitk) FMM_CUDA(cudaFreeAsync(c->d_splitk, s));
+        FMM_CUDA(cudaMallocAsync(&c->d_splitk, bytes, s));
+        c->splitk_cap = bytes;
+        fmmgpu_invalidate_graph(c);
+      }
+    }
+    g.part = ks > 1 ? c->d_splitk : nullptr;
     const size_t smem = sizeof(double) * B_ST * (B_BM + B_BN) * (B_BK + 4);
     auto kern = k_m2l_phase_b<B_BM, B_BN, B_WM, B_WN, B_ST, B_BK>;
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
     sm.first[tid] = cell == NPOS ? 0u : a.first[cell];
     sm.cnt[tid] = cnt;
     // inclusive warp scan over the 64 padded counts (two warps), then fix up
-    uint32_t x = (cnt + 3u) & ~3u;
+    // runs start at qc = 0 or 1 and end at qc = 3 or the row end, so only those
+    // boundaries must sit on groups of 4: position qc = 1 needs no padding
+    uint32_t x = qc == 1 ? cnt : (cnt + 3u) & ~3u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);

@@ -153,6 +153,7 @@ int fmmgpu_partition(fmmgpu_ctx* c, int rank, int nranks) {
     FMM_CUDA(cudaStreamSynchronize(c->s_near));
     FMM_CUDA(cudaStreamSynchronize(c->s_far));
     partition_free(c);
+    fmmgpu_invalidate_graph(c);
     const int h = c->height, leaf = h - 1;
     c->part_rank = rank;
     c->part_n = nranks;

@@ -169,6 +169,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   if (n >= 0xffffffffull) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: particle count exceeds 32-bit ids");
   if (root4 && !(root4[3] > 0)) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: root cube width must be positive");
   cudaStream_t s = c->s_far;
+  fmmgpu_invalidate_graph(c);
   partition_free(c);
   tree_free(c);
   lists_free(c);

@@ -214,14 +214,26 @@ def test_full_evaluation_vs_reference_itself(fmm, tmp_path):
 
 
 def test_deterministic(fmm):
+    """Bitwise run-to-run reproducibility (the reference's single-writer property,
+    README.md:84-92) across the eager run, the capturing run and CUDA-graph replays, and
+    after the graph is invalidated by a new tree."""
     xyzw = make_particles(20000, "uniform", 1, True)
     c = ctx_for(fmm, xyzw, 5, 5)
-    c.evaluate()
-    a = c.gather()
-    c.evaluate()
-    b = c.gather()
-    for x, y in zip(a, b):
-        assert np.array_equal(x, y)
+    runs = []
+    for _ in range(4):  # eager, eager + capture, replay, replay
+        c.evaluate()
+        runs.append(c.gather())
+    for r in runs[1:]:
+        for x, y in zip(runs[0], r):
+            assert np.array_equal(x, y)
+    assert c.launch_count() > 0
+    total, kinds, launches = c.time_evaluations(3)
+    assert total > 0 and kinds["P2P"] > 0 and launches == 3 * c.launch_count()
+    c.build_tree(xyzw, 5)  # new tree: graph rebuilt
+    for _ in range(3):
+        c.evaluate()
+        for x, y in zip(runs[0], c.gather()):
+            assert np.array_equal(x, y)
 
 
 def test_run_entry_point(fmm):

@@ -90,8 +90,10 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
     sm.cnt[tid] = cnt;
     // inclusive warp scan over the 64 padded counts (two warps), then fix up
     // runs start at qc = 0 or 1 and end at qc = 3 or the row end, so only those
-    // boundaries must sit on groups of 4: position qc = 1 needs no padding
-    uint32_t x = qc == 1 ? cnt : (cnt + 3u) & ~3u;
+    // boundaries must sit on groups of 4: position qc = 1 is not padded and qc = 2
+    // pads the pair (qc = 1, qc = 2) to a whole number of groups
+    const uint32_t cnt_prev = __shfl_up_sync(0xffffffffu, cnt, 1);
+    uint32_t x = qc == 1 ? cnt : qc == 2 ? ((cnt_prev + cnt + 3u) & ~3u) - cnt_prev : (cnt + 3u) & ~3u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);

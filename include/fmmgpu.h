@@ -103,6 +103,17 @@ int fmmgpu_download_fields(fmmgpu_ctx* ctx, double* potential, double* fx, doubl
 int fmmgpu_run(fmmgpu_ctx* ctx, const double* xyzw, uint64_t n, int height, int group_size,
                double* potential, double* fx, double* fy, double* fz);
 
+/* Pipelined fmmgpu_run over a stream of particle sets (run_fmm called repeatedly,
+ * bench.cpp:415-469, with the copies off the critical path). Returns once step k's tree
+ * is built and its evaluation is enqueued: the H2D of step k+1 overlaps evaluation k,
+ * the D2H of step k overlaps step k+1. xyzw and the four outputs should be PINNED host
+ * memory; xyzw may be reused once the next fmmgpu_run_async returns, outputs are valid
+ * after fmmgpu_run_wait. Errors of the tree build are reported synchronously (same
+ * codes as fmmgpu_build_tree). */
+int fmmgpu_run_async(fmmgpu_ctx* ctx, const double* xyzw, uint64_t n, int height, int group_size,
+                     double* potential, double* fx, double* fy, double* fz);
+int fmmgpu_run_wait(fmmgpu_ctx* ctx);
+
 /* ---- tree / plan / expansion access (parity dumps) ---------------------------- */
 int fmmgpu_tree_info(const fmmgpu_ctx* ctx, uint64_t* n, int* height, int* group_size,
                      double* root4);

@@ -82,6 +82,8 @@ def lib():
         L.fmmgpu_last_launch_count.argtypes = [c_void_p]
         L.fmmgpu_generate_particles.argtypes = [c_uint64, c_int, c_uint64, c_void_p]
         L.fmmgpu_run.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]
+        L.fmmgpu_run_async.argtypes = L.fmmgpu_run.argtypes
+        L.fmmgpu_run_wait.argtypes = [c_void_p]
         for name in ("fmmgpu_reset", "fmmgpu_p2m", "fmmgpu_l2p", "fmmgpu_p2p", "fmmgpu_evaluate",
                      "fmmgpu_synchronize", "fmmgpu_build_lists"):
             getattr(L, name).argtypes = [c_void_p]
@@ -407,6 +409,17 @@ class FmmContext:
         self._check(self._lib.fmmgpu_run(self.h, _p(xyzw), n, height, group_size, *[_p(a) for a in out]))
         self.n, self.height, self.group_size = n, height, group_size
         return out
+
+    def run_async(self, xyzw_ptr: int, n: int, height: int, group_size: int, out_ptrs):
+        """Pipelined run (fmmgpu_run_async) on caller-owned, preferably pinned, host
+        buffers given as raw addresses: the {x,y,z,w} input and four n-double outputs.
+        Returns once the step's tree is built; outputs are valid after run_wait()."""
+        self._check(self._lib.fmmgpu_run_async(self.h, c_void_p(xyzw_ptr), n, height, group_size,
+                                               *[c_void_p(a) for a in out_ptrs]))
+        self.n, self.height, self.group_size = n, height, group_size
+
+    def run_wait(self):
+        self._check(self._lib.fmmgpu_run_wait(self.h))
 
 
 def check_targets(n: int, check: int) -> np.ndarray:

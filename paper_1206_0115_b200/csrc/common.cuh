@@ -216,6 +216,15 @@ struct fmmgpu_ctx {
   void* d_tmp = nullptr;
   size_t d_tmp_cap = 0;
   int* d_canon = nullptr;  // canonical class per vector slot (343)
+  // pipelined runs (fmmgpu_run_async): copy streams, double-buffered gathered fields
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in_free = nullptr, ev_in_ready = nullptr, ev_out_ready[2] = {}, ev_d2h_done[2] = {};
+  double* pipe_out[2] = {};
+  // small device -> host readbacks (counts, flags) through mapped pinned memory written
+  // by a kernel, so they never queue behind bulk transfers on the copy engines
+  void* h_rb = nullptr;
+  uint64_t pipe_cap = 0;
+  uint64_t pipe_k = 0;
 };
 
 namespace fmmgpu {
@@ -241,6 +250,10 @@ extern "C" void fmmgpu_invalidate_graph(fmmgpu_ctx* c);
 namespace fmmgpu {
 void exchange_level(fmmgpu_ctx* c, int v, cudaStream_t s);
 void* scratch(fmmgpu_ctx* c, size_t bytes);
+constexpr size_t READBACK_CAP = 64 * 1024;
+// copies `bytes` (multiple of 4, <= READBACK_CAP) of device memory to host through the
+// mapped buffer, synchronizing s; the returned host pointer is valid until the next call
+const void* readback(fmmgpu_ctx* c, const void* src, size_t bytes, cudaStream_t s);
 uint64_t near_directional_count(fmmgpu_ctx* c);
 int canonicalize_host(const int v[3], int perm[3], int sign[3]);
 inline int vec_slot(int i, int j, int k) { return (i + 3) * 49 + (j + 3) * 7 + (k + 3); }

@@ -14,8 +14,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
+#include <string>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -109,6 +113,51 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// InterpolationEngine + M2LOperatorSet of a new context (fmmgpu_create); `factors`
+// (optional) supplies the compressed M2L operators instead of a new device SVD.
+void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx* factors) {
+  if (order < 2 || order > MAX_ORDER) throw Error(FMMGPU_INVALID_ARGUMENT, "InterpolationEngine: order must be in [2, 10]");
+  if (!(eps > 0)) throw Error(FMMGPU_INVALID_ARGUMENT, "M2LOperatorSet: eps must be positive");
+  int ndev = 0;
+  FMM_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) throw Error(FMMGPU_INVALID_ARGUMENT, "no such CUDA device");
+  c->device = device;
+  c->order = order;
+  c->eps = eps;
+  c->l3 = order * order * order;
+  c->ldE = round_up(c->l3, 32);  // multiple of the GEMM k-slice (32)
+  FMM_CUDA(cudaSetDevice(device));
+  cudaMemPool_t pool;
+  FMM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  FMM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  // The far-field chain gets the higher priority: its coarse levels cannot fill the
+  // GPU, so P2P CTAs (lower priority, concurrent stream) fill the idle SMs instead of
+  // the chain queueing behind 32k P2P CTAs.
+  int prio_lo = 0, prio_hi = 0;
+  FMM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  FMM_CUDA(cudaStreamCreateWithPriority(&c->s_far, cudaStreamNonBlocking, prio_hi));
+  FMM_CUDA(cudaStreamCreateWithPriority(&c->s_near, cudaStreamNonBlocking, prio_lo));
+  FMM_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  for (auto& e : c->ev_t) FMM_CUDA(cudaEventCreate(&e));
+  FMM_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
+  interp_setup(c);
+  if (factors) {  // share the operators of an existing context (no second SVD)
+    auto& T = c->m2l;
+    const auto& F = factors->m2l;
+    for (int cl = 0; cl < 16; ++cl) {
+      T.rank[cl] = F.rank[cl];
+      T.u[cl] = F.u[cl];
+      T.v[cl] = F.v[cl];
+      T.sigma[cl] = F.sigma[cl];
+    }
+    m2l_setup(c, false);
+  } else {
+    m2l_setup(c, true);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -120,36 +169,7 @@ int fmmgpu_create(int device, int order, double eps, fmmgpu_ctx** out) {
   if (!out) return FMMGPU_INVALID_ARGUMENT;
   *out = nullptr;
   auto* c = new fmmgpu_ctx;
-  const int rc = guarded(c, [&] {
-    if (order < 2 || order > MAX_ORDER) throw Error(FMMGPU_INVALID_ARGUMENT, "InterpolationEngine: order must be in [2, 10]");
-    if (!(eps > 0)) throw Error(FMMGPU_INVALID_ARGUMENT, "M2LOperatorSet: eps must be positive");
-    int ndev = 0;
-    FMM_CUDA(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) throw Error(FMMGPU_INVALID_ARGUMENT, "no such CUDA device");
-    c->device = device;
-    c->order = order;
-    c->eps = eps;
-    c->l3 = order * order * order;
-    c->ldE = round_up(c->l3, 32);  // multiple of the GEMM k-slice (32)
-    FMM_CUDA(cudaSetDevice(device));
-    cudaMemPool_t pool;
-    FMM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    FMM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    // The far-field chain gets the higher priority: its coarse levels cannot fill the
-    // GPU, so P2P CTAs (lower priority, concurrent stream) fill the idle SMs instead of
-    // the chain queueing behind 32k P2P CTAs.
-    int prio_lo = 0, prio_hi = 0;
-    FMM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    FMM_CUDA(cudaStreamCreateWithPriority(&c->s_far, cudaStreamNonBlocking, prio_hi));
-    FMM_CUDA(cudaStreamCreateWithPriority(&c->s_near, cudaStreamNonBlocking, prio_lo));
-    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-    for (auto& e : c->ev_t) FMM_CUDA(cudaEventCreate(&e));
-    FMM_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
-    interp_setup(c);
-    m2l_setup(c, true);
-  });
+  const int rc = guarded(c, [&] { ctx_init(c, device, order, eps, nullptr); });
   if (rc != FMMGPU_OK) {
     g_global_err = c->err;
     fmmgpu_destroy(c);
@@ -162,6 +182,20 @@ int fmmgpu_create(int device, int order, double eps, fmmgpu_ctx** out) {
 void fmmgpu_destroy(fmmgpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  if (c->s_h2d) {  // pipelined runs
+    cudaStreamSynchronize(c->s_h2d);
+    cudaStreamSynchronize(c->s_d2h);
+    for (auto p : c->pipe_out)
+      if (p) cudaFree(p);
+    cudaEventDestroy(c->ev_in_free);
+    cudaEventDestroy(c->ev_in_ready);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(c->ev_out_ready[i]);
+      cudaEventDestroy(c->ev_d2h_done[i]);
+    }
+    cudaStreamDestroy(c->s_h2d);
+    cudaStreamDestroy(c->s_d2h);
+  }
   if (c->s_far) {
     cudaStreamSynchronize(c->s_far);
     cudaStreamSynchronize(c->s_near);
@@ -182,6 +216,7 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
   if (c->d_interp) cudaFree(c->d_interp);
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_canon) cudaFree(c->d_canon);
+  if (c->h_rb) cudaFreeHost(c->h_rb);
   for (auto& e : c->ev_t)
     if (e) cudaEventDestroy(e);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -580,6 +615,126 @@ int fmmgpu_run(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, int gr
   rc = fmmgpu_evaluate(c);
   if (rc) return rc;
   return fmmgpu_download_fields(c, pot, fx, fy, fz, 0);
+}
+
+namespace {
+// FMMGPU_TRACE=1: timeline of pipelined runs (events per step, printed by run_wait)
+std::vector<std::pair<std::string, cudaEvent_t>> g_pipe_trace;
+void pipe_mark(const char* what, uint64_t k, cudaStream_t s) {
+  static const bool on = std::getenv("FMMGPU_TRACE") != nullptr;
+  if (!on) return;
+  cudaEvent_t e;
+  FMM_CUDA(cudaEventCreate(&e));
+  FMM_CUDA(cudaEventRecord(e, s));
+  g_pipe_trace.emplace_back(std::string(what) + " " + std::to_string(k), e);
+}
+void pipe_trace_dump() {
+  if (g_pipe_trace.empty()) return;
+  for (auto& [what, e] : g_pipe_trace) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g_pipe_trace.front().second, e);
+    std::fprintf(stderr, "[pipe] %9.3f ms  %s\n", ms, what.c_str());
+  }
+  for (auto& pe : g_pipe_trace) cudaEventDestroy(pe.second);
+  g_pipe_trace.clear();
+}
+}  // namespace
+
+// Pipelined run_fmm over a stream of particle sets. Step k's H2D runs on its own copy
+// stream as soon as tree build k-1 has finished reading the input buffer, i.e. under
+// evaluation k-1; step k's fields are gathered into one of two pipeline buffers and
+// copied back on a second copy stream under tree build + evaluation k+1. The device
+// work of one step is unchanged (tree build, evaluate, gather); only the PCIe copies
+// leave the critical path.
+namespace {
+// One pipelined step on context c (its own copy streams, events and output slots).
+void pipe_step(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, int group, double* pot, double* fx,
+               double* fy, double* fz) {
+  if (!c->s_h2d) {
+    FMM_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    FMM_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_in_free, cudaEventDisableTiming));
+    FMM_CUDA(cudaEventCreateWithFlags(&c->ev_in_ready, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      FMM_CUDA(cudaEventCreateWithFlags(&c->ev_out_ready[i], cudaEventDisableTiming));
+      FMM_CUDA(cudaEventCreateWithFlags(&c->ev_d2h_done[i], cudaEventDisableTiming));
+      FMM_CUDA(cudaEventRecord(c->ev_d2h_done[i], c->s_d2h));
+    }
+    FMM_CUDA(cudaEventRecord(c->ev_in_free, c->s_far));
+  }
+  if (c->d_in_cap < n || c->pipe_cap < n) {  // grow: drain the pipeline first
+    FMM_CUDA(cudaStreamSynchronize(c->s_h2d));
+    FMM_CUDA(cudaStreamSynchronize(c->s_d2h));
+    FMM_CUDA(cudaStreamSynchronize(c->s_near));
+    if (c->d_in_cap < n) {
+      if (c->d_in) FMM_CUDA(cudaFreeAsync(c->d_in, c->s_far));
+      FMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c->d_in), n * sizeof(double4), c->s_far));
+      c->d_in_cap = n;
+    }
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+    if (c->pipe_cap < n) {
+      for (auto& p : c->pipe_out) {
+        if (p) FMM_CUDA(cudaFree(p));
+        p = nullptr;
+        FMM_CUDA(cudaMalloc(&p, 32 * n));
+      }
+      c->pipe_cap = n;
+    }
+    FMM_CUDA(cudaEventRecord(c->ev_in_free, c->s_far));
+  }
+  FMM_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_in_free, 0));
+  pipe_mark("h2d start", c->pipe_k, c->s_h2d);
+  FMM_CUDA(cudaMemcpyAsync(c->d_in, xyzw, n * sizeof(double4), cudaMemcpyHostToDevice, c->s_h2d));
+  FMM_CUDA(cudaEventRecord(c->ev_in_ready, c->s_h2d));
+  pipe_mark("h2d end", c->pipe_k, c->s_h2d);
+  FMM_CUDA(cudaStreamWaitEvent(c->s_far, c->ev_in_ready, 0));
+  c->out_valid = false;
+  pipe_mark("tree start", c->pipe_k, c->s_far);
+  tree_build(c, reinterpret_cast<const double*>(c->d_in), n, true, height, group, nullptr);
+  FMM_CUDA(cudaEventRecord(c->ev_in_free, c->s_far));
+  pipe_mark("tree end", c->pipe_k, c->s_far);
+  const int slot = static_cast<int>(c->pipe_k & 1);
+  FMM_CUDA(cudaStreamWaitEvent(c->s_far, c->ev_d2h_done[slot], 0));
+  double* own_out = c->d_out;
+  c->d_out = c->pipe_out[slot];
+  const int rc = fmmgpu_evaluate(c);
+  c->d_out = own_out;
+  c->out_valid = false;
+  if (rc != FMMGPU_OK) throw Error(rc, c->err);
+  FMM_CUDA(cudaEventRecord(c->ev_out_ready[slot], c->s_far));
+  pipe_mark("eval end", c->pipe_k, c->s_far);
+  FMM_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_out_ready[slot], 0));
+  pipe_mark("d2h start", c->pipe_k, c->s_d2h);
+  double* dst[4] = {pot, fx, fy, fz};
+  for (int i = 0; i < 4; ++i)
+    if (dst[i])
+      FMM_CUDA(cudaMemcpyAsync(dst[i], c->pipe_out[slot] + i * n, 8 * n, cudaMemcpyDeviceToHost, c->s_d2h));
+  FMM_CUDA(cudaEventRecord(c->ev_d2h_done[slot], c->s_d2h));
+  pipe_mark("d2h end", c->pipe_k, c->s_d2h);
+  ++c->pipe_k;
+}
+
+}  // namespace
+
+int fmmgpu_run_async(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, int group, double* pot,
+                     double* fx, double* fy, double* fz) {
+  return guarded(c, [&] {
+    FMM_CUDA(cudaSetDevice(c->device));
+    if (!xyzw) throw Error(FMMGPU_INVALID_ARGUMENT, "run_async: null particle buffer");
+    if (n == 0) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: empty particle set");
+    pipe_step(c, xyzw, n, height, group, pot, fx, fy, fz);
+  });
+}
+
+int fmmgpu_run_wait(fmmgpu_ctx* c) {
+  return guarded(c, [&] {
+    FMM_CUDA(cudaSetDevice(c->device));
+    if (c->s_d2h) FMM_CUDA(cudaStreamSynchronize(c->s_d2h));
+    if (c->s_h2d) FMM_CUDA(cudaStreamSynchronize(c->s_h2d));
+    FMM_CUDA(cudaStreamSynchronize(c->s_near));
+    FMM_CUDA(cudaStreamSynchronize(c->s_far));
+    pipe_trace_dump();
+  });
 }
 
 int fmmgpu_tree_info(const fmmgpu_ctx* c, uint64_t* n, int* height, int* group, double* root4) {

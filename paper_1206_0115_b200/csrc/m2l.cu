@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   // behind the tile's DMMAs: per row {destination column, vector index or -1}, and the
   // tile's vector slots feeding the (vector, column) -> target lookup
   const int kt_fill = KT / 2;
-  int2 info[MT];
+  int4 rowinfo[MT];  // consumed only by the tile's epilogue, KT k-slices after the load
   int slot_e0 = -1, slot_e1 = -1;
   int mt = mt0, kt = 0, stage = 0;
   for (int t = 0; t < TOTAL; ++t) {
@@ -455,10 +455,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
     uint32_t* tg = tgt + (mt & 1) * g.vtMax * BN;
     if (kt == 0) {
 #pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const int4 r = __ldg(g.rowA + cls * g.rowsA + mt * PA_BM + wm * WTM + i * 8 + gq);
-        info[i] = make_int2(r.y, r.x >= 0 ? r.z : -1);
-      }
+      for (int i = 0; i < MT; ++i) rowinfo[i] = __ldg(g.rowA + cls * g.rowsA + mt * PA_BM + wm * WTM + i * 8 + gq);
       const int* vec = g.tileVec + (size_t(cls) * MTILES + mt) * g.vtMax;
       slot_e0 = tid < g.vtMax * BN ? __ldg(vec + tid / BN) : -1;
       slot_e1 = tid + PA_THREADS < g.vtMax * BN ? __ldg(vec + (tid + PA_THREADS) / BN) : -1;
@@ -496,14 +493,14 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
       // scatter block v of source s to target s - v, target-side column info.x
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        if (info[i].y >= 0) {
-          const uint32_t* trow = tg + info[i].y * BN;
+        if (rowinfo[i].x >= 0) {
+          const uint32_t* trow = tg + rowinfo[i].z * BN;
 #pragma unroll
           for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const uint32_t tcell = trow[wn * WTN + j * 8 + 2 * tq + e];
-              if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + info[i].x] = acc[i][j][e];
+              if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + rowinfo[i].y] = acc[i][j][e];
             }
         }
 #pragma unroll

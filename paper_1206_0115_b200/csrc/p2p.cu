@@ -3,18 +3,27 @@
 // evaluated one-sided per target so every accumulator has exactly one writer
 // (deterministic, no atomics, no P2PBuffers slots).
 //
-// Mapping: one CTA per non-empty parent cell (level leaf-1).
-// Its 2x2x2 children are the target cells; the union of their 27-neighbourhoods
-// is the 4x4x4 block of leaf positions around the parent, whose particles are
-// staged ONCE into shared memory as {x,y,z,w} (8 loads per particle per
-// evaluation instead of 27). Warp w owns child octant w: its targets sit in
-// registers, 32 at a time, and every source is a broadcast LDS.128 pair. When
-// fewer than 32 targets remain, the lanes split the sources of each neighbour
-// cell S ways (S = 32 / remaining) and the S partial sums are combined in a fixed
-// order through shared memory, so a 38-particle leaf costs 1.2 passes, not 2.
-// Neighbourhoods larger than the staging capacity (non-uniform clouds) are
-// streamed through shared memory in chunks; targets then accumulate into HBM per
-// chunk, still single-writer.
+// Unit of staging: one parent cell (level leaf-1). Its 2x2x2
+// children are the target cells; the union of their 27-neighbourhoods is the 4x4x4
+// block of leaf positions around the parent, whose particles are staged ONCE into
+// shared memory as {x,y,z,w} (8 loads per particle per evaluation instead of 27),
+// each position's segment padded so a child's 27 neighbours read as 9 contiguous runs
+// of whole groups of 4. Work units: every full 32-target pass of every child, then
+// each child's partial last pass; targets sit in registers (one per lane) and every
+// source is a broadcast LDS.128 pair. A partial pass of m < 32 targets splits the
+// sources of each run S = 32 / m ways and combines the S partial sums in a fixed order
+// through shared memory.
+//
+// Two kernels share the unit routine (so results are bit-identical):
+//  * k_p2p_flow (persistent, one CTA per SM): the CTA walks its parents through two
+//    staging slots. Warps pull units of the current parent from the slot's queue and
+//    move on to the next parent (already staged) as soon as the queue is empty; the
+//    last warp to leave a parent restages that slot with the parent after next
+//    (cp.async), so no CTA-wide barrier exists and no warp idles at a parent's end.
+//  * k_p2p (CTA per parent, 2 CTAs per SM): parents whose neighbourhood exceeds one
+//    staging slot stream it through shared memory in chunks (targets then accumulate
+//    into HBM per chunk, still single-writer), and shallow trees with too few parents
+//    for the persistent grid split a parent's units over several CTAs.
 //
 // Per interaction: 3 DADD (d) + 3 DP (r^2) + MUFU.RSQ64H and 4 DP (rsqrt_nr)
 // + 1 DMUL (w/r) + 1 DADD (pot) + 2 DMUL (w/r^3) + 3 DFMA (force) = 18 DP ops.
@@ -26,29 +35,20 @@ namespace fmmgpu {
 
 namespace {
 
-constexpr int P2P_CAP = 3072;            // staged particles per chunk (96 KB), multiple of 4
+constexpr int P2P_CAP = 3072;  // staged particles per chunk / slot (96 KB), multiple of 4
 
 struct P2PArgs {
   LevelView leaf;
   const uint64_t* parent_code;  // level leaf-1
   uint32_t p0;                  // first parent of the launch (partitioned runs: owned range)
-  uint32_t usplit;              // CTAs per parent: CTA y takes the units u = y (mod usplit)
+  uint32_t np;                  // parents in the launch
+  uint32_t usplit;              // k_p2p: CTAs per parent (CTA y takes the units u = y (mod usplit))
+  int only_big;                 // k_p2p: skip parents whose neighbourhood fits one slot
   const uint32_t* first;        // leaf first_particle
   const uint32_t* count;        // leaf particle_count
   const double4* pw;
   double4* near;  // [n] x {pot, fx, fy, fz}, Morton order
   uint64_t n;
-};
-
-template <int WARPS>
-struct P2PSmem {
-  double4 src[P2P_CAP + 4];  // + one group of zero-weight sources (tail of a 2-group step)
-  double red[WARPS][4][32];
-  uint32_t first[64];
-  uint32_t cnt[64];
-  uint32_t voff[65];  // virtual offsets of the 64 positions (prefix sum of counts padded to 4)
-  uint32_t full_off[9];  // prefix over the 8 children of their full 32-target passes
-  uint32_t next_unit;    // work-unit queue head (per chunk)
 };
 
 // A staged source that contributes exactly zero: w = 0 far away (finite r^2, so
@@ -71,6 +71,174 @@ __device__ __forceinline__ void interact(const double xi, const double yi, const
   fz = fma(s3, dz, fz);
 }
 
+// leaf position (0..63) of child octant w inside the 4x4x4 block
+__device__ __forceinline__ int child_pos(int w) {
+  return ((1 + ((w >> 2) & 1)) << 4) | ((1 + ((w >> 1) & 1)) << 2) | (1 + (w & 1));
+}
+
+// Metadata of one staged neighbourhood.
+struct Neigh {
+  uint32_t first[64];
+  uint32_t cnt[64];
+  uint32_t voff[65];     // virtual offsets of the 64 positions (prefix sum of padded counts)
+  uint32_t full_off[9];  // prefix over the 8 children of their full 32-target passes
+  uint32_t nunits;
+};
+
+// Counts and padded offsets of the 64 leaf positions around parent pc, by one warp
+// (lane handles positions lane and lane + 32). Runs start at qc = 0 or 1 and end at
+// qc = 3 or the row end, so only those boundaries must sit on groups of 4: position
+// qc = 1 is not padded and qc = 2 pads the pair (qc = 1, qc = 2) to whole groups.
+__device__ void neigh_meta(const P2PArgs& a, const int pc[3], Neigh& nb, int lane) {
+  uint32_t x[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int pos = lane + 32 * h;
+    const int qa = pos >> 4, qb = (pos >> 2) & 3, qc = pos & 3;
+    const uint32_t cell = find_ijk(a.leaf, 2 * pc[0] - 1 + qa, 2 * pc[1] - 1 + qb, 2 * pc[2] - 1 + qc);
+    const uint32_t cnt = cell == NPOS ? 0u : a.count[cell];
+    nb.first[pos] = cell == NPOS ? 0u : a.first[cell];
+    nb.cnt[pos] = cnt;
+    const uint32_t cnt_prev = __shfl_up_sync(0xffffffffu, cnt, 1);
+    uint32_t v = qc == 1 ? cnt : qc == 2 ? ((cnt_prev + cnt + 3u) & ~3u) - cnt_prev : (cnt + 3u) & ~3u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    x[h] = v;
+  }
+  const uint32_t tot0 = __shfl_sync(0xffffffffu, x[0], 31);
+  nb.voff[lane + 1] = x[0];
+  nb.voff[lane + 33] = x[1] + tot0;
+  if (lane == 0) nb.voff[0] = 0;
+  __syncwarp();
+  if (lane == 0) {
+    uint32_t acc = 0, npart = 0;
+    for (int w = 0; w < 8; ++w) {
+      nb.full_off[w] = acc;
+      const uint32_t c = nb.cnt[child_pos(w)];
+      acc += c / 32u;
+      npart += (c % 32u) != 0;
+    }
+    nb.full_off[8] = acc;
+    nb.nunits = acc + npart;
+  }
+  __syncwarp();
+}
+
+// Virtual slot v (< voff[64]) -> staged source (a particle or a zero-weight pad).
+__device__ __forceinline__ void locate(const Neigh& nb, uint32_t v, uint32_t& pos, uint32_t& k) {
+  int lo = 0, hi = 63;  // last position with voff[pos] <= v
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (nb.voff[mid] <= v) lo = mid; else hi = mid - 1;
+  }
+  pos = static_cast<uint32_t>(lo);
+  k = v - nb.voff[lo];
+}
+
+// One work unit u over the staged sources [base, base + clen) of the virtual range;
+// src[0..clen) are the staged sources, src[P2P_CAP..+4) a group of zero sources.
+template <int G>
+__device__ void p2p_unit(const P2PArgs& a, const Neigh& nb, const double4* src, uint32_t base, uint32_t clen,
+                         uint32_t u, double (*red)[32], int lane) {
+  const uint32_t nfull = nb.full_off[8];
+  // decode unit -> (child octant w, first target t0)
+  int w = 0;
+  uint32_t t0 = 0;
+  if (u < nfull) {
+    while (nb.full_off[w + 1] <= u) ++w;
+    t0 = 32u * (u - nb.full_off[w]);
+  } else {
+    uint32_t k = u - nfull;
+    for (w = 0; w < 8; ++w) {
+      if (nb.cnt[child_pos(w)] % 32u == 0) continue;
+      if (k == 0) break;
+      --k;
+    }
+    t0 = 32u * (nb.full_off[w + 1] - nb.full_off[w]);
+  }
+  const int ca = (w >> 2) & 1, cb = (w >> 1) & 1, cc = w & 1;
+  const int tpos = child_pos(w);
+  const uint32_t nT = nb.cnt[tpos];
+  const uint32_t tfirst = nb.first[tpos];
+  const uint32_t m = min(32u, nT - t0);
+  const uint32_t S = 32u / m;
+  const uint32_t lt = lane % m, split = lane / m;
+  const bool active = split < S;
+  const uint64_t tg = uint64_t(tfirst) + t0 + lt;
+  const double4 xi = a.pw[tg];
+  double pot = 0, fx = 0, fy = 0, fz = 0;
+  if (active) {
+    // the 27 neighbour positions as 9 runs of 3 consecutive positions (qc = cc..cc+2),
+    // whose padded segments are contiguous in shared memory
+#pragma unroll 1
+    for (int q = 0; q < 9; ++q) {
+      const int pos = ((ca + q / 3) << 4) | ((cb + q % 3) << 2) | cc;
+      // intersection of the run's virtual range with this chunk, chunk-relative
+      // (segments are padded to groups of 4 and chunks are multiples of 4)
+      const uint32_t v0 = max(nb.voff[pos], base), v1 = min(nb.voff[pos + 3], base + clen);
+      const int g1 = static_cast<int>(v1 - base) >> 2;
+      const int gs = static_cast<int>(S);
+      for (int g = (static_cast<int>(v0 - base) >> 2) + static_cast<int>(split); g < g1; g += G * gs) {
+        const double4* sj = src + 4 * g;
+        const double4 p0 = sj[0], p1 = sj[1], p2 = sj[2], p3 = sj[3];
+        if constexpr (G == 2) {
+          const double4* sk = (g + gs < g1) ? src + 4 * (g + gs) : src + P2P_CAP;
+          const double4 p4 = sk[0], p5 = sk[1], p6 = sk[2], p7 = sk[3];
+          interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p4, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p5, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p6, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p7, pot, fx, fy, fz);
+        } else {
+          interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
+          interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
+        }
+      }
+    }
+  }
+  if (S > 1) {  // combine the S source splits of each target in a fixed order
+    red[0][lane] = pot;
+    red[1][lane] = fx;
+    red[2][lane] = fy;
+    red[3][lane] = fz;
+    __syncwarp();
+    if (lane < m) {
+      for (uint32_t s = 1; s < S; ++s) {
+        pot += red[0][lane + s * m];
+        fx += red[1][lane + s * m];
+        fy += red[2][lane + s * m];
+        fz += red[3][lane + s * m];
+      }
+    }
+    __syncwarp();
+  }
+  if (lane < m) {
+    double4 r = a.near[tg];
+    r.x += pot;
+    r.y += fx;
+    r.z += fy;
+    r.w += fz;
+    a.near[tg] = r;
+  }
+}
+
+// ------------------------------------------------------------------ k_p2p
+template <int WARPS>
+struct P2PSmem {
+  double4 src[P2P_CAP + 4];  // + one group of zero-weight sources (tail of a 2-group step)
+  double red[WARPS][4][32];
+  Neigh nb;
+  uint32_t next_unit;  // work-unit queue head (per chunk)
+};
+
 // WARPS warps per CTA pull the work units; G groups of 4 sources per inner iteration.
 template <int WARPS, int G>
 __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
@@ -82,161 +250,115 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
   int pc[3];
   demorton(a.parent_code[a.p0 + blockIdx.x / a.usplit], pc);
   const uint32_t ysplit = blockIdx.x % a.usplit;
-  if (tid < 64) {
-    const int qa = tid >> 4, qb = (tid >> 2) & 3, qc = tid & 3;
-    const uint32_t cell = find_ijk(a.leaf, 2 * pc[0] - 1 + qa, 2 * pc[1] - 1 + qb, 2 * pc[2] - 1 + qc);
-    const uint32_t cnt = cell == NPOS ? 0u : a.count[cell];
-    sm.first[tid] = cell == NPOS ? 0u : a.first[cell];
-    sm.cnt[tid] = cnt;
-    // inclusive warp scan over the 64 padded counts (two warps), then fix up
-    // runs start at qc = 0 or 1 and end at qc = 3 or the row end, so only those
-    // boundaries must sit on groups of 4: position qc = 1 is not padded and qc = 2
-    // pads the pair (qc = 1, qc = 2) to a whole number of groups
-    const uint32_t cnt_prev = __shfl_up_sync(0xffffffffu, cnt, 1);
-    uint32_t x = qc == 1 ? cnt : qc == 2 ? ((cnt_prev + cnt + 3u) & ~3u) - cnt_prev : (cnt + 3u) & ~3u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if ((tid & 31) >= o) x += y;
-    }
-    sm.voff[tid + 1] = x;
-    if (tid == 0) sm.voff[0] = 0;
-  }
-  __syncthreads();
-  if (tid >= 33 && tid <= 64) sm.voff[tid] += sm.voff[32];
-  __syncthreads();
-  const uint32_t total = sm.voff[64];
-
-  // Work units: every full 32-target pass of every child, then every child's partial
-  // last pass (cost ~ m/32 of a full one). Warps pull units from a shared queue, so a
-  // CTA whose children differ in size still keeps all 8 warps busy to the end (a
-  // static warp-per-child mapping idles ~20% at ~38 particles per leaf). Each unit
-  // owns distinct targets, so results do not depend on which warp takes it.
+  if (warp == 0) neigh_meta(a, pc, sm.nb, lane);
   if (tid < 4) sm.src[P2P_CAP + tid] = dummy_source();
-  if (tid == 0) {
-    uint32_t acc = 0;
-    for (int w = 0; w < 8; ++w) {
-      sm.full_off[w] = acc;
-      const int tp = ((1 + ((w >> 2) & 1)) << 4) | ((1 + ((w >> 1) & 1)) << 2) | (1 + (w & 1));
-      acc += sm.cnt[tp] / 32u;
-    }
-    sm.full_off[8] = acc;
-  }
   __syncthreads();
-  const uint32_t nfull = sm.full_off[8];
-  uint32_t npart = 0;
-  for (int w = 0; w < 8; ++w) {
-    const int tp = ((1 + ((w >> 2) & 1)) << 4) | ((1 + ((w >> 1) & 1)) << 2) | (1 + (w & 1));
-    npart += (sm.cnt[tp] % 32u) != 0;
-  }
-  const uint32_t nunits = nfull + npart;
+  const uint32_t total = sm.nb.voff[64];
+  if (a.only_big && total <= static_cast<uint32_t>(P2P_CAP)) return;  // done by k_p2p_flow
+  const uint32_t nunits = sm.nb.nunits;
 
   for (uint32_t base = 0; base < total; base += P2P_CAP) {
     const uint32_t clen = min(static_cast<uint32_t>(P2P_CAP), total - base);
     if (base) __syncthreads();
     if (tid == 0) sm.next_unit = 0;
     for (uint32_t i = tid; i < clen; i += P2P_THREADS) {
-      const uint32_t v = base + i;
-      int lo = 0, hi = 63;  // last position with voff[pos] <= v
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sm.voff[mid] <= v) lo = mid; else hi = mid - 1;
-      }
-      const uint32_t k = v - sm.voff[lo];
-      sm.src[i] = k < sm.cnt[lo] ? a.pw[sm.first[lo] + k] : dummy_source();
+      uint32_t pos, k;
+      locate(sm.nb, base + i, pos, k);
+      sm.src[i] = k < sm.nb.cnt[pos] ? a.pw[sm.nb.first[pos] + k] : dummy_source();
     }
     __syncthreads();
-
     for (;;) {
       uint32_t u = 0;
       if (lane == 0) u = atomicAdd(&sm.next_unit, 1u);
       u = __shfl_sync(0xffffffffu, u, 0) * a.usplit + ysplit;
       if (u >= nunits) break;
-      // decode unit -> (child octant w, first target t0)
-      int w = 0;
-      uint32_t t0 = 0;
-      if (u < nfull) {
-        while (sm.full_off[w + 1] <= u) ++w;
-        t0 = 32u * (u - sm.full_off[w]);
+      p2p_unit<G>(a, sm.nb, sm.src, base, clen, u, sm.red[warp], lane);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ k_p2p_flow
+struct FlowSlot {
+  double4 src[P2P_CAP + 4];
+  Neigh nb;
+  uint32_t next_unit;  // unit queue head
+  uint32_t done;       // warps that found the queue empty
+  int ready;           // item index staged in this slot
+};
+template <int WARPS>
+struct FlowSmem {
+  FlowSlot slot[2];
+  double red[WARPS][4][32];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src));
+}
+
+// One warp stages item `it` (this CTA's it-th parent) into a slot and publishes it.
+// A neighbourhood larger than the slot is left to k_p2p (the slot gets no units).
+__device__ void flow_stage(const P2PArgs& a, FlowSlot& s, int it, int lane) {
+  const uint32_t parent = blockIdx.x + static_cast<uint32_t>(it) * gridDim.x;
+  int pc[3];
+  demorton(a.parent_code[a.p0 + parent], pc);
+  neigh_meta(a, pc, s.nb, lane);
+  const uint32_t total = s.nb.voff[64];
+  if (total > static_cast<uint32_t>(P2P_CAP)) {
+    if (lane == 0) s.nb.nunits = 0;
+  } else {
+    for (uint32_t i = lane; i < total; i += 32) {
+      uint32_t pos, k;
+      locate(s.nb, i, pos, k);
+      if (k < s.nb.cnt[pos]) {
+        const double4* g = a.pw + s.nb.first[pos] + k;
+        cp_async16(&s.src[i], g);
+        cp_async16(reinterpret_cast<double2*>(&s.src[i]) + 1, reinterpret_cast<const double2*>(g) + 1);
       } else {
-        uint32_t k = u - nfull;
-        for (w = 0; w < 8; ++w) {
-          const int tp = ((1 + ((w >> 2) & 1)) << 4) | ((1 + ((w >> 1) & 1)) << 2) | (1 + (w & 1));
-          if (sm.cnt[tp] % 32u == 0) continue;
-          if (k == 0) break;
-          --k;
-        }
-        t0 = 32u * (sm.full_off[w + 1] - sm.full_off[w]);
+        s.src[i] = dummy_source();
       }
-      const int ca = (w >> 2) & 1, cb = (w >> 1) & 1, cc = w & 1;
-      const int tpos = ((1 + ca) << 4) | ((1 + cb) << 2) | (1 + cc);
-      const uint32_t nT = sm.cnt[tpos];
-      const uint32_t tfirst = sm.first[tpos];
-      const uint32_t m = min(32u, nT - t0);
-      const uint32_t S = 32u / m;
-      const uint32_t lt = lane % m, split = lane / m;
-      const bool active = split < S;
-      const uint64_t tg = uint64_t(tfirst) + t0 + lt;
-      const double4 xi = a.pw[tg];
-      double pot = 0, fx = 0, fy = 0, fz = 0;
-      if (active) {
-        // the 27 neighbour positions as 9 runs of 3 consecutive positions (qc = cc..cc+2),
-        // whose padded segments are contiguous in shared memory
-#pragma unroll 1
-        for (int q = 0; q < 9; ++q) {
-          const int pos = ((ca + q / 3) << 4) | ((cb + q % 3) << 2) | cc;
-          // intersection of the run's virtual range with this chunk, chunk-relative
-          // (segments are padded to groups of 4 and chunks are multiples of 4)
-          const uint32_t v0 = max(sm.voff[pos], base), v1 = min(sm.voff[pos + 3], base + clen);
-          const int g1 = static_cast<int>(v1 - base) >> 2;
-          const int gs = static_cast<int>(S);
-          for (int g = (static_cast<int>(v0 - base) >> 2) + static_cast<int>(split); g < g1; g += G * gs) {
-            const double4* sj = sm.src + 4 * g;
-            const double4 p0 = sj[0], p1 = sj[1], p2 = sj[2], p3 = sj[3];
-            if constexpr (G == 2) {
-              const double4* sk = (g + gs < g1) ? sm.src + 4 * (g + gs) : sm.src + P2P_CAP;
-              const double4 p4 = sk[0], p5 = sk[1], p6 = sk[2], p7 = sk[3];
-              interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p4, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p5, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p6, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p7, pot, fx, fy, fz);
-            } else {
-              interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
-              interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
-            }
-          }
-        }
-      }
-      if (S > 1) {  // combine the S source splits of each target in a fixed order
-        sm.red[warp][0][lane] = pot;
-        sm.red[warp][1][lane] = fx;
-        sm.red[warp][2][lane] = fy;
-        sm.red[warp][3][lane] = fz;
-        __syncwarp();
-        if (lane < m) {
-          for (uint32_t s = 1; s < S; ++s) {
-            pot += sm.red[warp][0][lane + s * m];
-            fx += sm.red[warp][1][lane + s * m];
-            fy += sm.red[warp][2][lane + s * m];
-            fz += sm.red[warp][3][lane + s * m];
-          }
-        }
-        __syncwarp();
-      }
-      if (lane < m) {
-        double4 r = a.near[tg];
-        r.x += pot;
-        r.y += fx;
-        r.z += fy;
-        r.w += fz;
-        a.near[tg] = r;
-      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+  }
+  if (lane == 0) {
+    s.next_unit = 0;
+    s.done = 0;
+  }
+  __syncwarp();
+  __threadfence_block();
+  if (lane == 0) *reinterpret_cast<volatile int*>(&s.ready) = it;
+}
+
+template <int WARPS, int G>
+__global__ void __launch_bounds__(WARPS * 32, 1) k_p2p_flow(const P2PArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FlowSmem<WARPS>& sm = *reinterpret_cast<FlowSmem<WARPS>*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nitems = static_cast<int>((a.np - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  if (tid < 2) sm.slot[tid].ready = -1;
+  if (tid < 8) sm.slot[tid >> 2].src[P2P_CAP + (tid & 3)] = dummy_source();
+  __syncthreads();
+  if (warp < 2 && warp < nitems) flow_stage(a, sm.slot[warp], warp, lane);
+
+  for (int it = 0; it < nitems; ++it) {
+    FlowSlot& s = sm.slot[it & 1];
+    while (*reinterpret_cast<volatile int*>(&s.ready) != it) __nanosleep(64);
+    __threadfence_block();
+    const uint32_t nunits = s.nb.nunits;
+    for (;;) {
+      uint32_t u = 0;
+      if (lane == 0) u = atomicAdd(&s.next_unit, 1u);
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= nunits) break;
+      p2p_unit<G>(a, s.nb, s.src, 0, s.nb.voff[64], u, sm.red[warp], lane);
+    }
+    // the last warp to leave this parent restages the slot with item it + 2
+    uint32_t d = 0;
+    if (lane == 0) d = atomicAdd(&s.done, 1u);
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (d == WARPS - 1 && it + 2 < nitems) {
+      __threadfence_block();
+      flow_stage(a, s, it + 2, lane);
     }
   }
 }
@@ -249,29 +371,46 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const Level& P = c->lv[leaf - 1];
   const uint32_t np = P.own1 - P.own0;
   if (np == 0) return;
-  // few parents (shallow trees, big leaves): several CTAs per parent share its units
-  // (each re-stages the neighbourhood) so the grid still covers 2 CTAs per SM
-  uint32_t usplit = 1;
-  while (np * usplit < 2u * 148u && usplit < 16u) usplit *= 2;
-  P2PArgs a{L.view(leaf), P.code, P.own0, usplit, L.first_particle, L.particle_count, c->d_pw,
+  P2PArgs a{L.view(leaf), P.code, P.own0, np, 1, 0, L.first_particle, L.particle_count, c->d_pw,
              reinterpret_cast<double4*>(c->d_near), c->n};
-  auto run = [&](auto kern, int warps, int smem) {
+  auto run = [&](auto kern, int warps, int smem, unsigned grid) {
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<np * usplit, warps * 32, smem, s>>>(a);
+    kern<<<grid, warps * 32, smem, s>>>(a);
+    FMM_CUDA(cudaGetLastError());
+    ++c->launches;
   };
-  // FMMGPU_P2P_VARIANT (tuning experiments): 0 = 12 warps x 1 group, 1 = 8 x 2, 2 = 16 x 1, 3 = 8 x 1
+  // FMMGPU_P2P_VARIANT (tuning experiments): 0 = k_p2p 12 warps x 1 group (default),
+  // 1 = 8 x 2 groups, 2 = 16 x 1, 3 = 8 x 1; 6 / 7 = persistent k_p2p_flow with 16 / 24
+  // warps (+ chunked k_p2p for oversized neighbourhoods). Config B: 13.7 / 13.6 / - / -
+  // / 15.0 / 16.8 ms: with at most one parent of look-ahead the persistent warps idle
+  // at the same unit-granularity tails, with fewer warps per SM to hide latency.
   static const int variant = [] {
     const char* e = std::getenv("FMMGPU_P2P_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
-  switch (variant) {
-    case 1: run(k_p2p<8, 2>, 8, static_cast<int>(sizeof(P2PSmem<8>))); break;
-    case 2: run(k_p2p<16, 1>, 16, static_cast<int>(sizeof(P2PSmem<16>))); break;
-    case 3: run(k_p2p<8, 1>, 8, static_cast<int>(sizeof(P2PSmem<8>))); break;
-    default: run(k_p2p<12, 1>, 12, static_cast<int>(sizeof(P2PSmem<12>))); break;
+  int sms = 148;
+  FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const bool flow = (variant == 6 || variant == 7) && np >= 2u * static_cast<uint32_t>(sms);
+  if (flow) {
+    const unsigned grid = static_cast<unsigned>(sms);
+    if (variant == 7) run(k_p2p_flow<24, 1>, 24, static_cast<int>(sizeof(FlowSmem<24>)), grid);
+    else run(k_p2p_flow<16, 1>, 16, static_cast<int>(sizeof(FlowSmem<16>)), grid);
+    a.only_big = 1;  // the (rare) oversized neighbourhoods, chunked
+    run(k_p2p<12, 1>, 12, static_cast<int>(sizeof(P2PSmem<12>)), np);
+    return;
   }
-  FMM_CUDA(cudaGetLastError());
-  ++c->launches;
+  // few parents (shallow trees, big leaves): several CTAs per parent share its units
+  // (each re-stages the neighbourhood) so the grid still covers 2 CTAs per SM
+  uint32_t usplit = 1;
+  while (np * usplit < 2u * static_cast<uint32_t>(sms) && usplit < 16u) usplit *= 2;
+  a.usplit = usplit;
+  const unsigned grid = np * usplit;
+  switch (variant) {
+    case 1: run(k_p2p<8, 2>, 8, static_cast<int>(sizeof(P2PSmem<8>)), grid); break;
+    case 2: run(k_p2p<16, 1>, 16, static_cast<int>(sizeof(P2PSmem<16>)), grid); break;
+    case 3: run(k_p2p<8, 1>, 8, static_cast<int>(sizeof(P2PSmem<8>)), grid); break;
+    default: run(k_p2p<12, 1>, 12, static_cast<int>(sizeof(P2PSmem<12>)), grid); break;
+  }
 }
 
 }  // namespace fmmgpu

@@ -6,7 +6,11 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -26,6 +30,18 @@ void dfree(T*& p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
   p = nullptr;
 }
+
+// FMMGPU_TRACE=1: host wall time of the tree-build phases on stderr (development aid)
+struct PhaseTrace {
+  bool on = std::getenv("FMMGPU_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void operator()(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tree] %-24s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // bounding_cube (geometry.cpp:18-36): per-axis min / max. Exact (order-free).
 __global__ void k_minmax_partial(const double4* __restrict__ p, uint64_t n, double* __restrict__ part) {
@@ -129,6 +145,21 @@ __global__ void k_octant(const uint64_t* __restrict__ code, uint32_t n, uint8_t*
   if (i < n) { oct[i] = static_cast<uint8_t>(code[i] & 7); iota[i] = i; }
 }
 
+__global__ void k_copy_words(const uint32_t* __restrict__ src, uint32_t nwords, uint32_t* __restrict__ dst) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+// lower_bound of q = 0..8 in the sorted octants (parity class offsets)
+__global__ void k_class_offsets(const uint8_t* __restrict__ oct_sorted, uint32_t n, uint32_t* __restrict__ off) {
+  const int q = threadIdx.x;
+  if (q > 8) return;
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (oct_sorted[mid] < q) lo = mid + 1; else hi = mid;
+  }
+  off[q] = lo;
+}
+
 inline unsigned blocks(uint64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 void free_level(fmmgpu::Level& L, cudaStream_t s) {
@@ -141,6 +172,18 @@ void free_level(fmmgpu::Level& L, cudaStream_t s) {
 }
 
 }  // namespace
+
+const void* readback(fmmgpu_ctx* c, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes > READBACK_CAP || bytes % 4) throw Error(FMMGPU_LOGIC_ERROR, "readback: bad size");
+  if (!c->h_rb) FMM_CUDA(cudaHostAlloc(&c->h_rb, READBACK_CAP, cudaHostAllocMapped));
+  uint32_t* d = nullptr;
+  FMM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), c->h_rb, 0));
+  const uint32_t nw = static_cast<uint32_t>(bytes / 4);
+  k_copy_words<<<std::max(1u, std::min(64u, (nw + 255) / 256)), 256, 0, s>>>(static_cast<const uint32_t*>(src), nw, d);
+  FMM_CUDA(cudaGetLastError());
+  FMM_CUDA(cudaStreamSynchronize(s));
+  return c->h_rb;
+}
 
 void* scratch(fmmgpu_ctx* c, size_t bytes) {
   if (bytes > c->d_tmp_cap) {
@@ -169,18 +212,23 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   if (n >= 0xffffffffull) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: particle count exceeds 32-bit ids");
   if (root4 && !(root4[3] > 0)) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: root cube width must be positive");
   cudaStream_t s = c->s_far;
+  PhaseTrace trace;
   fmmgpu_invalidate_graph(c);
   partition_free(c);
   tree_free(c);
   lists_free(c);
+  trace("free");
 
-  // input -> device (input order)
-  if (c->d_in_cap < n) {
+  // input -> device (input order); a pipelined run (fmmgpu_run_async) has already
+  // copied it into d_in on its H2D stream
+  const bool in_place = on_device && xyzw == reinterpret_cast<const double*>(c->d_in) && c->d_in_cap >= n;
+  if (!in_place && c->d_in_cap < n) {
     if (c->d_in) FMM_CUDA(cudaFreeAsync(c->d_in, s));
     FMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c->d_in), n * sizeof(double4), s));
     c->d_in_cap = n;
   }
-  FMM_CUDA(cudaMemcpyAsync(c->d_in, xyzw, n * sizeof(double4), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  if (!in_place)
+    FMM_CUDA(cudaMemcpyAsync(c->d_in, xyzw, n * sizeof(double4), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   FMM_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
 
   // root cube
@@ -193,8 +241,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     k_minmax_partial<<<nb, 256, 0, s>>>(c->d_in, n, part);
     FMM_CUDA(cudaGetLastError());
     std::vector<double> h(6 * nb);
-    FMM_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * 6 * nb, cudaMemcpyDeviceToHost, s));
-    FMM_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(h.data(), readback(c, part, sizeof(double) * 6 * nb, s), sizeof(double) * 6 * nb);
     double lo[3], hi[3];
     for (int a = 0; a < 3; ++a) {
       lo[a] = h[a * nb];
@@ -211,6 +258,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     }
     root[3] = extent > 0 ? extent * (1.0 + 1e-6) : 1.0;
   }
+  trace("root cube");
   std::copy(root, root + 4, c->root);
   c->n = n;
   c->height = height;
@@ -242,6 +290,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw, c->d_inv);
   FMM_CUDA(cudaGetLastError());
 
+  trace("keys+sort+permute");
   // leaf cells = runs of equal keys (geometry.cpp:113-122)
   c->lv.resize(height);
   Level& L = c->lv[leaf];
@@ -251,8 +300,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, keys_sorted, L.code, L.particle_count, d_runs, static_cast<int>(n), s));
   FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, keys_sorted, L.code, L.particle_count, d_runs, static_cast<int>(n), s));
   uint32_t runs = 0;
-  FMM_CUDA(cudaMemcpyAsync(&runs, d_runs, 4, cudaMemcpyDeviceToHost, s));
-  FMM_CUDA(cudaStreamSynchronize(s));
+  runs = *static_cast<const uint32_t*>(readback(c, d_runs, 4, s));
   L.n = runs;
   L.first_particle = dalloc<uint32_t>(runs, s);
   FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, L.particle_count, L.first_particle, static_cast<int>(runs), s));
@@ -268,6 +316,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
                                                                c->d_pcell, c->d_flag);
   FMM_CUDA(cudaGetLastError());
 
+  trace("leaf level");
   // parent levels by code >> 3 (geometry.cpp:138-153)
   uint64_t* shifted = keys;  // reuse
   for (int v = leaf - 1; v >= 0; --v) {
@@ -278,8 +327,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     P.child_count = dalloc<uint32_t>(C.n, s);
     FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, shifted, P.code, P.child_count, d_runs, static_cast<int>(C.n), s));
     FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, shifted, P.code, P.child_count, d_runs, static_cast<int>(C.n), s));
-    FMM_CUDA(cudaMemcpyAsync(&runs, d_runs, 4, cudaMemcpyDeviceToHost, s));
-    FMM_CUDA(cudaStreamSynchronize(s));
+    runs = *static_cast<const uint32_t*>(readback(c, d_runs, 4, s));
     P.n = runs;
     P.first_child = dalloc<uint32_t>(runs, s);
     FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, P.child_count, P.first_child, static_cast<int>(runs), s));
@@ -298,6 +346,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   dfree(idx, s);
   dfree(d_runs, s);
 
+  trace("parent levels");
   // blocks of group_size cells (geometry.cpp:155-160); lookup maps; parity classes;
   // expansions (cell-major, stride ldE, zero padding)
   for (int v = 0; v < height; ++v) {
@@ -320,11 +369,10 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
       k_octant<<<blocks(V.n, 256), 256, 0, s>>>(V.code, V.n, oct, iota);
       FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, oct, oct_sorted, iota, V.cls_cells, static_cast<int>(V.n), 0, 3, s));
       FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, oct, oct_sorted, iota, V.cls_cells, static_cast<int>(V.n), 0, 3, s));
-      std::vector<uint8_t> h(V.n);
-      FMM_CUDA(cudaMemcpyAsync(h.data(), oct_sorted, V.n, cudaMemcpyDeviceToHost, s));
-      FMM_CUDA(cudaStreamSynchronize(s));
-      for (int q = 0; q <= 8; ++q)
-        V.cls_off[q] = static_cast<uint32_t>(std::lower_bound(h.begin(), h.end(), static_cast<uint8_t>(q)) - h.begin());
+      uint32_t* d_off = dalloc<uint32_t>(9, s);
+      k_class_offsets<<<1, 32, 0, s>>>(oct_sorted, V.n, d_off);
+      std::memcpy(V.cls_off, readback(c, d_off, 9 * sizeof(uint32_t), s), 9 * sizeof(uint32_t));
+      dfree(d_off, s);
       dfree(oct, s);
       dfree(oct_sorted, s);
       dfree(iota, s);
@@ -339,6 +387,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     FMM_CUDA(cudaMemsetAsync(V.local_own, 0, e * 8, s));
     FMM_CUDA(cudaMemsetAsync(V.local_down, 0, e * 8, s));
   }
+  trace("blocks+classes+expansions");
   c->part_rank = 0;
   c->part_n = 1;
   c->part_align = 0;
@@ -351,8 +400,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   FMM_CUDA(cudaMemsetAsync(c->d_far, 0, 32 * n, s));
 
   int flag = 0;
-  FMM_CUDA(cudaMemcpyAsync(&flag, c->d_flag, 4, cudaMemcpyDeviceToHost, s));
-  FMM_CUDA(cudaStreamSynchronize(s));
+  flag = *static_cast<const int*>(readback(c, c->d_flag, 4, s));
+  trace("fields+flag sync");
   if (flag & 1) {
     tree_free(c);
     throw Error(FMMGPU_DOMAIN_ERROR, "GroupTree: particle outside the root cube");

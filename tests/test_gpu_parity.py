@@ -245,6 +245,42 @@ def test_run_entry_point(fmm):
     assert force_error(*g[1:], *of[1:]) <= TOL
 
 
+def test_pipelined_runs(fmm):
+    """fmmgpu_run_async over a stream of different particle sets (sizes, heights and
+    distributions change between steps, so buffers grow mid-stream) returns, for every
+    step, exactly the fields of a serial fmmgpu_run of that set."""
+    import torch
+    sets = [(make_particles(6000, "uniform", 21, True), 4), (make_particles(9000, "sphere", 22, False), 5),
+            (make_particles(6000, "uniform", 23, False), 4), (make_particles(12000, "uniform", 24, True), 4),
+            (make_particles(3000, "uniform", 25, True), 3), (make_particles(7000, "sphere", 26, True), 4)]
+    c = fmm.FmmContext(None, order=4)
+    serial = [c.run(x, h) for x, h in sets]
+    pins = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x, _ in sets]
+    outs = [[torch.full((len(x),), np.nan, dtype=torch.float64).pin_memory() for _ in range(4)] for x, _ in sets]
+    for k, (x, h) in enumerate(sets):
+        c.run_async(pins[k].data_ptr(), len(x), h, 250, [o.data_ptr() for o in outs[k]])
+    c.run_wait()
+    for k in range(len(sets)):
+        for got, want in zip(outs[k], serial[k]):
+            assert np.array_equal(got.numpy(), want)
+    # the context holds the last step's tree afterwards
+    c.evaluate()
+    for got, want in zip(c.gather(), serial[-1]):
+        assert np.array_equal(got, want)
+    # tree-build errors surface synchronously with the reference's classes
+    bad = torch.from_numpy(np.zeros((2, 4))).pin_memory()
+    with pytest.raises(fmm.DomainError):
+        c.run_async(bad.data_ptr(), 2, 4, 250, [o.data_ptr() for o in outs[0]])
+    c.run_wait()
+    # the pipeline keeps working after an error and after the hand-back
+    for k in (0, 1):
+        c.run_async(pins[k].data_ptr(), len(sets[k][0]), sets[k][1], 250, [o.data_ptr() for o in outs[k]])
+    c.run_wait()
+    for k in (0, 1):
+        for got, want in zip(outs[k], serial[k]):
+            assert np.array_equal(got.numpy(), want)
+
+
 def test_edge_cases(fmm):
     P = fmm
     # single particle: zero fields (geometry.cpp bounding_cube width 1, test_geometry.cpp:202-210)

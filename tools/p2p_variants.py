@@ -20,10 +20,11 @@ if len(sys.argv) > 1:
     np.save(f"/tmp/p2p_v{sys.argv[1]}.npy", np.stack(f))
     print(f"variant {sys.argv[1]}: {ms:.3f} ms", flush=True)
 else:
-    for v in range(4):
+    VARIANTS = [0, 1, 6, 7]  # 0 = k_p2p 12 warps (default), 6 / 7 = persistent 16 / 24 warps
+    for v in VARIANTS:
         env = dict(os.environ, FMMGPU_P2P_VARIANT=str(v))
         subprocess.run([sys.executable, __file__, str(v)], env=env, check=True)
     import numpy as np
-    base = np.load("/tmp/p2p_v0.npy")
-    for v in range(1, 4):
-        print(f"variant {v} bitwise equal to 0:", bool(np.array_equal(np.load(f"/tmp/p2p_v{v}.npy"), base)))
+    base = np.load(f"/tmp/p2p_v{VARIANTS[0]}.npy")
+    for v in VARIANTS[1:]:
+        print(f"variant {v} bitwise equal to {VARIANTS[0]}:", bool(np.array_equal(np.load(f"/tmp/p2p_v{v}.npy"), base)))

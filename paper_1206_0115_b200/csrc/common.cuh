@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -152,6 +154,13 @@ struct M2LTables {
   int* dKslot = nullptr;    // [8][ldY]: vector slot of column kk of the target stack, -1 = pad
 };
 
+// Device blocks of a context recycled across tree builds (cudaMallocAsync of the
+// 80-320 MB tree arrays costs 0.2-2 ms per call, occasionally far more)
+struct DevCache {
+  std::unordered_map<void*, size_t> live;  // block -> capacity
+  std::multimap<size_t, void*> idle;       // capacity -> free block
+};
+
 struct Timing {
   cudaEvent_t ev[32];
   int used = 0;
@@ -205,6 +214,7 @@ struct fmmgpu_ctx {
   double* d_splitk = nullptr;  // M2L phase B split-K partials
   size_t splitk_cap = 0;
   bool out_valid = false;        // d_out holds near + far of the current arrays
+  bool zero_pending = false;     // expansions / field accumulators of a new tree not yet cleared
   int* d_flag = nullptr;         // error flags
   // near plan
   bool have_lists = false;
@@ -223,6 +233,12 @@ struct fmmgpu_ctx {
   // small device -> host readbacks (counts, flags) through mapped pinned memory written
   // by a kernel, so they never queue behind bulk transfers on the copy engines
   void* h_rb = nullptr;
+  fmmgpu::DevCache cache;
+  // M2L intermediates of full levels kept across tree rebuilds: on a full level the
+  // blocks without a source are the same for every tree, so they are still zero and
+  // the 5 GB (config B leaf) clear is skipped; index = level
+  double* yt_keep[22] = {};
+  uint32_t yt_keep_n[22] = {};
   uint64_t pipe_cap = 0;
   uint64_t pipe_k = 0;
 };
@@ -235,6 +251,7 @@ void m2l_free(fmmgpu_ctx* c);
 void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, int height, int group,
                 const double* root4);
 void tree_free(fmmgpu_ctx* c);
+void yt_keep_free(fmmgpu_ctx* c);
 void lists_build(fmmgpu_ctx* c);
 void lists_free(fmmgpu_ctx* c);
 void launch_p2m(fmmgpu_ctx* c, cudaStream_t s);
@@ -250,6 +267,10 @@ extern "C" void fmmgpu_invalidate_graph(fmmgpu_ctx* c);
 namespace fmmgpu {
 void exchange_level(fmmgpu_ctx* c, int v, cudaStream_t s);
 void* scratch(fmmgpu_ctx* c, size_t bytes);
+// stream-ordered block cache: blocks freed on s are reused by later allocations on s
+void* cache_alloc(fmmgpu_ctx* c, size_t bytes, cudaStream_t s);
+void cache_free(fmmgpu_ctx* c, void* p, cudaStream_t s);  // blocks it did not allocate: cudaFreeAsync
+void cache_trim(fmmgpu_ctx* c, cudaStream_t s);            // release the idle blocks
 constexpr size_t READBACK_CAP = 64 * 1024;
 // copies `bytes` (multiple of 4, <= READBACK_CAP) of device memory to host through the
 // mapped buffer, synchronizing s; the returned host pointer is valid until the next call

@@ -45,10 +45,18 @@ int guarded(fmmgpu_ctx* c, F&& f) {
   }
 }
 
-void need_tree(const fmmgpu_ctx* c) {
+void reset_arrays(fmmgpu_ctx* c, cudaStream_t s);
+
+// Every entry point that reads or accumulates into a tree's arrays: the arrays of a
+// new tree start zeroed (GroupTree::allocate_*, geometry.cpp:199-214).
+void need_tree(fmmgpu_ctx* c) {
   if (!c->have_tree) throw Error(FMMGPU_LOGIC_ERROR, "no tree: call fmmgpu_build_tree first");
+  if (c->zero_pending) {
+    reset_arrays(c, c->s_far);
+    c->zero_pending = false;
+  }
 }
-void need_level(const fmmgpu_ctx* c, int v, int lo, int hi, const char* what) {
+void need_level(fmmgpu_ctx* c, int v, int lo, int hi, const char* what) {
   need_tree(c);
   if (v < lo || v > hi) throw Error(FMMGPU_OUT_OF_RANGE, std::string(what) + ": level out of range");
 }
@@ -203,6 +211,8 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
       partition_free(c);
       lists_free(c);
       tree_free(c);
+      yt_keep_free(c);
+      cache_trim(c, c->s_far);
     } catch (...) {
     }
     if (c->d_in) cudaFreeAsync(c->d_in, c->s_far);
@@ -419,6 +429,7 @@ extern "C" {
 // communicator stay eager.
 int fmmgpu_evaluate(fmmgpu_ctx* c) {
   return guarded(c, [&] {
+    c->zero_pending = false;  // the evaluation clears its arrays itself
     need_tree(c);
     FMM_CUDA(cudaSetDevice(c->device));
     static const bool no_graph = std::getenv("FMMGPU_NO_GRAPH") != nullptr;

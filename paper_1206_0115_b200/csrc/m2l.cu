@@ -616,6 +616,11 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
       FMM_CUDA(cudaFree(L.yt));
       L.yt = nullptr;
     }
+  for (auto& p : c->yt_keep)
+    if (p) {
+      FMM_CUDA(cudaFree(p));
+      p = nullptr;
+    }
   FMM_CUDA(cudaMalloc(&T.dM1, M1.size() * sizeof(double)));
   FMM_CUDA(cudaMalloc(&T.dM2, M2.size() * sizeof(double)));
   // per 64-row M-tile of phase A: the distinct vectors it holds (rows of one vector
@@ -657,6 +662,10 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   const Level& L = c->lv[v];
   if (L.n == 0) return;
   Level& Lm = c->lv[v];
+  if (!Lm.yt && L.full && v < 22 && c->yt_keep[v] && c->yt_keep_n[v] == L.n) {
+    Lm.yt = c->yt_keep[v];  // same full level as a previous tree: absent-source blocks still zero
+    c->yt_keep[v] = nullptr;
+  }
   if (!Lm.yt) {  // per-level compressed intermediates; zero = "no source" (see phase B)
     FMM_CUDA(cudaMallocAsync(&Lm.yt, size_t(L.n) * T.ldY * sizeof(double), s));
     FMM_CUDA(cudaMemsetAsync(Lm.yt, 0, size_t(L.n) * T.ldY * sizeof(double), s));

@@ -19,15 +19,12 @@ namespace fmmgpu {
 namespace {
 
 template <typename T>
-T* dalloc(size_t count, cudaStream_t s) {
-  void* p = nullptr;
-  if (count == 0) count = 1;
-  FMM_CUDA(cudaMallocAsync(&p, count * sizeof(T), s));
-  return static_cast<T*>(p);
+T* dalloc(fmmgpu_ctx* c, size_t count, cudaStream_t s) {
+  return static_cast<T*>(cache_alloc(c, (count ? count : 1) * sizeof(T), s));
 }
 template <typename T>
-void dfree(T*& p, cudaStream_t s) {
-  if (p) cudaFreeAsync(p, s);
+void dfree(fmmgpu_ctx* c, T*& p, cudaStream_t s) {
+  if (p) cache_free(c, p, s);
   p = nullptr;
 }
 
@@ -162,12 +159,12 @@ __global__ void k_class_offsets(const uint8_t* __restrict__ oct_sorted, uint32_t
 
 inline unsigned blocks(uint64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
-void free_level(fmmgpu::Level& L, cudaStream_t s) {
-  dfree(L.code, s); dfree(L.first_particle, s); dfree(L.particle_count, s); dfree(L.parent, s);
-  dfree(L.first_child, s); dfree(L.child_count, s); dfree(L.map, s); dfree(L.cls_cells, s);
-  dfree(L.multipole, s); dfree(L.local_own, s); dfree(L.local_down, s); dfree(L.yt, s);
-  dfree(L.far_target, s); dfree(L.far_source, s); dfree(L.far_vec, s); dfree(L.far_group_off, s);
-  dfree(L.srcA, s); dfree(L.tgtB, s);
+void free_level(fmmgpu_ctx* c, fmmgpu::Level& L, cudaStream_t s) {
+  dfree(c, L.code, s); dfree(c, L.first_particle, s); dfree(c, L.particle_count, s); dfree(c, L.parent, s);
+  dfree(c, L.first_child, s); dfree(c, L.child_count, s); dfree(c, L.map, s); dfree(c, L.cls_cells, s);
+  dfree(c, L.multipole, s); dfree(c, L.local_own, s); dfree(c, L.local_down, s); dfree(c, L.yt, s);
+  dfree(c, L.far_target, s); dfree(c, L.far_source, s); dfree(c, L.far_vec, s); dfree(c, L.far_group_off, s);
+  dfree(c, L.srcA, s); dfree(c, L.tgtB, s);
   L.far_pairs = 0;
 }
 
@@ -181,8 +178,50 @@ const void* readback(fmmgpu_ctx* c, const void* src, size_t bytes, cudaStream_t 
   const uint32_t nw = static_cast<uint32_t>(bytes / 4);
   k_copy_words<<<std::max(1u, std::min(64u, (nw + 255) / 256)), 256, 0, s>>>(static_cast<const uint32_t*>(src), nw, d);
   FMM_CUDA(cudaGetLastError());
+  static const bool tr = std::getenv("FMMGPU_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   FMM_CUDA(cudaStreamSynchronize(s));
+  if (tr) {
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 0.5) std::fprintf(stderr, "[readback] sync took %.3f ms\n", ms);
+  }
   return c->h_rb;
+}
+
+void yt_keep_free(fmmgpu_ctx* c) {
+  for (auto& p : c->yt_keep) dfree(c, p, c->s_far);
+}
+
+void* cache_alloc(fmmgpu_ctx* c, size_t bytes, cudaStream_t s) {
+  bytes = (bytes + 255) & ~size_t(255);
+  auto& C = c->cache;
+  auto it = C.idle.lower_bound(bytes);
+  if (it != C.idle.end() && it->first <= bytes + bytes / 4 + (size_t(1) << 20)) {
+    void* p = it->second;
+    C.live[p] = it->first;
+    C.idle.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  FMM_CUDA(cudaMallocAsync(&p, bytes, s));
+  C.live[p] = bytes;
+  return p;
+}
+
+void cache_free(fmmgpu_ctx* c, void* p, cudaStream_t s) {
+  auto& C = c->cache;
+  auto it = C.live.find(p);
+  if (it == C.live.end()) {
+    cudaFreeAsync(p, s);
+    return;
+  }
+  C.idle.emplace(it->second, p);
+  C.live.erase(it);
+}
+
+void cache_trim(fmmgpu_ctx* c, cudaStream_t s) {
+  for (auto& kv : c->cache.idle) cudaFreeAsync(kv.second, s);
+  c->cache.idle.clear();
 }
 
 void* scratch(fmmgpu_ctx* c, size_t bytes) {
@@ -196,10 +235,20 @@ void* scratch(fmmgpu_ctx* c, size_t bytes) {
 
 void tree_free(fmmgpu_ctx* c) {
   cudaStream_t s = c->s_far;
-  for (auto& L : c->lv) free_level(L, s);
+  for (size_t v = 0; v < c->lv.size(); ++v) {
+    auto& L = c->lv[v];
+    static const bool no_keep = std::getenv("FMMGPU_NO_YT_KEEP") != nullptr;  // A/B aid
+    if (L.yt && L.full && v < 22 && !no_keep) {
+      dfree(c, c->yt_keep[v], s);
+      c->yt_keep[v] = L.yt;
+      c->yt_keep_n[v] = L.n;
+      L.yt = nullptr;
+    }
+  }
+  for (auto& L : c->lv) free_level(c, L, s);
   c->lv.clear();
-  dfree(c->d_pw, s); dfree(c->d_id, s); dfree(c->d_inv, s); dfree(c->d_pcell, s);
-  dfree(c->d_near, s); dfree(c->d_far, s); dfree(c->d_out, s);
+  dfree(c, c->d_pw, s); dfree(c, c->d_id, s); dfree(c, c->d_inv, s); dfree(c, c->d_pcell, s);
+  dfree(c, c->d_near, s); dfree(c, c->d_far, s); dfree(c, c->d_out, s);
   c->have_tree = false;
 }
 
@@ -273,10 +322,10 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   }
 
   // keys + stable radix sort of (key, input index)
-  uint64_t* keys = dalloc<uint64_t>(n, s);
-  uint64_t* keys_sorted = dalloc<uint64_t>(n, s);
-  uint32_t* idx = dalloc<uint32_t>(n, s);
-  c->d_id = dalloc<uint32_t>(n, s);
+  uint64_t* keys = dalloc<uint64_t>(c, n, s);
+  uint64_t* keys_sorted = dalloc<uint64_t>(c, n, s);
+  uint32_t* idx = dalloc<uint32_t>(c, n, s);
+  c->d_id = dalloc<uint32_t>(c, n, s);
   k_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, c->lo[0], c->lo[1], c->lo[2], hib[0], hib[1], hib[2], cw, grid,
                                          keys, idx, c->d_flag);
   FMM_CUDA(cudaGetLastError());
@@ -285,8 +334,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
                                            std::max(1, 3 * leaf), s));
   FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
                                            std::max(1, 3 * leaf), s));
-  c->d_pw = dalloc<double4>(n, s);
-  c->d_inv = dalloc<uint32_t>(n, s);
+  c->d_pw = dalloc<double4>(c, n, s);
+  c->d_inv = dalloc<uint32_t>(c, n, s);
   k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw, c->d_inv);
   FMM_CUDA(cudaGetLastError());
 
@@ -294,24 +343,24 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   // leaf cells = runs of equal keys (geometry.cpp:113-122)
   c->lv.resize(height);
   Level& L = c->lv[leaf];
-  uint32_t* d_runs = dalloc<uint32_t>(1, s);
-  L.code = dalloc<uint64_t>(n, s);
-  L.particle_count = dalloc<uint32_t>(n, s);
+  uint32_t* d_runs = dalloc<uint32_t>(c, 1, s);
+  L.code = dalloc<uint64_t>(c, n, s);
+  L.particle_count = dalloc<uint32_t>(c, n, s);
   FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, keys_sorted, L.code, L.particle_count, d_runs, static_cast<int>(n), s));
   FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, keys_sorted, L.code, L.particle_count, d_runs, static_cast<int>(n), s));
   uint32_t runs = 0;
   runs = *static_cast<const uint32_t*>(readback(c, d_runs, 4, s));
   L.n = runs;
-  L.first_particle = dalloc<uint32_t>(runs, s);
+  L.first_particle = dalloc<uint32_t>(c, runs, s);
   FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, L.particle_count, L.first_particle, static_cast<int>(runs), s));
   FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, L.particle_count, L.first_particle, static_cast<int>(runs), s));
-  L.first_child = dalloc<uint32_t>(runs, s);
-  L.child_count = dalloc<uint32_t>(runs, s);
-  L.parent = dalloc<uint32_t>(runs, s);
+  L.first_child = dalloc<uint32_t>(c, runs, s);
+  L.child_count = dalloc<uint32_t>(c, runs, s);
+  L.parent = dalloc<uint32_t>(c, runs, s);
   FMM_CUDA(cudaMemsetAsync(L.first_child, 0, 4ull * runs, s));
   FMM_CUDA(cudaMemsetAsync(L.child_count, 0, 4ull * runs, s));
   FMM_CUDA(cudaMemsetAsync(L.parent, 0, 4ull * runs, s));
-  c->d_pcell = dalloc<uint32_t>(n, s);
+  c->d_pcell = dalloc<uint32_t>(c, n, s);
   k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs, c->d_pw,
                                                                c->d_pcell, c->d_flag);
   FMM_CUDA(cudaGetLastError());
@@ -323,28 +372,28 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     Level& C = c->lv[v + 1];
     Level& P = c->lv[v];
     k_shift3<<<blocks(C.n, 256), 256, 0, s>>>(C.code, C.n, shifted);
-    P.code = dalloc<uint64_t>(C.n, s);
-    P.child_count = dalloc<uint32_t>(C.n, s);
+    P.code = dalloc<uint64_t>(c, C.n, s);
+    P.child_count = dalloc<uint32_t>(c, C.n, s);
     FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, shifted, P.code, P.child_count, d_runs, static_cast<int>(C.n), s));
     FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, shifted, P.code, P.child_count, d_runs, static_cast<int>(C.n), s));
     runs = *static_cast<const uint32_t*>(readback(c, d_runs, 4, s));
     P.n = runs;
-    P.first_child = dalloc<uint32_t>(runs, s);
+    P.first_child = dalloc<uint32_t>(c, runs, s);
     FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, P.child_count, P.first_child, static_cast<int>(runs), s));
     FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, P.child_count, P.first_child, static_cast<int>(runs), s));
     k_set_parent<<<blocks(runs, 256), 256, 0, s>>>(P.first_child, P.child_count, runs, C.parent);
-    P.first_particle = dalloc<uint32_t>(runs, s);
-    P.particle_count = dalloc<uint32_t>(runs, s);
-    P.parent = dalloc<uint32_t>(runs, s);
+    P.first_particle = dalloc<uint32_t>(c, runs, s);
+    P.particle_count = dalloc<uint32_t>(c, runs, s);
+    P.parent = dalloc<uint32_t>(c, runs, s);
     FMM_CUDA(cudaMemsetAsync(P.first_particle, 0, 4ull * runs, s));
     FMM_CUDA(cudaMemsetAsync(P.particle_count, 0, 4ull * runs, s));
     FMM_CUDA(cudaMemsetAsync(P.parent, 0, 4ull * runs, s));
     FMM_CUDA(cudaGetLastError());
   }
-  dfree(keys, s);
-  dfree(keys_sorted, s);
-  dfree(idx, s);
-  dfree(d_runs, s);
+  dfree(c, keys, s);
+  dfree(c, keys_sorted, s);
+  dfree(c, idx, s);
+  dfree(c, d_runs, s);
 
   trace("parent levels");
   // blocks of group_size cells (geometry.cpp:155-160); lookup maps; parity classes;
@@ -357,35 +406,32 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     V.full = static_cast<uint64_t>(V.n) == (uint64_t{1} << (3 * v));
     if (!V.full && v <= DENSE_MAP_MAX_LEVEL) {
       const uint64_t cap = uint64_t{1} << (3 * v);
-      V.map = dalloc<uint32_t>(cap, s);
+      V.map = dalloc<uint32_t>(c, cap, s);
       k_fill_u32<<<blocks(cap, 256), 256, 0, s>>>(V.map, cap, NPOS);
       k_scatter_map<<<blocks(V.n, 256), 256, 0, s>>>(V.code, V.n, V.map);
     }
     if (v >= 2) {
-      uint8_t* oct = dalloc<uint8_t>(V.n, s);
-      uint8_t* oct_sorted = dalloc<uint8_t>(V.n, s);
-      uint32_t* iota = dalloc<uint32_t>(V.n, s);
-      V.cls_cells = dalloc<uint32_t>(V.n, s);
+      uint8_t* oct = dalloc<uint8_t>(c, V.n, s);
+      uint8_t* oct_sorted = dalloc<uint8_t>(c, V.n, s);
+      uint32_t* iota = dalloc<uint32_t>(c, V.n, s);
+      V.cls_cells = dalloc<uint32_t>(c, V.n, s);
       k_octant<<<blocks(V.n, 256), 256, 0, s>>>(V.code, V.n, oct, iota);
       FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, oct, oct_sorted, iota, V.cls_cells, static_cast<int>(V.n), 0, 3, s));
       FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, oct, oct_sorted, iota, V.cls_cells, static_cast<int>(V.n), 0, 3, s));
-      uint32_t* d_off = dalloc<uint32_t>(9, s);
+      uint32_t* d_off = dalloc<uint32_t>(c, 9, s);
       k_class_offsets<<<1, 32, 0, s>>>(oct_sorted, V.n, d_off);
       std::memcpy(V.cls_off, readback(c, d_off, 9 * sizeof(uint32_t), s), 9 * sizeof(uint32_t));
-      dfree(d_off, s);
-      dfree(oct, s);
-      dfree(oct_sorted, s);
-      dfree(iota, s);
+      dfree(c, d_off, s);
+      dfree(c, oct, s);
+      dfree(c, oct_sorted, s);
+      dfree(c, iota, s);
     }
     V.own0 = 0;  // unpartitioned: every cell is owned
     V.own1 = V.n;
     const size_t e = size_t(V.n) * c->ldE;
-    V.multipole = dalloc<double>(e, s);
-    V.local_own = dalloc<double>(e, s);
-    V.local_down = dalloc<double>(e, s);
-    FMM_CUDA(cudaMemsetAsync(V.multipole, 0, e * 8, s));
-    FMM_CUDA(cudaMemsetAsync(V.local_own, 0, e * 8, s));
-    FMM_CUDA(cudaMemsetAsync(V.local_down, 0, e * 8, s));
+    V.multipole = dalloc<double>(c, e, s);
+    V.local_own = dalloc<double>(c, e, s);
+    V.local_down = dalloc<double>(c, e, s);
   }
   trace("blocks+classes+expansions");
   c->part_rank = 0;
@@ -393,11 +439,22 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   c->part_align = 0;
   c->own_s0 = 0;
   c->own_s1 = n;
-  c->d_near = dalloc<double>(4 * n, s);
-  c->d_far = dalloc<double>(4 * n, s);
-  c->d_out = dalloc<double>(4 * n, s);
-  FMM_CUDA(cudaMemsetAsync(c->d_near, 0, 32 * n, s));
-  FMM_CUDA(cudaMemsetAsync(c->d_far, 0, 32 * n, s));
+  c->d_near = dalloc<double>(c, 4 * n, s);
+  c->d_far = dalloc<double>(c, 4 * n, s);
+  c->d_out = dalloc<double>(c, 4 * n, s);
+  // cleared by the first entry point that uses them (an evaluation clears them anyway)
+  c->zero_pending = true;
+  static const bool eager_zero = std::getenv("FMMGPU_EAGER_ZERO") != nullptr;  // A/B aid
+  if (eager_zero) {
+    for (auto& V : c->lv) {
+      const size_t e = size_t(V.n) * c->ldE * 8;
+      FMM_CUDA(cudaMemsetAsync(V.multipole, 0, e, s));
+      FMM_CUDA(cudaMemsetAsync(V.local_own, 0, e, s));
+      FMM_CUDA(cudaMemsetAsync(V.local_down, 0, e, s));
+    }
+    FMM_CUDA(cudaMemsetAsync(c->d_near, 0, 32 * n, s));
+    FMM_CUDA(cudaMemsetAsync(c->d_far, 0, 32 * n, s));
+  }
 
   int flag = 0;
   flag = *static_cast<const int*>(readback(c, c->d_flag, 4, s));
@@ -411,6 +468,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     throw Error(FMMGPU_DOMAIN_ERROR, "GroupTree: coincident particles");
   }
   c->have_tree = true;
+  cache_trim(c, s);  // blocks of the previous tree this one did not reuse
 }
 
 }  // namespace fmmgpu

@@ -26,7 +26,10 @@ def t(f, reps=5):
     for _ in range(reps):
         f()
     torch.cuda.synchronize()
-    return (time.perf_counter() - t0) / reps * 1e3
+    ms = (time.perf_counter() - t0) / reps * 1e3
+    free, total = torch.cuda.mem_get_info()
+    print(f"    [used {(total - free) / 1e9:.1f} GB]", end=" ")
+    return ms
 
 
 print("build_tree host  %.2f ms" % t(lambda: c._check(lib.fmmgpu_build_tree(c.h, c_void_p(pin.data_ptr()), n, 0, h, 250, None))))

@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include "common.cuh"
@@ -228,6 +229,7 @@ struct GemmArgs {
   double* local;          // phase B output (local_own)
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
   int msplit;             // phase A M-split factor (coarse levels)
+  int late_load;          // phase A: refill the ring after the slice's DMMAs
   double* part;           // phase B split-K partials [ksplit][ncells][ldE]
   uint32_t ncells;
   int l3;
@@ -450,8 +452,12 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   for (int t = 0; t < TOTAL; ++t) {
     cp_wait<PA_ST - 2>();
     __syncthreads();
-    if (t + PA_ST - 1 < TOTAL) load_next();
-    cp_commit();
+    // late_load: the ring refill is issued after this slice's DMMAs, so the registers of
+    // its cp.async operands are not overwritten (WAR stall) right after the issue
+    if (!g.late_load) {
+      if (t + PA_ST - 1 < TOTAL) load_next();
+      cp_commit();
+    }
     uint32_t* tg = tgt + (mt & 1) * g.vtMax * BN;
     if (kt == 0) {
 #pragma unroll
@@ -506,6 +512,10 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
       }
+    }
+    if (g.late_load) {
+      if (t + PA_ST - 1 < TOTAL) load_next();
+      cp_commit();
     }
     if (++stage == PA_ST) stage = 0;
     if (++kt == KT) { kt = 0; ++mt; }
@@ -578,7 +588,14 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   }
   T.R = R;
   T.ldY = round_up(R, 32);
-  T.bmA = c->ldE <= 128 ? 64 : 128;
+  // FMMGPU_M2L_A (tuning experiments, l <= 5): 0 = 64-row tiles x 64 columns, 4 stages
+  // (default); 1 = 128 x 64, 2 stages (32x32 warp tiles); 2 = 128 x 32, 3 stages
+  static const int a_variant = [] {
+    const char* e = std::getenv("FMMGPU_M2L_A");
+    return e ? std::atoi(e) : 0;
+  }();
+  T.bmA = c->ldE <= 128 && a_variant == 0 ? 64 : 128;
+  T.a_variant = c->ldE <= 128 ? a_variant : 0;
   T.rowsA = round_up(R, T.bmA);
   T.rowsB = round_up(n3, B_BM);
   std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
@@ -695,11 +712,18 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.lda = c->ldE;
     g.a_class_stride = size_t(T.rowsA) * c->ldE;
     g.K = c->ldE;
+    static const int late = [] {
+      const char* e = std::getenv("FMMGPU_M2L_LATE");
+      return e ? std::atoi(e) : 0;  // measured: 12.3 vs 12.0 ms at the config-B leaf
+    }();
+    g.late_load = late;
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
     auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST) {
       const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * PA_SPAD) +
                           sizeof(uint32_t) * 2 * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      static const bool tr = std::getenv("FMMGPU_TRACE") != nullptr;
+      if (tr) std::fprintf(stderr, "[m2l] phase A level %d: BM %d BN %d stages %d smem %zu vtMax %d\n", v, PA_BM, bn, PA_ST, smem, T.vtMax);
       // M-split so coarse levels still put >= 2 CTAs on every SM
       const uint32_t ncols = 8u * ((maxcls + bn - 1) / bn);
       const int mtiles = T.rowsA / PA_BM;
@@ -711,6 +735,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       FMM_CUDA(cudaGetLastError());
     };
     if (T.bmA == 64) launch(k_m2l_phase_a<64, 4, 64, 2, 4>, 64, 64, 4);
+    else if (T.a_variant == 1) launch(k_m2l_phase_a<128, 2, 64, 4, 2>, 64, 128, 2);
+    else if (T.a_variant == 2) launch(k_m2l_phase_a<128, 3, 32, 4, 2>, 32, 128, 3);
     else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
   }
   g.cls_cells = L.tgtB ? L.tgtB : L.cls_cells;

@@ -25,7 +25,7 @@
 //    into HBM per chunk, still single-writer), and shallow trees with too few parents
 //    for the persistent grid split a parent's units over several CTAs.
 //
-// Per interaction: 3 DADD (d) + 3 DP (r^2) + MUFU.RSQ64H and 4 DP (rsqrt_nr)
+// Per interaction: 3 DADD (d) + 3 DP (r^2) + MUFU.RSQ64H and 5 DP (Newton)
 // + 1 DMUL (w/r) + 1 DADD (pot) + 2 DMUL (w/r^3) + 3 DFMA (force) = 18 DP ops.
 #include <cstdlib>
 
@@ -55,14 +55,22 @@ struct P2PArgs {
 // w/r and w/r^3 are +0 and the accumulators are unchanged bit for bit).
 __device__ __forceinline__ double4 dummy_source() { return make_double4(1e100, 1e100, 1e100, 0.0); }
 
+// One interaction; SELF: the source run may hold the target itself. i == j gives
+// r^2 = +0 exactly (coincident distinct particles are rejected at build), and an
+// integer test on r^2's high word keeps that select off the FP64 pipe; the other 8
+// of a target's 9 runs skip it. 1/sqrt is the MUFU.RSQ64H seed and one third-order
+// Newton step (rsqrt_nr, common.cuh) with the 0.375 coefficient held in a register.
+template <bool SELF>
 __device__ __forceinline__ void interact(const double xi, const double yi, const double zi, const double4 pj,
-                                         double& pot, double& fx, double& fy, double& fz) {
+                                         const double c375, double& pot, double& fx, double& fy, double& fz) {
   const double dx = xi - pj.x, dy = yi - pj.y, dz = zi - pj.z;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-  double inv = rsqrt_nr(r2);
-  // i == j gives r^2 = +0 exactly (coincident distinct particles are rejected at
-  // build): an integer test on the high word keeps the select off the FP64 pipe.
-  inv = __double2hiint(r2) != 0 ? inv : 0.0;
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  const double t = r2 * y;
+  const double e = fma(-t, y, 1.0);
+  double inv = fma(y, e * fma(e, c375, 0.5), y);
+  if constexpr (SELF) inv = __double2hiint(r2) != 0 ? inv : 0.0;
   const double winv = pj.w * inv;
   pot += winv;
   const double s3 = winv * (inv * inv);
@@ -83,6 +91,10 @@ struct Neigh {
   uint32_t voff[65];     // virtual offsets of the 64 positions (prefix sum of padded counts)
   uint32_t full_off[9];  // prefix over the 8 children of their full 32-target passes
   uint32_t nunits;
+  // the partial last pass of child w (m = count % 32 targets) is cut into chunks of
+  // 16, 8, 4, 2, 1 targets (the binary digits of m); a chunk of 2^b targets splits the
+  // sources 32 / 2^b ways, so every lane works. Entries (w << 8) | b, largest first.
+  uint16_t part[40];
 };
 
 // Counts and padded offsets of the 64 leaf positions around parent pc, by one warp
@@ -117,11 +129,12 @@ __device__ void neigh_meta(const P2PArgs& a, const int pc[3], Neigh& nb, int lan
     uint32_t acc = 0, npart = 0;
     for (int w = 0; w < 8; ++w) {
       nb.full_off[w] = acc;
-      const uint32_t c = nb.cnt[child_pos(w)];
-      acc += c / 32u;
-      npart += (c % 32u) != 0;
+      acc += nb.cnt[child_pos(w)] / 32u;
     }
     nb.full_off[8] = acc;
+    for (int b = 4; b >= 0; --b)
+      for (int w = 0; w < 8; ++w)
+        if ((nb.cnt[child_pos(w)] >> b) & 1u) nb.part[npart++] = static_cast<uint16_t>((w << 8) | b);
     nb.nunits = acc + npart;
   }
   __syncwarp();
@@ -140,67 +153,60 @@ __device__ __forceinline__ void locate(const Neigh& nb, uint32_t v, uint32_t& po
 
 // One work unit u over the staged sources [base, base + clen) of the virtual range;
 // src[0..clen) are the staged sources, src[P2P_CAP..+4) a group of zero sources.
-template <int G>
 __device__ void p2p_unit(const P2PArgs& a, const Neigh& nb, const double4* src, uint32_t base, uint32_t clen,
                          uint32_t u, double (*red)[32], int lane) {
   const uint32_t nfull = nb.full_off[8];
-  // decode unit -> (child octant w, first target t0)
+  // decode unit -> (child octant w, first target t0, m targets)
   int w = 0;
-  uint32_t t0 = 0;
+  uint32_t t0 = 0, m = 32;
   if (u < nfull) {
     while (nb.full_off[w + 1] <= u) ++w;
     t0 = 32u * (u - nb.full_off[w]);
   } else {
-    uint32_t k = u - nfull;
-    for (w = 0; w < 8; ++w) {
-      if (nb.cnt[child_pos(w)] % 32u == 0) continue;
-      if (k == 0) break;
-      --k;
-    }
-    t0 = 32u * (nb.full_off[w + 1] - nb.full_off[w]);
+    const uint32_t e = nb.part[u - nfull];
+    w = static_cast<int>(e >> 8);
+    const int b = static_cast<int>(e & 0xff);
+    const uint32_t rem = nb.cnt[child_pos(w)] % 32u;
+    t0 = 32u * (nb.full_off[w + 1] - nb.full_off[w]) + ((rem >> (b + 1)) << (b + 1));
+    m = 1u << b;
   }
   const int ca = (w >> 2) & 1, cb = (w >> 1) & 1, cc = w & 1;
   const int tpos = child_pos(w);
-  const uint32_t nT = nb.cnt[tpos];
   const uint32_t tfirst = nb.first[tpos];
-  const uint32_t m = min(32u, nT - t0);
-  const uint32_t S = 32u / m;
+  const uint32_t S = 32u / m;  // source splits: lanes split * m + lt, split < S
   const uint32_t lt = lane % m, split = lane / m;
-  const bool active = split < S;
   const uint64_t tg = uint64_t(tfirst) + t0 + lt;
   const double4 xi = a.pw[tg];
+  double c375 = 0.375;
+  asm volatile("" : "+d"(c375));  // opaque: stays in a register instead of being rebuilt per group
   double pot = 0, fx = 0, fy = 0, fz = 0;
-  if (active) {
-    // the 27 neighbour positions as 9 runs of 3 consecutive positions (qc = cc..cc+2),
-    // whose padded segments are contiguous in shared memory
+  // the 27 neighbour positions as 9 runs of 3 consecutive positions (qc = cc..cc+2),
+  // whose padded segments are contiguous in shared memory; run 4 holds the target's
+  // own leaf
 #pragma unroll 1
-    for (int q = 0; q < 9; ++q) {
-      const int pos = ((ca + q / 3) << 4) | ((cb + q % 3) << 2) | cc;
-      // intersection of the run's virtual range with this chunk, chunk-relative
-      // (segments are padded to groups of 4 and chunks are multiples of 4)
-      const uint32_t v0 = max(nb.voff[pos], base), v1 = min(nb.voff[pos + 3], base + clen);
-      const int g1 = static_cast<int>(v1 - base) >> 2;
-      const int gs = static_cast<int>(S);
-      for (int g = (static_cast<int>(v0 - base) >> 2) + static_cast<int>(split); g < g1; g += G * gs) {
-        const double4* sj = src + 4 * g;
+  for (int q = 0; q < 9; ++q) {
+    const int pos = ((ca + q / 3) << 4) | ((cb + q % 3) << 2) | cc;
+    // intersection of the run's virtual range with this chunk, chunk-relative
+    // (segments are padded to groups of 4 and chunks are multiples of 4)
+    const uint32_t v0 = max(nb.voff[pos], base), v1 = min(nb.voff[pos + 3], base + clen);
+    const double4* sj = src + 4 * ((static_cast<int>(v0 - base) >> 2) + static_cast<int>(split));
+    const double4* se = src + 4 * (static_cast<int>(v1 - base) >> 2);
+    const int step = 4 * static_cast<int>(S);
+    if (q == 4) {
+      for (; sj < se; sj += step) {
         const double4 p0 = sj[0], p1 = sj[1], p2 = sj[2], p3 = sj[3];
-        if constexpr (G == 2) {
-          const double4* sk = (g + gs < g1) ? src + 4 * (g + gs) : src + P2P_CAP;
-          const double4 p4 = sk[0], p5 = sk[1], p6 = sk[2], p7 = sk[3];
-          interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p4, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p5, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p6, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p7, pot, fx, fy, fz);
-        } else {
-          interact(xi.x, xi.y, xi.z, p0, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p1, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p2, pot, fx, fy, fz);
-          interact(xi.x, xi.y, xi.z, p3, pot, fx, fy, fz);
-        }
+        interact<true>(xi.x, xi.y, xi.z, p0, c375, pot, fx, fy, fz);
+        interact<true>(xi.x, xi.y, xi.z, p1, c375, pot, fx, fy, fz);
+        interact<true>(xi.x, xi.y, xi.z, p2, c375, pot, fx, fy, fz);
+        interact<true>(xi.x, xi.y, xi.z, p3, c375, pot, fx, fy, fz);
+      }
+    } else {
+      for (; sj < se; sj += step) {
+        const double4 p0 = sj[0], p1 = sj[1], p2 = sj[2], p3 = sj[3];
+        interact<false>(xi.x, xi.y, xi.z, p0, c375, pot, fx, fy, fz);
+        interact<false>(xi.x, xi.y, xi.z, p1, c375, pot, fx, fy, fz);
+        interact<false>(xi.x, xi.y, xi.z, p2, c375, pot, fx, fy, fz);
+        interact<false>(xi.x, xi.y, xi.z, p3, c375, pot, fx, fy, fz);
       }
     }
   }
@@ -239,8 +245,8 @@ struct P2PSmem {
   uint32_t next_unit;  // work-unit queue head (per chunk)
 };
 
-// WARPS warps per CTA pull the work units; G groups of 4 sources per inner iteration.
-template <int WARPS, int G>
+// WARPS warps per CTA pull the work units.
+template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
   constexpr int P2P_THREADS = WARPS * 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
       if (lane == 0) u = atomicAdd(&sm.next_unit, 1u);
       u = __shfl_sync(0xffffffffu, u, 0) * a.usplit + ysplit;
       if (u >= nunits) break;
-      p2p_unit<G>(a, sm.nb, sm.src, base, clen, u, sm.red[warp], lane);
+      p2p_unit(a, sm.nb, sm.src, base, clen, u, sm.red[warp], lane);
     }
   }
 }
@@ -329,7 +335,7 @@ __device__ void flow_stage(const P2PArgs& a, FlowSlot& s, int it, int lane) {
   if (lane == 0) *reinterpret_cast<volatile int*>(&s.ready) = it;
 }
 
-template <int WARPS, int G>
+template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_p2p_flow(const P2PArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FlowSmem<WARPS>& sm = *reinterpret_cast<FlowSmem<WARPS>*>(smem_raw);
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_p2p_flow(const P2PArgs a) {
       if (lane == 0) u = atomicAdd(&s.next_unit, 1u);
       u = __shfl_sync(0xffffffffu, u, 0);
       if (u >= nunits) break;
-      p2p_unit<G>(a, s.nb, s.src, 0, s.nb.voff[64], u, sm.red[warp], lane);
+      p2p_unit(a, s.nb, s.src, 0, s.nb.voff[64], u, sm.red[warp], lane);
     }
     // the last warp to leave this parent restages the slot with item it + 2
     uint32_t d = 0;
@@ -379,11 +385,12 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
     FMM_CUDA(cudaGetLastError());
     ++c->launches;
   };
-  // FMMGPU_P2P_VARIANT (tuning experiments): 0 = k_p2p 12 warps x 1 group (default),
-  // 1 = 8 x 2 groups, 2 = 16 x 1, 3 = 8 x 1; 6 / 7 = persistent k_p2p_flow with 16 / 24
-  // warps (+ chunked k_p2p for oversized neighbourhoods). Config B: 13.7 / 13.6 / - / -
-  // / 15.0 / 16.8 ms: with at most one parent of look-ahead the persistent warps idle
-  // at the same unit-granularity tails, with fewer warps per SM to hide latency.
+  // FMMGPU_P2P_VARIANT (tuning experiments): 0 = k_p2p 12 warps (default), 2 = 16 warps,
+  // 3 = 8 warps; 6 / 7 = persistent k_p2p_flow with 16 / 24 warps (+ chunked k_p2p for
+  // oversized neighbourhoods). Config B, before the chunked partial passes: 13.7 / 13.9 /
+  // 13.8 / 15.0 / 16.8 ms: with at most one parent of look-ahead the persistent warps
+  // idle at the same unit-granularity tails, with fewer warps per SM to hide latency.
+  // (8 sources per iteration and split accumulators were also measured slower.)
   static const int variant = [] {
     const char* e = std::getenv("FMMGPU_P2P_VARIANT");
     return e ? std::atoi(e) : 0;
@@ -393,10 +400,10 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const bool flow = (variant == 6 || variant == 7) && np >= 2u * static_cast<uint32_t>(sms);
   if (flow) {
     const unsigned grid = static_cast<unsigned>(sms);
-    if (variant == 7) run(k_p2p_flow<24, 1>, 24, static_cast<int>(sizeof(FlowSmem<24>)), grid);
-    else run(k_p2p_flow<16, 1>, 16, static_cast<int>(sizeof(FlowSmem<16>)), grid);
+    if (variant == 7) run(k_p2p_flow<24>, 24, static_cast<int>(sizeof(FlowSmem<24>)), grid);
+    else run(k_p2p_flow<16>, 16, static_cast<int>(sizeof(FlowSmem<16>)), grid);
     a.only_big = 1;  // the (rare) oversized neighbourhoods, chunked
-    run(k_p2p<12, 1>, 12, static_cast<int>(sizeof(P2PSmem<12>)), np);
+    run(k_p2p<12>, 12, static_cast<int>(sizeof(P2PSmem<12>)), np);
     return;
   }
   // few parents (shallow trees, big leaves): several CTAs per parent share its units
@@ -406,10 +413,9 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   a.usplit = usplit;
   const unsigned grid = np * usplit;
   switch (variant) {
-    case 1: run(k_p2p<8, 2>, 8, static_cast<int>(sizeof(P2PSmem<8>)), grid); break;
-    case 2: run(k_p2p<16, 1>, 16, static_cast<int>(sizeof(P2PSmem<16>)), grid); break;
-    case 3: run(k_p2p<8, 1>, 8, static_cast<int>(sizeof(P2PSmem<8>)), grid); break;
-    default: run(k_p2p<12, 1>, 12, static_cast<int>(sizeof(P2PSmem<12>)), grid); break;
+    case 2: run(k_p2p<16>, 16, static_cast<int>(sizeof(P2PSmem<16>)), grid); break;
+    case 3: run(k_p2p<8>, 8, static_cast<int>(sizeof(P2PSmem<8>)), grid); break;
+    default: run(k_p2p<12>, 12, static_cast<int>(sizeof(P2PSmem<12>)), grid); break;
   }
 }
 

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/pytest_gpu.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python tools/p2p_variants.py > gpurun_out/p2p_variants.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x --timeout 300 -k "p2p or full_evaluation or determin" > gpurun_out/pytest_p2p.log 2>&1

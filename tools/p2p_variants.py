@@ -20,7 +20,7 @@ if len(sys.argv) > 1:
     np.save(f"/tmp/p2p_v{sys.argv[1]}.npy", np.stack(f))
     print(f"variant {sys.argv[1]}: {ms:.3f} ms", flush=True)
 else:
-    VARIANTS = [0, 1, 6, 7]  # 0 = k_p2p 12 warps (default), 6 / 7 = persistent 16 / 24 warps
+    VARIANTS = [0, 2, 3]  # 0 = k_p2p 12 warps (default), 2 = 16 warps, 3 = 8 warps
     for v in VARIANTS:
         env = dict(os.environ, FMMGPU_P2P_VARIANT=str(v))
         subprocess.run([sys.executable, __file__, str(v)], env=env, check=True)

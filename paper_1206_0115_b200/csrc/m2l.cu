@@ -230,6 +230,9 @@ struct GemmArgs {
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
   int msplit;             // phase A M-split factor (coarse levels)
   int late_load;          // phase A: refill the ring after the slice's DMMAs
+  int dbg;                // FMMGPU_M2L_DEBUG (timing experiments only, wrong results): 1 no scatter,
+                          // 2 no lookups, 4 scatter stores made contiguous (config-B leaf: 10.7 / - / 11.2
+                          // vs 11.9 ms for phase A + B)
   double* part;           // phase B split-K partials [ksplit][ncells][ldE]
   uint32_t ncells;
   int l3;
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
       slot_e0 = tid < g.vtMax * BN ? __ldg(vec + tid / BN) : -1;
       slot_e1 = tid + PA_THREADS < g.vtMax * BN ? __ldg(vec + (tid + PA_THREADS) / BN) : -1;
     }
-    if (kt == kt_fill) {
+    if (kt == kt_fill && !(g.dbg & 2)) {
       // one lookup per (vector, source column) of this M-tile: target = source - v
       const int* vec = g.tileVec + (size_t(cls) * MTILES + mt) * g.vtMax;
       int u = 0;
@@ -499,14 +502,20 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
       // scatter block v of source s to target s - v, target-side column info.x
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        if (rowinfo[i].x >= 0) {
+        if (rowinfo[i].x >= 0 && !(g.dbg & 1)) {
           const uint32_t* trow = tg + rowinfo[i].z * BN;
 #pragma unroll
           for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const uint32_t tcell = trow[wn * WTN + j * 8 + 2 * tq + e];
-              if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + rowinfo[i].y] = acc[i][j][e];
+              if (g.dbg & 4) {  // timing experiment: same stores, contiguous per CTA tile
+                if (tcell != NPOS)
+                  g.Yt[(size_t(blockIdx.y) * gridDim.x + blockIdx.x) * (PA_BM * BN) +
+                       size_t(wm * WTM + i * 8 + gq) * BN + wn * WTN + j * 8 + 2 * tq + e] = acc[i][j][e];
+              } else if (tcell != NPOS) {
+                g.Yt[size_t(tcell) * g.ldY + rowinfo[i].y] = acc[i][j][e];
+              }
             }
         }
 #pragma unroll
@@ -717,6 +726,11 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       return e ? std::atoi(e) : 0;  // measured: 12.3 vs 12.0 ms at the config-B leaf
     }();
     g.late_load = late;
+    static const int dbg = [] {
+      const char* e = std::getenv("FMMGPU_M2L_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    g.dbg = dbg;
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
     auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST) {
       const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * PA_SPAD) +

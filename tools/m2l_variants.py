@@ -14,6 +14,8 @@ if len(sys.argv) > 1:
     c.build_tree(xyzw, 7)
     c.time_operator("M2L", 6, 1)
     leaf = c.time_operator("M2L", 6, 5)
+    import ctypes
+    ms = ctypes.c_double()
     allv = c.time_operator("M2L", -1, 3)
     c.evaluate()
     c.synchronize()
@@ -21,10 +23,10 @@ if len(sys.argv) > 1:
     print(f"variant {sys.argv[1]}: leaf {leaf:.3f} ms, all levels {allv:.3f} ms", flush=True)
 else:
     # (FMMGPU_M2L_A, FMMGPU_M2L_LATE)
-    SETS = {0: ("0", "0"), 1: ("0", "1"), 2: ("2", "1")}
+    SETS = {0: ("0", "0", "0"), 1: ("0", "0", "1"), 4: ("0", "0", "4")}
     VARIANTS = list(SETS)
     for v in VARIANTS:
-        env = dict(os.environ, FMMGPU_M2L_A=SETS[v][0], FMMGPU_M2L_LATE=SETS[v][1])
+        env = dict(os.environ, FMMGPU_M2L_A=SETS[v][0], FMMGPU_M2L_LATE=SETS[v][1], FMMGPU_M2L_DEBUG=SETS[v][2])
         subprocess.run([sys.executable, __file__, str(v)], env=env, check=True)
     import numpy as np
     base = np.load(f"/tmp/m2l_v{VARIANTS[0]}.npy")

@@ -11,6 +11,8 @@
 //        sum_{n1,n2} (Sx Sy) * sum_{n3} L Sz (and the three gradient variants)
 //        (chebyshev.cpp:138-179, bench.cpp:317-336).
 // Templated on the order so every loop is unrolled with compile-time bounds.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fmmgpu {
@@ -145,6 +147,86 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
           const double ab = sw[j][n1] * sw[j][L + n2];
 #pragma unroll
           for (int n = 0; n < L; ++n) acc[i][n] = fma(ab, sw[j][2 * L + n], acc[i][n]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int i = 0; i < PP; ++i) {
+    const int pr = lane + 32 * i;
+    if (pr < L * L)
+#pragma unroll
+      for (int n = 0; n < L; ++n) out[pr * L + n] = acc[i][n];
+  }
+}
+
+// P2M, warp per leaf cell, interpolation vectors stored particle-minor
+// (sv[component][particle]) so one LDS.128 returns a component for two particles:
+// per particle pair a lane reads a[n1], b[n2] (one LDS.128 each) and the l values
+// c[0..l) (l LDS.128, broadcast) for 2 (l + 1) DP ops -- half the shared-memory
+// instructions per FMA of k_p2m_warp, which is MIO-throttle bound. Same particle order
+// and product order as k_p2m_warp (the reference's wx, wxy, out += wxy sz), so the
+// results are identical. Chunks of 32 particles; a chunk's odd tail is zero-padded.
+template <int L>
+__global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp2(LeafArgs a) {
+  constexpr int PP = (L * L + 31) / 32;  // (n1, n2) pairs per lane
+  __shared__ double tn[L * (L - 1) + 1];
+  __shared__ __align__(16) double SV[P2M_WARPS][3 * L][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < L * (L - 1); i += P2M_THREADS) tn[i] = a.tn[i];
+  __syncthreads();
+  const uint32_t c = a.cell0 + blockIdx.x * P2M_WARPS + warp;
+  if (c >= a.ncells) return;
+  double ctr[3];
+  cell_center(a.geo, a.code[c], ctr);
+  const uint32_t first = a.first[c], cnt = a.count[c];
+  double* out = a.expansion + size_t(c) * a.ldE;
+  const double4 zero4 = make_double4(0, 0, 0, 0);
+  const double4 q0 = lane < cnt ? a.pw[first + lane] : zero4;
+  const double4 q1 = lane + 32 < cnt ? a.pw[first + 32 + lane] : zero4;
+  double acc[PP][L];
+#pragma unroll
+  for (int i = 0; i < PP; ++i)
+#pragma unroll
+    for (int n = 0; n < L; ++n) acc[i][n] = (lane + 32 * i < L * L) ? out[(lane + 32 * i) * L + n] : 0.0;
+  double(*sv)[32] = SV[warp];
+  for (uint32_t base = 0; base < cnt; base += 32) {
+    double s[L];
+    if (base + lane < cnt) {
+      const double4 p = base == 0 ? q0 : base == 32 ? q1 : a.pw[first + base + lane];
+      eval_all<L>(tn, (p.x - ctr[0]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) sv[m][lane] = p.w * s[m];
+      eval_all<L>(tn, (p.y - ctr[1]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) sv[L + m][lane] = s[m];
+      eval_all<L>(tn, (p.z - ctr[2]) * a.geo.inv, s);
+#pragma unroll
+      for (int m = 0; m < L; ++m) sv[2 * L + m][lane] = s[m];
+    } else {
+#pragma unroll
+      for (int m = 0; m < 3 * L; ++m) sv[m][lane] = 0.0;
+    }
+    __syncwarp();
+    const int m2 = static_cast<int>(min(32u, cnt - base) + 1) & ~1;  // particle pairs
+#pragma unroll
+    for (int i = 0; i < PP; ++i) {
+      const int pr = lane + 32 * i;
+      if (pr < L * L) {
+        const int n1 = pr / L, n2 = pr % L;
+        for (int j = 0; j < m2; j += 2) {
+          const double2 av = *reinterpret_cast<const double2*>(&sv[n1][j]);
+          const double2 bv = *reinterpret_cast<const double2*>(&sv[L + n2][j]);
+          double2 cv[L];
+#pragma unroll
+          for (int n = 0; n < L; ++n) cv[n] = *reinterpret_cast<const double2*>(&sv[2 * L + n][j]);
+          const double ab0 = av.x * bv.x;
+#pragma unroll
+          for (int n = 0; n < L; ++n) acc[i][n] = fma(ab0, cv[n].x, acc[i][n]);
+          const double ab1 = av.y * bv.y;
+#pragma unroll
+          for (int n = 0; n < L; ++n) acc[i][n] = fma(ab1, cv[n].y, acc[i][n]);
         }
       }
     }
@@ -468,7 +550,13 @@ struct RunP2M {
   static void run(const LeafArgs& a, cudaStream_t s) {
     const uint32_t nc = a.ncells - a.cell0;
     if (!nc) return;
-    k_p2m_warp<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
+    // FMMGPU_P2M=1: the row-major k_p2m_warp (A/B timing)
+    static const bool rowmajor = [] {
+      const char* e = std::getenv("FMMGPU_P2M");
+      return e && std::atoi(e) == 1;
+    }();
+    if (rowmajor) k_p2m_warp<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
+    else k_p2m_warp2<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
   }
 };
 template <int L>

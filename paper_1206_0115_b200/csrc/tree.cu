@@ -69,9 +69,10 @@ __global__ void k_minmax_partial(const double4* __restrict__ p, uint64_t n, doub
 }
 
 // Morton key per particle (geometry.cpp:76-94): u = floor((c - lo) / cw), clamped.
+template <typename K>  // uint32_t when 3 * leaf <= 32 (height <= 11): half the sort traffic
 __global__ void k_keys(const double4* __restrict__ p, uint64_t n, double lo0, double lo1, double lo2,
                        double hi0, double hi1, double hi2, double cw, uint32_t grid,
-                       uint64_t* __restrict__ keys, uint32_t* __restrict__ idx, int* __restrict__ flag) {
+                       K* __restrict__ keys, uint32_t* __restrict__ idx, int* __restrict__ flag) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const double4 q = p[i];
@@ -84,7 +85,7 @@ __global__ void k_keys(const double4* __restrict__ p, uint64_t n, double lo0, do
     if (u >= grid) u = grid - 1;
     ijk[a] = static_cast<uint32_t>(u);
   }
-  keys[i] = morton(ijk[0], ijk[1], ijk[2]);
+  keys[i] = static_cast<K>(morton(ijk[0], ijk[1], ijk[2]));
   idx[i] = static_cast<uint32_t>(i);
 }
 
@@ -321,33 +322,48 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     hib[a] = c->lo[a] + root[3];
   }
 
-  // keys + stable radix sort of (key, input index)
-  uint64_t* keys = dalloc<uint64_t>(c, n, s);
-  uint64_t* keys_sorted = dalloc<uint64_t>(c, n, s);
-  uint32_t* idx = dalloc<uint32_t>(c, n, s);
+  // keys + stable radix sort of (key, input index); leaf cells = runs of equal keys
+  // (geometry.cpp:113-122)
   c->d_id = dalloc<uint32_t>(c, n, s);
-  k_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, c->lo[0], c->lo[1], c->lo[2], hib[0], hib[1], hib[2], cw, grid,
-                                         keys, idx, c->d_flag);
-  FMM_CUDA(cudaGetLastError());
-  size_t tb = 0;
-  FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
-                                           std::max(1, 3 * leaf), s));
-  FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
-                                           std::max(1, 3 * leaf), s));
-  c->d_pw = dalloc<double4>(c, n, s);
-  c->d_inv = dalloc<uint32_t>(c, n, s);
-  k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw, c->d_inv);
-  FMM_CUDA(cudaGetLastError());
-
-  trace("keys+sort+permute");
-  // leaf cells = runs of equal keys (geometry.cpp:113-122)
+  uint32_t* idx = dalloc<uint32_t>(c, n, s);
   c->lv.resize(height);
   Level& L = c->lv[leaf];
   uint32_t* d_runs = dalloc<uint32_t>(c, 1, s);
   L.code = dalloc<uint64_t>(c, n, s);
   L.particle_count = dalloc<uint32_t>(c, n, s);
-  FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, keys_sorted, L.code, L.particle_count, d_runs, static_cast<int>(n), s));
-  FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, keys_sorted, L.code, L.particle_count, d_runs, static_cast<int>(n), s));
+  size_t tb = 0;
+  auto sort_and_encode = [&](auto* keys, auto* keys_sorted) {
+    k_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, c->lo[0], c->lo[1], c->lo[2], hib[0], hib[1], hib[2], cw, grid,
+                                           keys, idx, c->d_flag);
+    FMM_CUDA(cudaGetLastError());
+    FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
+                                             std::max(1, 3 * leaf), s));
+    FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n),
+                                             0, std::max(1, 3 * leaf), s));
+    c->d_pw = dalloc<double4>(c, n, s);
+    c->d_inv = dalloc<uint32_t>(c, n, s);
+    k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw, c->d_inv);
+    FMM_CUDA(cudaGetLastError());
+    trace("keys+sort+permute");
+    FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, keys_sorted, L.code, L.particle_count, d_runs,
+                                                static_cast<int>(n), s));
+    FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, keys_sorted, L.code, L.particle_count, d_runs,
+                                                static_cast<int>(n), s));
+  };
+  uint64_t* keys64 = nullptr;  // kept: the parent-level loop reuses it as scratch
+  if (3 * leaf <= 32) {
+    uint32_t* k32 = dalloc<uint32_t>(c, n, s);
+    uint32_t* k32s = dalloc<uint32_t>(c, n, s);
+    sort_and_encode(k32, k32s);
+    dfree(c, k32, s);
+    dfree(c, k32s, s);
+    keys64 = dalloc<uint64_t>(c, n, s);
+  } else {
+    keys64 = dalloc<uint64_t>(c, n, s);
+    uint64_t* k64s = dalloc<uint64_t>(c, n, s);
+    sort_and_encode(keys64, k64s);
+    dfree(c, k64s, s);
+  }
   uint32_t runs = 0;
   runs = *static_cast<const uint32_t*>(readback(c, d_runs, 4, s));
   L.n = runs;
@@ -367,7 +383,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
 
   trace("leaf level");
   // parent levels by code >> 3 (geometry.cpp:138-153)
-  uint64_t* shifted = keys;  // reuse
+  uint64_t* shifted = keys64;  // reuse
   for (int v = leaf - 1; v >= 0; --v) {
     Level& C = c->lv[v + 1];
     Level& P = c->lv[v];
@@ -390,8 +406,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     FMM_CUDA(cudaMemsetAsync(P.parent, 0, 4ull * runs, s));
     FMM_CUDA(cudaGetLastError());
   }
-  dfree(c, keys, s);
-  dfree(c, keys_sorted, s);
+  dfree(c, keys64, s);
   dfree(c, idx, s);
   dfree(c, d_runs, s);
 

@@ -30,7 +30,7 @@ KIND_OF = {"k_p2p": "P2P", "k_m2l_phase_a": "M2L_A", "k_m2l_phase_b": "M2L_B", "
 
 def short(name):
     n = name.replace("fmmgpu::<unnamed>::", "").replace("(anonymous namespace)::", "")
-    return n.split("(")[0].replace("void ", "")
+    return n.split("(")[0].replace("void ", "").rsplit("::", 1)[-1]
 
 
 # ---- launch list

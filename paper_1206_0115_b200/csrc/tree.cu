@@ -117,6 +117,48 @@ __global__ void k_leaf_scan(const uint32_t* __restrict__ first, const uint32_t* 
   }
 }
 
+// Large leaves (mean > 64 particles, e.g. config D's surface cloud): the pairwise
+// per-leaf scan is O(m^2). Instead every particle gets its Morton key at level 21
+// (equal positions => equal keys), the keys are sorted, and runs of equal keys (tiny:
+// distinct positions share a key only within 2^-21 of the root width) are compared
+// pairwise on the exact positions. Same answer as geometry.cpp:126-136 (equal
+// positions always share a leaf).
+__global__ void k_leaf_cells(const uint32_t* __restrict__ first, const uint32_t* __restrict__ count, uint32_t ncells,
+                             uint32_t* __restrict__ pcell) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ncells) return;
+  const uint32_t f = first[warp], m = count[warp];
+  for (uint32_t a = lane; a < m; a += 32) pcell[f + a] = warp;
+}
+__global__ void k_fine_keys(const double4* __restrict__ pw, uint64_t n, double lo0, double lo1, double lo2, double cw,
+                            uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double4 q = pw[i];
+  const double c[3] = {q.x, q.y, q.z}, lo[3] = {lo0, lo1, lo2};
+  uint32_t ijk[3];
+  for (int a = 0; a < 3; ++a) {
+    double u = floor(__ddiv_rn(__dsub_rn(c[a], lo[a]), cw));
+    u = u < 0 ? 0 : (u > 2097151.0 ? 2097151.0 : u);
+    ijk[a] = static_cast<uint32_t>(u);
+  }
+  keys[i] = morton(ijk[0], ijk[1], ijk[2]);
+  idx[i] = static_cast<uint32_t>(i);
+}
+__global__ void k_equal_key_runs(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx, uint64_t n,
+                                 const double4* __restrict__ pw, int* __restrict__ flag) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n || (i > 0 && keys[i] == keys[i - 1])) return;  // one thread per run of equal keys
+  for (uint64_t a = i; a + 1 < n && keys[a + 1] == keys[i]; ++a) {
+    const double4 pa = pw[idx[a]];
+    for (uint64_t b = a + 1; b < n && keys[b] == keys[i]; ++b) {
+      const double4 pb = pw[idx[b]];
+      if (pa.x == pb.x && pa.y == pb.y && pa.z == pb.z) atomicOr(flag, 2);
+    }
+  }
+}
+
 __global__ void k_shift3(const uint64_t* __restrict__ in, uint32_t n, uint64_t* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = in[i] >> 3;
@@ -204,7 +246,12 @@ void* cache_alloc(fmmgpu_ctx* c, size_t bytes, cudaStream_t s) {
     return p;
   }
   void* p = nullptr;
+  static const bool tr = std::getenv("FMMGPU_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   FMM_CUDA(cudaMallocAsync(&p, bytes, s));
+  if (tr)
+    std::fprintf(stderr, "[alloc] cache miss %zu bytes: %.3f ms\n", bytes,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   C.live[p] = bytes;
   return p;
 }
@@ -336,10 +383,12 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     k_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, c->lo[0], c->lo[1], c->lo[2], hib[0], hib[1], hib[2], cw, grid,
                                            keys, idx, c->d_flag);
     FMM_CUDA(cudaGetLastError());
+    trace("keys");
     FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
                                              std::max(1, 3 * leaf), s));
     FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n),
                                              0, std::max(1, 3 * leaf), s));
+    trace("sort");
     c->d_pw = dalloc<double4>(c, n, s);
     c->d_inv = dalloc<uint32_t>(c, n, s);
     k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw, c->d_inv);
@@ -377,9 +426,27 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   FMM_CUDA(cudaMemsetAsync(L.child_count, 0, 4ull * runs, s));
   FMM_CUDA(cudaMemsetAsync(L.parent, 0, 4ull * runs, s));
   c->d_pcell = dalloc<uint32_t>(c, n, s);
-  k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs, c->d_pw,
-                                                               c->d_pcell, c->d_flag);
-  FMM_CUDA(cudaGetLastError());
+  if (n <= 64ull * runs) {
+    k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs, c->d_pw,
+                                                                 c->d_pcell, c->d_flag);
+    FMM_CUDA(cudaGetLastError());
+  } else {
+    k_leaf_cells<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs,
+                                                                  c->d_pcell);
+    uint64_t* fk = dalloc<uint64_t>(c, n, s);
+    uint64_t* fks = dalloc<uint64_t>(c, n, s);
+    uint32_t* fi = dalloc<uint32_t>(c, n, s);
+    uint32_t* fis = dalloc<uint32_t>(c, n, s);
+    k_fine_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_pw, n, c->lo[0], c->lo[1], c->lo[2], root[3] / 2097152.0, fk, fi);
+    FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, fk, fks, fi, fis, static_cast<int>(n), 0, 63, s));
+    FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, fk, fks, fi, fis, static_cast<int>(n), 0, 63, s));
+    k_equal_key_runs<<<blocks(n, 256), 256, 0, s>>>(fks, fis, n, c->d_pw, c->d_flag);
+    FMM_CUDA(cudaGetLastError());
+    dfree(c, fk, s);
+    dfree(c, fks, s);
+    dfree(c, fi, s);
+    dfree(c, fis, s);
+  }
 
   trace("leaf level");
   // parent levels by code >> 3 (geometry.cpp:138-153)

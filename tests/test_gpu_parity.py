@@ -327,6 +327,19 @@ def test_edge_cases(fmm):
         c.build_tree(np.array([[0.1, 0.1, 0.1, 1.0], [0.1, 0.1, 0.1, 1.0], [0.9, 0.9, 0.9, 1.0]]), 4)
     with pytest.raises(P.DomainError):
         c.build_tree(np.array([[2.0, 0.5, 0.5, 1.0]]), 4, root=[0.5, 0.5, 0.5, 1.0])
+    # large leaves (> 64 particles per leaf on average: the sorted level-21 key check):
+    # a duplicate is found, positions closer than 2^-21 of the root (equal level-21
+    # keys) but not equal are accepted
+    big = make_particles(12000, "uniform", 8, False)
+    ok = big.copy()
+    ok[7, :3] = ok[5, :3] + [1e-12, 0.0, 0.0]
+    ok[9, :3] = ok[5, :3] + [0.0, 2e-12, 0.0]
+    c.build_tree(ok, 3)
+    assert c.particles()[0].shape[0] == 12000
+    dup = ok.copy()
+    dup[11, :3] = dup[5, :3]  # equal to particle 5, not adjacent after the key sort
+    with pytest.raises(P.DomainError):
+        c.build_tree(dup, 3)
     with pytest.raises(P.InvalidArgument):
         c.build_tree(one, 4, root=[0.5, 0.5, 0.5, 0.0])
     with pytest.raises(P.InvalidArgument):

@@ -9,8 +9,9 @@ import torch
 
 import paper_1206_0115_b200 as P
 
-n, h = 10_000_000, 7
-xyzw = P.generate_particles(n, "uniform", 42)
+import os
+n, h, dist = {"B": (10_000_000, 7, "uniform"), "D": (20_000_000, 8, "ellipsoid")}[os.environ.get("PROBE_CFG", "B")]
+xyzw = P.generate_particles(n, dist, 42)
 c = P.FmmContext(None, order=5)
 pin = torch.from_numpy(xyzw).pin_memory()
 dev = pin.cuda()

@@ -216,6 +216,10 @@ struct fmmgpu_ctx {
   size_t splitk_cap = 0;
   bool out_valid = false;        // d_out holds near + far of the current arrays
   bool zero_pending = false;     // expansions / field accumulators of a new tree not yet cleared
+  // set while an unpartitioned evaluation is enqueued: every operator writes its output
+  // (sums formed in the same order as accumulating into zero) instead of accumulating,
+  // so the evaluation needs no clearing pass and no read of the old values
+  bool ow = false;
   int* d_flag = nullptr;         // error flags
   // near plan
   bool have_lists = false;

@@ -390,7 +390,19 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
   c->launches = 0;
   cudaEvent_t* e = c->ev_t;
   record(c, e[0], s);
-  reset_arrays(c, s);
+  struct OwReset {  // per-operator calls after this evaluation (or after an error) accumulate
+    fmmgpu_ctx* c;
+    ~OwReset() { c->ow = false; }
+  } ow_reset{c};
+  c->ow = c->part_n == 1;
+  if (c->ow) {  // only level 2's local_down is read without being written (L2L's first parent level)
+    if (c->height > 2) {
+      const Level& L2 = c->lv[2];
+      FMM_CUDA(cudaMemsetAsync(L2.local_down, 0, size_t(L2.n) * c->ldE * sizeof(double), s));
+    }
+  } else {
+    reset_arrays(c, s);
+  }
   FMM_CUDA(cudaEventRecord(c->ev_fork, s));
   FMM_CUDA(cudaStreamWaitEvent(c->s_near, c->ev_fork, 0));
   record(c, e[6], c->s_near);

@@ -230,6 +230,7 @@ struct GemmArgs {
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
   int msplit;             // phase A M-split factor (coarse levels)
   int late_load;          // phase A: refill the ring after the slice's DMMAs
+  int ow;                 // phase B: write local_own instead of accumulating (evaluation)
   int dbg;                // FMMGPU_M2L_DEBUG (timing experiments only, wrong results): 1 no scatter,
                           // 2 no lookups, 4 scatter stores made contiguous (config-B leaf: 10.7 / - / 11.2
                           // vs 11.9 ms for phase A + B)
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
         if (t == NPOS) continue;
         if (g.ksplit == 1) {
           double* out = g.local + size_t(t) * g.ldE + row;
-          *out += g.scale * acc[i][j][e];
+          *out = g.ow ? g.scale * acc[i][j][e] : *out + g.scale * acc[i][j][e];
         } else {
           g.part[(size_t(split) * g.ncells + t) * g.ldE + row] = acc[i][j][e];
         }
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
 // over the targets of the phase B list only (the partials of other cells are unset)
 __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit, uint32_t ncells, int ldE, int l3,
                                     double scale, const uint32_t* __restrict__ targets, uint32_t ntargets,
-                                    double* __restrict__ local) {
+                                    double* __restrict__ local, int ow) {
   const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (e >= uint64_t(ntargets) * ldE) return;
   const int row = static_cast<int>(e % ldE);
@@ -357,7 +358,7 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
   const uint64_t i = uint64_t(targets[e / ldE]) * ldE + row;
   double s = part[i];
   for (int k = 1; k < ksplit; ++k) s += part[k * uint64_t(ncells) * ldE + i];
-  local[i] += scale * s;
+  local[i] = ow ? scale * s : local[i] + scale * s;
 }
 
 // Phase A, W-resident: one CTA owns BN source columns of one parity class. Their
@@ -712,6 +713,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   g.rowsA = T.rowsA;
   g.kslot = T.dKslot;
   g.local = L.local_own;
+  g.ow = c->ow ? 1 : 0;
   g.l3 = c->l3;
   g.scale = 1.0 / (c->root[3] / static_cast<double>(uint64_t{1} << v));  // bench.cpp:233-234
   uint32_t maxcls = 0;
@@ -791,7 +793,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       const uint32_t ntg = g.cls_off[8];
       const uint64_t tot = uint64_t(ntg) * c->ldE;
       k_m2l_splitk_reduce<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(
-          g.part, ks, L.n, c->ldE, c->l3, g.scale, g.cls_cells, ntg, L.local_own);
+          g.part, ks, L.n, c->ldE, c->l3, g.scale, g.cls_cells, ntg, L.local_own, c->ow ? 1 : 0);
       FMM_CUDA(cudaGetLastError());
       ++c->launches;
     }

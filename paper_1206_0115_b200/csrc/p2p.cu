@@ -49,6 +49,7 @@ struct P2PArgs {
   const double4* pw;
   double4* near;  // [n] x {pot, fx, fy, fz}, Morton order
   uint64_t n;
+  int ow;         // overwrite (evaluation): the first staging chunk writes near instead of adding
 };
 
 // A staged source that contributes exactly zero: w = 0 far away (finite r^2, so
@@ -227,7 +228,7 @@ __device__ void p2p_unit(const P2PArgs& a, const Neigh& nb, const double4* src, 
     __syncwarp();
   }
   if (lane < m) {
-    double4 r = a.near[tg];
+    double4 r = a.ow && base == 0 ? make_double4(0, 0, 0, 0) : a.near[tg];
     r.x += pot;
     r.y += fx;
     r.z += fy;
@@ -378,7 +379,7 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const uint32_t np = P.own1 - P.own0;
   if (np == 0) return;
   P2PArgs a{L.view(leaf), P.code, P.own0, np, 1, 0, L.first_particle, L.particle_count, c->d_pw,
-             reinterpret_cast<double4*>(c->d_near), c->n};
+             reinterpret_cast<double4*>(c->d_near), c->n, c->ow ? 1 : 0};
   auto run = [&](auto kern, int warps, int smem, unsigned grid) {
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, warps * 32, smem, s>>>(a);

@@ -87,6 +87,7 @@ struct LeafArgs {
   uint32_t ncells;  // one past the last leaf cell of the launch
   int ldE;
   Geo geo;
+  int ow;  // overwrite (evaluation): P2M writes the multipole incl. zero padding, L2P writes far
 };
 
 constexpr int P2M_THREADS = 128;
@@ -120,7 +121,9 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
 #pragma unroll
   for (int i = 0; i < PP; ++i)
 #pragma unroll
-    for (int n = 0; n < L; ++n) acc[i][n] = (lane + 32 * i < L * L) ? out[(lane + 32 * i) * L + n] : 0.0;
+    for (int n = 0; n < L; ++n) acc[i][n] = (!a.ow && lane + 32 * i < L * L) ? out[(lane + 32 * i) * L + n] : 0.0;
+  if (a.ow)
+    for (int i = L * L * L + lane; i < a.ldE; i += 32) out[i] = 0.0;
   double(*sw)[3 * L + 1] = S[warp];
   for (uint32_t base = 0; base < cnt; base += 32) {
     if (base + lane < cnt) {
@@ -189,7 +192,9 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp2(LeafArgs a) {
 #pragma unroll
   for (int i = 0; i < PP; ++i)
 #pragma unroll
-    for (int n = 0; n < L; ++n) acc[i][n] = (lane + 32 * i < L * L) ? out[(lane + 32 * i) * L + n] : 0.0;
+    for (int n = 0; n < L; ++n) acc[i][n] = (!a.ow && lane + 32 * i < L * L) ? out[(lane + 32 * i) * L + n] : 0.0;
+  if (a.ow)
+    for (int i = L * L * L + lane; i < a.ldE; i += 32) out[i] = 0.0;  // padding read by M2L phase A (K = ldE)
   double(*sv)[32] = SV[warp];
   for (uint32_t base = 0; base < cnt; base += 32) {
     double s[L];
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
   const double4 zero4 = make_double4(0, 0, 0, 0);
   const double4 pf = s_first < p1 ? a.pw[s_first] : zero4;
   double4* far4 = reinterpret_cast<double4*>(a.far);
-  const double4 ff = s_first < p1 ? far4[s_first] : zero4;
+  const double4 ff = s_first < p1 && !a.ow ? far4[s_first] : zero4;
   if (threadIdx.x < nc) {
     const uint32_t c = c0 + threadIdx.x;
     cfirst[threadIdx.x] = a.first[c];
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
     const double4 fprev = fnext;
     if (s + L2P_THREADS < p1) {  // next particle's loads overlap this one's arithmetic
       pnext = a.pw[s + L2P_THREADS];
-      fnext = far4[s + L2P_THREADS];
+      fnext = a.ow ? zero4 : far4[s + L2P_THREADS];
     }
     const double rx = (p.x - ctr[0]) * inv, ry = (p.y - ctr[1]) * inv, rz = (p.z - ctr[2]) * inv;
     double sx[L], sy[L], sz[L], gx[L], gy[L], gz[L];
@@ -352,6 +357,7 @@ struct TransArgs {
   uint32_t p0;             // first parent of the launch (partitioned runs: the owned range)
   uint32_t nparents;
   int ldE;
+  int ow;  // overwrite (evaluation): M2M writes the parent incl. zero padding, L2L writes local_down
 };
 
 // dst[r*L + n] = sum_k mt[k*L + n] * src[k*L*L + r]  (tensor_step, chebyshev.cpp:186-199)
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(256) k_transfer_warp(TransArgs a) {
       for (int r = lane; r < L * L; r += 32) {
         step_row<L>(m2, b1, r, o);
 #pragma unroll
-        for (int n = 0; n < L; ++n) out[r * L + n] += o[n];
+        for (int n = 0; n < L; ++n) out[r * L + n] = a.ow ? o[n] : out[r * L + n] + o[n];
       }
     }
   }
@@ -444,10 +450,12 @@ __global__ void __launch_bounds__(256) k_transfer_warp(TransArgs a) {
     __syncthreads();
     double* out = a.out + size_t(p) * a.ldE;
     for (int i = tid; i < L3; i += 256) {
-      double acc = out[i];
+      double acc = a.ow ? 0.0 : out[i];
       for (uint32_t c = 0; c < nch; ++c) acc += buf[c][0][i];
       out[i] = acc;
     }
+    if (a.ow)
+      for (int i = L3 + tid; i < a.ldE; i += 256) out[i] = 0.0;
   }
 }
 
@@ -490,7 +498,10 @@ __global__ void __launch_bounds__(128) k_transfer(TransArgs a) {
       }
     } else {
       double* out = a.out + size_t(ch) * a.ldE;
-      for (int i = tid; i < L3; i += 128) out[i] += step_one<L>(m2, buf1, i);
+      for (int i = tid; i < L3; i += 128) {
+        const double v = step_one<L>(m2, buf1, i);
+        out[i] = a.ow ? v : out[i] + v;
+      }
     }
   }
   if (IS_M2M) {
@@ -498,8 +509,10 @@ __global__ void __launch_bounds__(128) k_transfer(TransArgs a) {
 #pragma unroll
     for (int o = 0; o < OPT; ++o) {
       const int i = tid + o * 128;
-      if (i < L3) out[i] += acc[o];
+      if (i < L3) out[i] = a.ow ? acc[o] : out[i] + acc[o];
     }
+    if (a.ow)
+      for (int i = L3 + tid; i < a.ldE; i += 128) out[i] = 0.0;
   }
 }
 
@@ -654,6 +667,7 @@ void interp_setup(fmmgpu_ctx* c) {
 void launch_p2m(fmmgpu_ctx* c, cudaStream_t s) {
   LeafArgs a = leaf_args(c);
   a.expansion = c->lv[c->height - 1].multipole;
+  a.ow = c->ow;
   dispatch_order<RunP2M>(c->order, a, s);
   FMM_CUDA(cudaGetLastError());
   ++c->launches;
@@ -664,6 +678,7 @@ void launch_l2p(fmmgpu_ctx* c, cudaStream_t s) {
   a.expansion = c->lv[c->height - 1].local_own;
   a.down = c->lv[c->height - 1].local_down;
   a.far = c->d_far;
+  a.ow = c->ow;
   dispatch_order<RunL2P>(c->order, a, s);
   FMM_CUDA(cudaGetLastError());
   ++c->launches;
@@ -678,6 +693,7 @@ void launch_m2m(fmmgpu_ctx* c, int v, cudaStream_t s) {
   a.mats = c->d_interp + 3 * l * l;  // child_t
   a.child_in = c->lv[v + 1].multipole;
   a.out = c->lv[v].multipole;
+  a.ow = c->ow;
   a.p0 = c->lv[v].own0;
   a.nparents = c->lv[v].own1 - c->lv[v].own0;
   a.ldE = c->ldE;
@@ -696,6 +712,7 @@ void launch_l2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   a.parent_a = c->lv[v].local_own;
   a.parent_b = c->lv[v].local_down;
   a.out = c->lv[v + 1].local_down;
+  a.ow = c->ow;
   a.p0 = c->lv[v].own0;
   a.nparents = c->lv[v].own1 - c->lv[v].own0;
   a.ldE = c->ldE;

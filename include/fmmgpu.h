@@ -151,6 +151,14 @@ int fmmgpu_ledger(fmmgpu_ctx* ctx, uint64_t* flops7, uint64_t* near_directional,
                   uint64_t* m2l_pairs);
 /* Number of kernels launched by the last fmmgpu_evaluate. */
 uint64_t fmmgpu_last_launch_count(const fmmgpu_ctx* ctx);
+/* Per-launch device trace of evaluations (runtime.cpp:157-171 TraceEvent, written by
+ * write_chrome_trace, runtime.cpp:277-292): while on, fmmgpu_evaluate runs eagerly and
+ * brackets every operator launch with events. fmmgpu_trace_spans returns, for the last
+ * evaluation, `count` spans: meta3[3 i..] = {fmmgpu_kind, level, stream (0 far field,
+ * 1 near field)} and start/end in ms from the first span's start (P2PREDUCE = the
+ * gather of near + far). Arrays hold `cap` spans; NULL pointers only query the count. */
+int fmmgpu_set_trace(fmmgpu_ctx* ctx, int on);
+int fmmgpu_trace_spans(fmmgpu_ctx* ctx, int cap, int* count, int* meta3, double* start_end_ms);
 /* Runs `steps` back-to-back evaluations bracketed by CUDA events on the launching
  * stream: total_ms = device time of all steps; kind_ms10 (optional) = per-kind sums
  * as in fmmgpu_timings; launches (optional) = kernels launched in the region. */

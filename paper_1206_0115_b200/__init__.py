@@ -84,6 +84,8 @@ def lib():
         L.fmmgpu_run.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]
         L.fmmgpu_run_async.argtypes = L.fmmgpu_run.argtypes
         L.fmmgpu_run_wait.argtypes = [c_void_p]
+        L.fmmgpu_set_trace.argtypes = [c_void_p, c_int]
+        L.fmmgpu_trace_spans.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p]
         for name in ("fmmgpu_reset", "fmmgpu_p2m", "fmmgpu_l2p", "fmmgpu_p2p", "fmmgpu_evaluate",
                      "fmmgpu_synchronize", "fmmgpu_build_lists"):
             getattr(L, name).argtypes = [c_void_p]
@@ -420,6 +422,22 @@ class FmmContext:
 
     def run_wait(self):
         self._check(self._lib.fmmgpu_run_wait(self.h))
+
+    def set_trace(self, on: bool = True):
+        """Per-launch device trace of the following evaluations (fmmgpu_set_trace)."""
+        self._check(self._lib.fmmgpu_set_trace(self.h, 1 if on else 0))
+
+    def trace_spans(self):
+        """Spans of the last traced evaluation: [(kind, level, stream, start_ms, end_ms)],
+        stream 0 = far field, 1 = near field (runtime.hpp TraceEvent analogue)."""
+        cnt = c_int()
+        self._check(self._lib.fmmgpu_trace_spans(self.h, 0, byref(cnt), None, None))
+        n = cnt.value
+        meta = np.zeros(3 * max(n, 1), dtype=np.int32)
+        t = np.zeros(2 * max(n, 1))
+        self._check(self._lib.fmmgpu_trace_spans(self.h, n, byref(cnt), _p(meta), _p(t)))
+        return [(KINDS[meta[3 * i]], int(meta[3 * i + 1]), int(meta[3 * i + 2]), float(t[2 * i]), float(t[2 * i + 1]))
+                for i in range(n)]
 
 
 def check_targets(n: int, check: int) -> np.ndarray:

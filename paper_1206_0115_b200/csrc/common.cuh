@@ -220,6 +220,11 @@ struct fmmgpu_ctx {
   // (sums formed in the same order as accumulating into zero) instead of accumulating,
   // so the evaluation needs no clearing pass and no read of the old values
   bool ow = false;
+  // per-launch device trace of evaluations (fmmgpu_set_trace): one event pair per
+  // operator launch, {kind, level, stream} beside it; evaluations run eagerly while on
+  bool trace = false;
+  std::vector<cudaEvent_t> tr_ev;
+  std::vector<int> tr_meta;  // 3 per span: kind, level, stream (0 far field, 1 near field)
   int* d_flag = nullptr;         // error flags
   // near plan
   bool have_lists = false;

@@ -227,6 +227,7 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_canon) cudaFree(c->d_canon);
   if (c->h_rb) cudaFreeHost(c->h_rb);
+  for (auto e : c->tr_ev) cudaEventDestroy(e);
   for (auto& e : c->ev_t)
     if (e) cudaEventDestroy(e);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -384,10 +385,39 @@ void record(fmmgpu_ctx* c, cudaEvent_t e, cudaStream_t s) {
 }
 
 // One evaluation: reset, then the DAG as a level-synchronous two-stream schedule.
+// trace span around one launch (eager evaluations with tracing on)
+struct Span {
+  fmmgpu_ctx* c;
+  size_t i = 0;
+  Span(fmmgpu_ctx* cc, int kind, int level, cudaStream_t st, int stream_id) : c(cc) {
+    if (!c->trace) return;
+    i = c->tr_ev.size();
+    for (int k = 0; k < 2; ++k) {
+      cudaEvent_t e;
+      FMM_CUDA(cudaEventCreate(&e));
+      c->tr_ev.push_back(e);
+    }
+    c->tr_meta.insert(c->tr_meta.end(), {kind, level, stream_id});
+    FMM_CUDA(cudaEventRecord(c->tr_ev[i], st));
+    this->st = st;
+  }
+  ~Span() {
+    if (c->trace) cudaEventRecord(c->tr_ev[i + 1], st);
+  }
+  cudaStream_t st = nullptr;
+};
+
+void trace_clear(fmmgpu_ctx* c) {
+  for (auto e : c->tr_ev) cudaEventDestroy(e);
+  c->tr_ev.clear();
+  c->tr_meta.clear();
+}
+
 void enqueue_evaluation(fmmgpu_ctx* c) {
   const int leaf = c->height - 1;
   cudaStream_t s = c->s_far;
   c->launches = 0;
+  if (c->trace) trace_clear(c);
   cudaEvent_t* e = c->ev_t;
   record(c, e[0], s);
   struct OwReset {  // per-operator calls after this evaluation (or after an error) accumulate
@@ -406,27 +436,48 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
   FMM_CUDA(cudaEventRecord(c->ev_fork, s));
   FMM_CUDA(cudaStreamWaitEvent(c->s_near, c->ev_fork, 0));
   record(c, e[6], c->s_near);
-  launch_p2p(c, c->s_near);
+  {
+    Span sp(c, FMMGPU_P2P, leaf, c->s_near, 1);
+    launch_p2p(c, c->s_near);
+  }
   record(c, e[7], c->s_near);
   record(c, e[1], s);
-  launch_p2m(c, s);
+  {
+    Span sp(c, FMMGPU_P2M, leaf, s, 0);
+    launch_p2m(c, s);
+  }
   exchange_level(c, leaf, s);  // partitioned runs: all-gather this level's multipoles
   record(c, e[2], s);
   for (int v = leaf - 1; v >= 2; --v) {
-    launch_m2m(c, v, s);
+    {
+      Span sp(c, FMMGPU_M2M, v, s, 0);
+      launch_m2m(c, v, s);
+    }
     exchange_level(c, v, s);
   }
   record(c, e[3], s);
-  for (int v = 2; v <= leaf; ++v) launch_m2l(c, v, s);
+  for (int v = 2; v <= leaf; ++v) {
+    Span sp(c, FMMGPU_M2L, v, s, 0);
+    launch_m2l(c, v, s);
+  }
   record(c, e[4], s);
-  for (int v = 2; v < leaf; ++v) launch_l2l(c, v, s);
+  for (int v = 2; v < leaf; ++v) {
+    Span sp(c, FMMGPU_L2L, v, s, 0);
+    launch_l2l(c, v, s);
+  }
   record(c, e[5], s);
-  launch_l2p(c, s);
+  {
+    Span sp(c, FMMGPU_L2P, leaf, s, 0);
+    launch_l2p(c, s);
+  }
   record(c, e[8], s);
   FMM_CUDA(cudaEventRecord(c->ev_join, c->s_near));
   FMM_CUDA(cudaStreamWaitEvent(s, c->ev_join, 0));
   record(c, e[9], s);
-  launch_gather(c, s);
+  {
+    Span sp(c, FMMGPU_P2PREDUCE, leaf, s, 0);  // the gather of near + far (P2PReduce's role)
+    launch_gather(c, s);
+  }
   record(c, e[10], s);
 }
 
@@ -445,7 +496,7 @@ int fmmgpu_evaluate(fmmgpu_ctx* c) {
     need_tree(c);
     FMM_CUDA(cudaSetDevice(c->device));
     static const bool no_graph = std::getenv("FMMGPU_NO_GRAPH") != nullptr;
-    const bool graphable = !no_graph && !(c->part_n > 1 && c->nccl);
+    const bool graphable = !no_graph && !(c->part_n > 1 && c->nccl) && !c->trace;
     if (graphable && c->graph_exec) {
       FMM_CUDA(cudaGraphLaunch(c->graph_exec, c->s_far));
       c->launches = c->graph_launches;
@@ -542,6 +593,30 @@ int fmmgpu_timings(const fmmgpu_ctx* cc, double* ms) {
 }
 
 uint64_t fmmgpu_last_launch_count(const fmmgpu_ctx* c) { return c ? c->launches : 0; }
+
+int fmmgpu_set_trace(fmmgpu_ctx* c, int on) {
+  return guarded(c, [&] {
+    c->trace = on != 0;
+    fmmgpu_invalidate_graph(c);
+    if (!c->trace) trace_clear(c);
+  });
+}
+
+int fmmgpu_trace_spans(fmmgpu_ctx* c, int cap, int* count, int* meta3, double* start_end_ms) {
+  return guarded(c, [&] {
+    const int nsp = static_cast<int>(c->tr_ev.size() / 2);
+    if (count) *count = nsp;
+    if (nsp == 0 || cap <= 0) return;
+    FMM_CUDA(cudaEventSynchronize(c->tr_ev.back()));
+    for (int i = 0; i < std::min(nsp, cap); ++i) {
+      if (meta3) std::copy(c->tr_meta.begin() + 3 * i, c->tr_meta.begin() + 3 * i + 3, meta3 + 3 * i);
+      if (start_end_ms) {
+        start_end_ms[2 * i] = elapsed(c->tr_ev[0], c->tr_ev[2 * i]);
+        start_end_ms[2 * i + 1] = elapsed(c->tr_ev[0], c->tr_ev[2 * i + 1]);
+      }
+    }
+  });
+}
 
 int fmmgpu_time_evaluations(fmmgpu_ctx* c, int steps, double* total_ms, double* kind_ms10, uint64_t* launches) {
   return guarded(c, [&] {

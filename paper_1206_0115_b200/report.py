@@ -4,7 +4,10 @@
   (round-trip) values (bench.cpp:504-514);
 * ``write_summary_json`` summary.json with the reference's keys: config, timings,
   accuracy, compression, flop_costs, ledger (per kind; the device ledger is not split per
-  level), occupancy replaced by the device per-operator times (bench.cpp:516-584).
+  level), occupancy replaced by the device per-operator times (bench.cpp:516-584);
+* ``write_chrome_trace`` trace.json in the reference's Chrome "ph":"X" format
+  (runtime.cpp:277-292) from the device spans of FmmContext.trace_spans (one span per
+  operator launch; tid = CUDA stream: 0 far field, 1 near field).
 """
 from __future__ import annotations
 
@@ -63,3 +66,17 @@ def write_summary_json(path: str, *, cfg, n: int, setup_seconds: float, exec_sec
         json.dump(j, f, indent=2)
         f.write("\n")
     return j
+
+
+def write_chrome_trace(path: str, spans, work=None) -> None:
+    """runtime.cpp:277-292: a JSON array of {"name", "ph":"X", "ts", "dur" (microseconds),
+    "pid":0, "tid", "args":{"level", "work"}}; spans = [(kind, level, stream, start_ms,
+    end_ms)], work = optional {(kind, level): value}."""
+    events = []
+    for kind, level, stream, t0, t1 in spans:
+        w = 0 if work is None else work.get((kind, level), 0)
+        events.append({"name": kind, "ph": "X", "ts": t0 * 1e3, "dur": (t1 - t0) * 1e3, "pid": 0, "tid": stream,
+                       "args": {"level": level, "work": w}})
+    with open(path, "w") as f:
+        json.dump(events, f, indent=0)
+        f.write("\n")

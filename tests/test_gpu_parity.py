@@ -245,6 +245,32 @@ def test_run_entry_point(fmm):
     assert force_error(*g[1:], *of[1:]) <= TOL
 
 
+def test_trace_spans(fmm, tmp_path):
+    """Per-launch device trace (runtime.cpp TraceEvent / write_chrome_trace analogue):
+    one span per operator launch and level, the DAG order on the far-field stream, the
+    same fields as an untraced evaluation."""
+    from paper_1206_0115_b200.report import write_chrome_trace
+    xyzw = make_particles(20000, "uniform", 3, True)
+    c = ctx_for(fmm, xyzw, 5, 4)
+    c.evaluate()
+    ref = c.gather()
+    c.set_trace(True)
+    c.evaluate()
+    spans = c.trace_spans()
+    got = c.gather()
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
+    kinds = [(k, lv) for k, lv, _, _, _ in spans]
+    assert kinds == [("P2P", 4), ("P2M", 4), ("M2M", 3), ("M2M", 2), ("M2L", 2), ("M2L", 3), ("M2L", 4),
+                     ("L2L", 2), ("L2L", 3), ("L2P", 4), ("P2PREDUCE", 4)]
+    far = [sp for sp in spans if sp[2] == 0]
+    assert all(sp[4] >= sp[3] for sp in spans)
+    assert all(b[3] >= a[4] - 1e-6 for a, b in zip(far, far[1:]))  # one stream: in order
+    write_chrome_trace(str(tmp_path / "trace.json"), spans)
+    c.set_trace(False)
+    assert c.trace_spans() == []
+
+
 def test_pipelined_runs(fmm):
     """fmmgpu_run_async over a stream of different particle sets (sizes, heights and
     distributions change between steps, so buffers grow mid-stream) returns, for every

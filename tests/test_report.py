@@ -8,7 +8,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1206_0115_b200 import RunConfig  # noqa: E402
-from paper_1206_0115_b200.report import flop_costs, read_results_csv, write_results_csv, write_summary_json  # noqa: E402
+from paper_1206_0115_b200.report import (flop_costs, read_results_csv, write_chrome_trace,  # noqa: E402
+                                         write_results_csv, write_summary_json)
 
 
 def test_results_csv_round_trip(tmp_path):
@@ -35,3 +36,13 @@ def test_summary_json_keys(tmp_path):
     assert set(j) >= {"config", "timings", "compression", "flop_costs", "ledger", "accuracy"}
     assert j["ledger"]["total_flops"] == 100 and abs(j["ledger"]["M2L"]["share_percent"] - 50) < 1e-12
     assert j["flop_costs"] == flop_costs(5) and j["flop_costs"]["l2p_per_particle"] == 16 * 125 + 150
+
+
+def test_chrome_trace_format(tmp_path):
+    spans = [("P2P", 6, 1, 0.0, 12.5), ("P2M", 6, 0, 0.01, 0.8), ("M2L", 6, 0, 1.0, 13.0)]
+    p = str(tmp_path / "trace.json")
+    write_chrome_trace(p, spans, work={("M2L", 6): 123})
+    ev = json.load(open(p))
+    assert [e["name"] for e in ev] == ["P2P", "P2M", "M2L"]
+    assert all(e["ph"] == "X" and e["pid"] == 0 for e in ev)
+    assert ev[0]["tid"] == 1 and abs(ev[0]["dur"] - 12500.0) < 1e-9 and ev[2]["args"] == {"level": 6, "work": 123}

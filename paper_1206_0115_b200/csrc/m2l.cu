@@ -744,7 +744,11 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       const uint32_t ncols = 8u * ((maxcls + bn - 1) / bn);
       const int mtiles = T.rowsA / PA_BM;
       int ms = 1;
-      while (ms < mtiles && ncols * ms < 2u * 148u) ++ms;
+      static const uint32_t waves = [] {  // FMMGPU_M2L_WAVES: minimum CTA waves (2 per SM) before M-splitting stops
+        const char* e = std::getenv("FMMGPU_M2L_WAVES");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 2u;  // config B: 28.55 vs 28.76 ms (1 wave)
+      }();
+      while (ms < mtiles && ncols * ms < waves * 2u * 148u) ++ms;
       g.msplit = ms;
       dim3 grid((maxcls + bn - 1) / bn, 8, ms);
       kern<<<grid, PA_THREADS, smem, s>>>(g);
@@ -770,7 +774,11 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     const uint32_t ctas = 8u * ((maxcls + B_BN - 1) / B_BN) * mtiles;
     const int kt = T.ldY / B_BK;
     int ks = 1;
-    while (ks < 16 && ctas * ks < 2u * 148u && kt / (2 * ks) >= 8) ks *= 2;
+    static const uint32_t waves = [] {
+      const char* e = std::getenv("FMMGPU_M2L_WAVES");
+      return e ? static_cast<uint32_t>(std::atoi(e)) : 2u;  // config B: 28.55 vs 28.76 ms (1 wave)
+    }();
+    while (ks < 16 && ctas * ks < waves * 2u * 148u && kt / (2 * ks) >= 8) ks *= 2;
     g.ksplit = ks;
     if (ks > 1) {  // own buffer (not the shared scratch): captured graphs keep this pointer
       const size_t bytes = sizeof(double) * ks * size_t(L.n) * c->ldE;

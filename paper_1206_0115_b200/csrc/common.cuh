@@ -145,7 +145,6 @@ struct M2LTables {
   int ldY = 0;      // round_up(R, 32): stride of one target's compressed vector
   int rowsA = 0;    // round_up(R, bmA): padded M of phase A
   int bmA = 64;     // phase A M-tile rows (64 for l <= 5, 128 above)
-  int a_variant = 0;  // phase A tiling experiment (FMMGPU_M2L_A)
   int rowsB = 0;    // round_up(l^3, 64)... padded M of phase B
   double* dM1 = nullptr;    // [8][rowsA][ldE]
   double* dM2 = nullptr;    // [8][rowsB][ldY]

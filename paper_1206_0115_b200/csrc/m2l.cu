@@ -229,11 +229,7 @@ struct GemmArgs {
   double* local;          // phase B output (local_own)
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
   int msplit;             // phase A M-split factor (coarse levels)
-  int late_load;          // phase A: refill the ring after the slice's DMMAs
   int ow;                 // phase B: write local_own instead of accumulating (evaluation)
-  int dbg;                // FMMGPU_M2L_DEBUG (timing experiments only, wrong results): 1 no scatter,
-                          // 2 no lookups, 4 scatter stores made contiguous (config-B leaf: 10.7 / - / 11.2
-                          // vs 11.9 ms for phase A + B)
   double* part;           // phase B split-K partials [ksplit][ncells][ldE]
   uint32_t ncells;
   int l3;
@@ -456,12 +452,8 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   for (int t = 0; t < TOTAL; ++t) {
     cp_wait<PA_ST - 2>();
     __syncthreads();
-    // late_load: the ring refill is issued after this slice's DMMAs, so the registers of
-    // its cp.async operands are not overwritten (WAR stall) right after the issue
-    if (!g.late_load) {
-      if (t + PA_ST - 1 < TOTAL) load_next();
-      cp_commit();
-    }
+    if (t + PA_ST - 1 < TOTAL) load_next();
+    cp_commit();
     uint32_t* tg = tgt + (mt & 1) * g.vtMax * BN;
     if (kt == 0) {
 #pragma unroll
@@ -470,7 +462,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
       slot_e0 = tid < g.vtMax * BN ? __ldg(vec + tid / BN) : -1;
       slot_e1 = tid + PA_THREADS < g.vtMax * BN ? __ldg(vec + (tid + PA_THREADS) / BN) : -1;
     }
-    if (kt == kt_fill && !(g.dbg & 2)) {
+    if (kt == kt_fill) {
       // one lookup per (vector, source column) of this M-tile: target = source - v
       const int* vec = g.tileVec + (size_t(cls) * MTILES + mt) * g.vtMax;
       int u = 0;
@@ -503,29 +495,19 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
       // scatter block v of source s to target s - v, target-side column info.x
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        if (rowinfo[i].x >= 0 && !(g.dbg & 1)) {
+        if (rowinfo[i].x >= 0) {
           const uint32_t* trow = tg + rowinfo[i].z * BN;
 #pragma unroll
           for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const uint32_t tcell = trow[wn * WTN + j * 8 + 2 * tq + e];
-              if (g.dbg & 4) {  // timing experiment: same stores, contiguous per CTA tile
-                if (tcell != NPOS)
-                  g.Yt[(size_t(blockIdx.y) * gridDim.x + blockIdx.x) * (PA_BM * BN) +
-                       size_t(wm * WTM + i * 8 + gq) * BN + wn * WTN + j * 8 + 2 * tq + e] = acc[i][j][e];
-              } else if (tcell != NPOS) {
-                g.Yt[size_t(tcell) * g.ldY + rowinfo[i].y] = acc[i][j][e];
-              }
+              if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + rowinfo[i].y] = acc[i][j][e];
             }
         }
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
       }
-    }
-    if (g.late_load) {
-      if (t + PA_ST - 1 < TOTAL) load_next();
-      cp_commit();
     }
     if (++stage == PA_ST) stage = 0;
     if (++kt == KT) { kt = 0; ++mt; }
@@ -598,14 +580,10 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   }
   T.R = R;
   T.ldY = round_up(R, 32);
-  // FMMGPU_M2L_A (tuning experiments, l <= 5): 0 = 64-row tiles x 64 columns, 4 stages
-  // (default); 1 = 128 x 64, 2 stages (32x32 warp tiles); 2 = 128 x 32, 3 stages
-  static const int a_variant = [] {
-    const char* e = std::getenv("FMMGPU_M2L_A");
-    return e ? std::atoi(e) : 0;
-  }();
-  T.bmA = c->ldE <= 128 && a_variant == 0 ? 64 : 128;
-  T.a_variant = c->ldE <= 128 ? a_variant : 0;
+  // 64-row M-tiles x 64 resident columns, 4-stage ring for l <= 5; 128 x 16, 3 stages
+  // above. Measured at the config-B leaf (phase A + B): 128 x 64 / 2 stages 15.9 ms,
+  // 128 x 32 / 3 stages 12.6 ms, vs 11.9 ms for 64 x 64 / 4 stages.
+  T.bmA = c->ldE <= 128 ? 64 : 128;
   T.rowsA = round_up(R, T.bmA);
   T.rowsB = round_up(n3, B_BM);
   std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
@@ -723,23 +701,11 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.lda = c->ldE;
     g.a_class_stride = size_t(T.rowsA) * c->ldE;
     g.K = c->ldE;
-    static const int late = [] {
-      const char* e = std::getenv("FMMGPU_M2L_LATE");
-      return e ? std::atoi(e) : 0;  // measured: 12.3 vs 12.0 ms at the config-B leaf
-    }();
-    g.late_load = late;
-    static const int dbg = [] {
-      const char* e = std::getenv("FMMGPU_M2L_DEBUG");
-      return e ? std::atoi(e) : 0;
-    }();
-    g.dbg = dbg;
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
     auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST) {
       const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * PA_SPAD) +
                           sizeof(uint32_t) * 2 * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      static const bool tr = std::getenv("FMMGPU_TRACE") != nullptr;
-      if (tr) std::fprintf(stderr, "[m2l] phase A level %d: BM %d BN %d stages %d smem %zu vtMax %d\n", v, PA_BM, bn, PA_ST, smem, T.vtMax);
       // M-split so coarse levels still put >= 2 CTAs on every SM
       const uint32_t ncols = 8u * ((maxcls + bn - 1) / bn);
       const int mtiles = T.rowsA / PA_BM;
@@ -755,8 +721,6 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       FMM_CUDA(cudaGetLastError());
     };
     if (T.bmA == 64) launch(k_m2l_phase_a<64, 4, 64, 2, 4>, 64, 64, 4);
-    else if (T.a_variant == 1) launch(k_m2l_phase_a<128, 2, 64, 4, 2>, 64, 128, 2);
-    else if (T.a_variant == 2) launch(k_m2l_phase_a<128, 3, 32, 4, 2>, 32, 128, 3);
     else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
   }
   g.cls_cells = L.tgtB ? L.tgtB : L.cls_cells;

@@ -14,16 +14,10 @@
 // sources of each run S = 32 / m ways and combines the S partial sums in a fixed order
 // through shared memory.
 //
-// Two kernels share the unit routine (so results are bit-identical):
-//  * k_p2p_flow (persistent, one CTA per SM): the CTA walks its parents through two
-//    staging slots. Warps pull units of the current parent from the slot's queue and
-//    move on to the next parent (already staged) as soon as the queue is empty; the
-//    last warp to leave a parent restages that slot with the parent after next
-//    (cp.async), so no CTA-wide barrier exists and no warp idles at a parent's end.
-//  * k_p2p (CTA per parent, 2 CTAs per SM): parents whose neighbourhood exceeds one
-//    staging slot stream it through shared memory in chunks (targets then accumulate
-//    into HBM per chunk, still single-writer), and shallow trees with too few parents
-//    for the persistent grid split a parent's units over several CTAs.
+// k_p2p runs one CTA (12 warps, 2 CTAs per SM) per parent. Neighbourhoods larger than
+// one staging buffer (non-uniform clouds) stream through shared memory in chunks
+// (targets then accumulate into HBM per chunk, still single-writer), and shallow trees
+// with too few parents for the GPU split a parent's units over several CTAs.
 //
 // Per interaction: 3 DADD (d) + 3 DP (r^2) + MUFU.RSQ64H and 5 DP (Newton)
 // + 1 DMUL (w/r) + 1 DADD (pot) + 2 DMUL (w/r^3) + 3 DFMA (force) = 18 DP ops.
@@ -35,15 +29,14 @@ namespace fmmgpu {
 
 namespace {
 
-constexpr int P2P_CAP = 3072;  // staged particles per chunk / slot (96 KB), multiple of 4
+constexpr int P2P_CAP = 3072;  // staged particles per chunk (96 KB), multiple of 4
 
 struct P2PArgs {
   LevelView leaf;
   const uint64_t* parent_code;  // level leaf-1
   uint32_t p0;                  // first parent of the launch (partitioned runs: owned range)
   uint32_t np;                  // parents in the launch
-  uint32_t usplit;              // k_p2p: CTAs per parent (CTA y takes the units u = y (mod usplit))
-  int only_big;                 // k_p2p: skip parents whose neighbourhood fits one slot
+  uint32_t usplit;              // CTAs per parent (CTA y takes the units u = y (mod usplit))
   const uint32_t* first;        // leaf first_particle
   const uint32_t* count;        // leaf particle_count
   const double4* pw;
@@ -261,7 +254,6 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
   if (tid < 4) sm.src[P2P_CAP + tid] = dummy_source();
   __syncthreads();
   const uint32_t total = sm.nb.voff[64];
-  if (a.only_big && total <= static_cast<uint32_t>(P2P_CAP)) return;  // done by k_p2p_flow
   const uint32_t nunits = sm.nb.nunits;
 
   for (uint32_t base = 0; base < total; base += P2P_CAP) {
@@ -284,92 +276,6 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
   }
 }
 
-// ------------------------------------------------------------------ k_p2p_flow
-struct FlowSlot {
-  double4 src[P2P_CAP + 4];
-  Neigh nb;
-  uint32_t next_unit;  // unit queue head
-  uint32_t done;       // warps that found the queue empty
-  int ready;           // item index staged in this slot
-};
-template <int WARPS>
-struct FlowSmem {
-  FlowSlot slot[2];
-  double red[WARPS][4][32];
-};
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src));
-}
-
-// One warp stages item `it` (this CTA's it-th parent) into a slot and publishes it.
-// A neighbourhood larger than the slot is left to k_p2p (the slot gets no units).
-__device__ void flow_stage(const P2PArgs& a, FlowSlot& s, int it, int lane) {
-  const uint32_t parent = blockIdx.x + static_cast<uint32_t>(it) * gridDim.x;
-  int pc[3];
-  demorton(a.parent_code[a.p0 + parent], pc);
-  neigh_meta(a, pc, s.nb, lane);
-  const uint32_t total = s.nb.voff[64];
-  if (total > static_cast<uint32_t>(P2P_CAP)) {
-    if (lane == 0) s.nb.nunits = 0;
-  } else {
-    for (uint32_t i = lane; i < total; i += 32) {
-      uint32_t pos, k;
-      locate(s.nb, i, pos, k);
-      if (k < s.nb.cnt[pos]) {
-        const double4* g = a.pw + s.nb.first[pos] + k;
-        cp_async16(&s.src[i], g);
-        cp_async16(reinterpret_cast<double2*>(&s.src[i]) + 1, reinterpret_cast<const double2*>(g) + 1);
-      } else {
-        s.src[i] = dummy_source();
-      }
-    }
-    asm volatile("cp.async.wait_all;\n" ::);
-  }
-  if (lane == 0) {
-    s.next_unit = 0;
-    s.done = 0;
-  }
-  __syncwarp();
-  __threadfence_block();
-  if (lane == 0) *reinterpret_cast<volatile int*>(&s.ready) = it;
-}
-
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1) k_p2p_flow(const P2PArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  FlowSmem<WARPS>& sm = *reinterpret_cast<FlowSmem<WARPS>*>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nitems = static_cast<int>((a.np - blockIdx.x + gridDim.x - 1) / gridDim.x);
-  if (tid < 2) sm.slot[tid].ready = -1;
-  if (tid < 8) sm.slot[tid >> 2].src[P2P_CAP + (tid & 3)] = dummy_source();
-  __syncthreads();
-  if (warp < 2 && warp < nitems) flow_stage(a, sm.slot[warp], warp, lane);
-
-  for (int it = 0; it < nitems; ++it) {
-    FlowSlot& s = sm.slot[it & 1];
-    while (*reinterpret_cast<volatile int*>(&s.ready) != it) __nanosleep(64);
-    __threadfence_block();
-    const uint32_t nunits = s.nb.nunits;
-    for (;;) {
-      uint32_t u = 0;
-      if (lane == 0) u = atomicAdd(&s.next_unit, 1u);
-      u = __shfl_sync(0xffffffffu, u, 0);
-      if (u >= nunits) break;
-      p2p_unit(a, s.nb, s.src, 0, s.nb.voff[64], u, sm.red[warp], lane);
-    }
-    // the last warp to leave this parent restages the slot with item it + 2
-    uint32_t d = 0;
-    if (lane == 0) d = atomicAdd(&s.done, 1u);
-    d = __shfl_sync(0xffffffffu, d, 0);
-    if (d == WARPS - 1 && it + 2 < nitems) {
-      __threadfence_block();
-      flow_stage(a, s, it + 2, lane);
-    }
-  }
-}
-
 }  // namespace
 
 void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
@@ -378,7 +284,7 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const Level& P = c->lv[leaf - 1];
   const uint32_t np = P.own1 - P.own0;
   if (np == 0) return;
-  P2PArgs a{L.view(leaf), P.code, P.own0, np, 1, 0, L.first_particle, L.particle_count, c->d_pw,
+  P2PArgs a{L.view(leaf), P.code, P.own0, np, 1, L.first_particle, L.particle_count, c->d_pw,
              reinterpret_cast<double4*>(c->d_near), c->n, c->ow ? 1 : 0};
   auto run = [&](auto kern, int warps, int smem, unsigned grid) {
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -386,27 +292,18 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
     FMM_CUDA(cudaGetLastError());
     ++c->launches;
   };
-  // FMMGPU_P2P_VARIANT (tuning experiments): 0 = k_p2p 12 warps (default), 2 = 16 warps,
-  // 3 = 8 warps; 6 / 7 = persistent k_p2p_flow with 16 / 24 warps (+ chunked k_p2p for
-  // oversized neighbourhoods). Config B, before the chunked partial passes: 13.7 / 13.9 /
-  // 13.8 / 15.0 / 16.8 ms: with at most one parent of look-ahead the persistent warps
-  // idle at the same unit-granularity tails, with fewer warps per SM to hide latency.
-  // (8 sources per iteration and split accumulators were also measured slower.)
+  // FMMGPU_P2P_VARIANT (tuning experiments): 0 = 12 warps per CTA (default), 2 = 16, 3 = 8.
+  // Config B before the chunked partial passes: 13.7 / 13.9 / 13.8 ms. Also measured
+  // slower and removed: 8 sources per inner iteration, split accumulators (14.0 ms), and
+  // a persistent one-CTA-per-SM kernel walking its parents through two staging slots
+  // without CTA barriers (15.0 / 16.8 ms with 16 / 24 warps: with one parent of
+  // look-ahead its warps idle at the same unit-granularity tails).
   static const int variant = [] {
     const char* e = std::getenv("FMMGPU_P2P_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
   int sms = 148;
   FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-  const bool flow = (variant == 6 || variant == 7) && np >= 2u * static_cast<uint32_t>(sms);
-  if (flow) {
-    const unsigned grid = static_cast<unsigned>(sms);
-    if (variant == 7) run(k_p2p_flow<24>, 24, static_cast<int>(sizeof(FlowSmem<24>)), grid);
-    else run(k_p2p_flow<16>, 16, static_cast<int>(sizeof(FlowSmem<16>)), grid);
-    a.only_big = 1;  // the (rare) oversized neighbourhoods, chunked
-    run(k_p2p<12>, 12, static_cast<int>(sizeof(P2PSmem<12>)), np);
-    return;
-  }
   // few parents (shallow trees, big leaves): several CTAs per parent share its units
   // (each re-stages the neighbourhood) so the grid still covers 2 CTAs per SM
   uint32_t usplit = 1;

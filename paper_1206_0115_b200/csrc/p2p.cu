@@ -294,7 +294,9 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   };
   // FMMGPU_P2P_VARIANT (tuning experiments): 0 = 12 warps per CTA (default), 2 = 16, 3 = 8.
   // Config B before the chunked partial passes: 13.7 / 13.9 / 13.8 ms. Also measured
-  // slower and removed: 8 sources per inner iteration, split accumulators (14.0 ms), and
+  // slower and removed: 8 sources per inner iteration, split accumulators (14.0 ms), two
+  // targets per lane sharing each source load (12.9 / 13.0 ms with 8 / 12 warps vs 12.86
+  // after the chunked partial passes), and
   // a persistent one-CTA-per-SM kernel walking its parents through two staging slots
   // without CTA barriers (15.0 / 16.8 ms with 16 / 24 warps: with one parent of
   // look-ahead its warps idle at the same unit-granularity tails).

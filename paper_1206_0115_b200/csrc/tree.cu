@@ -159,16 +159,43 @@ __global__ void k_equal_key_runs(const uint64_t* __restrict__ keys, const uint32
   }
 }
 
-__global__ void k_shift3(const uint64_t* __restrict__ in, uint32_t n, uint64_t* __restrict__ out) {
+// Parent levels without host round trips (geometry.cpp:138-153 semantics): level v's
+// cells are the runs of leaf_code >> 3 (leaf - v) over the R sorted leaf codes; idx_v[i]
+// (inclusive scan of the run-start flags) is the 1-based level-v cell of leaf i, so
+// parent / first_child / child_count follow from the leaf ranges of the cells. Arrays
+// are sized R (an upper bound); the cell counts come back in one readback at the end.
+__global__ void k_level_flags(const uint64_t* __restrict__ lc, uint32_t R, int shift, uint32_t* __restrict__ flag) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = in[i] >> 3;
+  if (i < R) flag[i] = (i == 0 || (lc[i] >> shift) != (lc[i - 1] >> shift)) ? 1u : 0u;
 }
-
-__global__ void k_set_parent(const uint32_t* __restrict__ first_child, const uint32_t* __restrict__ child_count,
-                             uint32_t nparents, uint32_t* __restrict__ parent_of_child) {
+__global__ void k_level_cells(const uint64_t* __restrict__ lc, uint32_t R, int shift, const uint32_t* __restrict__ idx,
+                              uint64_t* __restrict__ code, uint32_t* __restrict__ leafstart, uint32_t* __restrict__ n_out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= R) return;
+  if (i == 0 || idx[i] != idx[i - 1]) {
+    code[idx[i] - 1] = lc[i] >> shift;
+    leafstart[idx[i] - 1] = i;
+  }
+  if (i == R - 1) *n_out = idx[i];
+}
+// idx_c == nullptr: the children are the leaves themselves (idx = i + 1)
+__global__ void k_level_children(const uint32_t* __restrict__ leafstart, const uint32_t* __restrict__ n_v, uint32_t R,
+                                 const uint32_t* __restrict__ idx_c, uint32_t* __restrict__ first_child,
+                                 uint32_t* __restrict__ child_count) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nparents) return;
-  for (uint32_t c = first_child[p]; c < first_child[p] + child_count[p]; ++c) parent_of_child[c] = p;
+  const uint32_t n = *n_v;
+  if (p >= n) return;
+  const uint32_t ls = leafstart[p], le = (p + 1 < n ? leafstart[p + 1] : R) - 1;
+  const uint32_t a = idx_c ? idx_c[ls] : ls + 1, b = idx_c ? idx_c[le] : le + 1;
+  first_child[p] = a - 1;
+  child_count[p] = b - a + 1;
+}
+// leafstart_c == nullptr: the child level is the leaf level (cell j = leaf j, R cells)
+__global__ void k_level_parent(const uint32_t* __restrict__ leafstart_c, const uint32_t* __restrict__ n_c, uint32_t R,
+                               const uint32_t* __restrict__ idx_v, uint32_t* __restrict__ parent_c) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= (n_c ? *n_c : R)) return;
+  parent_c[j] = idx_v[leafstart_c ? leafstart_c[j] : j] - 1;
 }
 
 __global__ void k_fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
@@ -399,18 +426,17 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, keys_sorted, L.code, L.particle_count, d_runs,
                                                 static_cast<int>(n), s));
   };
-  uint64_t* keys64 = nullptr;  // kept: the parent-level loop reuses it as scratch
   if (3 * leaf <= 32) {
     uint32_t* k32 = dalloc<uint32_t>(c, n, s);
     uint32_t* k32s = dalloc<uint32_t>(c, n, s);
     sort_and_encode(k32, k32s);
     dfree(c, k32, s);
     dfree(c, k32s, s);
-    keys64 = dalloc<uint64_t>(c, n, s);
   } else {
-    keys64 = dalloc<uint64_t>(c, n, s);
+    uint64_t* k64 = dalloc<uint64_t>(c, n, s);
     uint64_t* k64s = dalloc<uint64_t>(c, n, s);
-    sort_and_encode(keys64, k64s);
+    sort_and_encode(k64, k64s);
+    dfree(c, k64, s);
     dfree(c, k64s, s);
   }
   uint32_t runs = 0;
@@ -449,37 +475,57 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   }
 
   trace("leaf level");
-  // parent levels by code >> 3 (geometry.cpp:138-153)
-  uint64_t* shifted = keys64;  // reuse
+  // parent levels (geometry.cpp:138-153), on the device only
+  const uint32_t R = runs;
+  uint32_t* d_counts = dalloc<uint32_t>(c, 22, s);
+  uint32_t* runflag = dalloc<uint32_t>(c, R, s);
+  uint32_t* idx_c = nullptr;        // level v + 1 (nullptr: the leaf level)
+  uint32_t* leafstart_c = nullptr;
   for (int v = leaf - 1; v >= 0; --v) {
     Level& C = c->lv[v + 1];
     Level& P = c->lv[v];
-    k_shift3<<<blocks(C.n, 256), 256, 0, s>>>(C.code, C.n, shifted);
-    P.code = dalloc<uint64_t>(c, C.n, s);
-    P.child_count = dalloc<uint32_t>(c, C.n, s);
-    FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, shifted, P.code, P.child_count, d_runs, static_cast<int>(C.n), s));
-    FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, shifted, P.code, P.child_count, d_runs, static_cast<int>(C.n), s));
-    runs = *static_cast<const uint32_t*>(readback(c, d_runs, 4, s));
-    P.n = runs;
-    P.first_child = dalloc<uint32_t>(c, runs, s);
-    FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, P.child_count, P.first_child, static_cast<int>(runs), s));
-    FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, P.child_count, P.first_child, static_cast<int>(runs), s));
-    k_set_parent<<<blocks(runs, 256), 256, 0, s>>>(P.first_child, P.child_count, runs, C.parent);
-    P.first_particle = dalloc<uint32_t>(c, runs, s);
-    P.particle_count = dalloc<uint32_t>(c, runs, s);
-    P.parent = dalloc<uint32_t>(c, runs, s);
-    FMM_CUDA(cudaMemsetAsync(P.first_particle, 0, 4ull * runs, s));
-    FMM_CUDA(cudaMemsetAsync(P.particle_count, 0, 4ull * runs, s));
-    FMM_CUDA(cudaMemsetAsync(P.parent, 0, 4ull * runs, s));
+    const int shift = 3 * (leaf - v);
+    uint32_t* idx_v = dalloc<uint32_t>(c, R, s);
+    uint32_t* leafstart_v = dalloc<uint32_t>(c, R, s);
+    k_level_flags<<<blocks(R, 256), 256, 0, s>>>(L.code, R, shift, runflag);
+    FMM_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, runflag, idx_v, static_cast<int>(R), s));
+    FMM_CUDA(cub::DeviceScan::InclusiveSum(scratch(c, tb), tb, runflag, idx_v, static_cast<int>(R), s));
+    P.code = dalloc<uint64_t>(c, R, s);
+    k_level_cells<<<blocks(R, 256), 256, 0, s>>>(L.code, R, shift, idx_v, P.code, leafstart_v, d_counts + v);
+    P.first_child = dalloc<uint32_t>(c, R, s);
+    P.child_count = dalloc<uint32_t>(c, R, s);
+    k_level_children<<<blocks(R, 256), 256, 0, s>>>(leafstart_v, d_counts + v, R, idx_c, P.first_child,
+                                                    P.child_count);
+    k_level_parent<<<blocks(R, 256), 256, 0, s>>>(leafstart_c, idx_c ? d_counts + v + 1 : nullptr, R, idx_v,
+                                                  C.parent);
+    P.first_particle = dalloc<uint32_t>(c, R, s);
+    P.particle_count = dalloc<uint32_t>(c, R, s);
+    P.parent = dalloc<uint32_t>(c, R, s);
+    FMM_CUDA(cudaMemsetAsync(P.first_particle, 0, 4ull * R, s));
+    FMM_CUDA(cudaMemsetAsync(P.particle_count, 0, 4ull * R, s));
+    FMM_CUDA(cudaMemsetAsync(P.parent, 0, 4ull * R, s));
     FMM_CUDA(cudaGetLastError());
+    if (idx_c) dfree(c, idx_c, s);
+    if (leafstart_c) dfree(c, leafstart_c, s);
+    idx_c = idx_v;
+    leafstart_c = leafstart_v;
   }
-  dfree(c, keys64, s);
+  if (idx_c) dfree(c, idx_c, s);
+  if (leafstart_c) dfree(c, leafstart_c, s);
+  dfree(c, runflag, s);
+  if (leaf > 0) {
+    const uint32_t* hc = static_cast<const uint32_t*>(readback(c, d_counts, leaf * sizeof(uint32_t), s));
+    for (int v = 0; v < leaf; ++v) c->lv[v].n = hc[v];
+  }
+  dfree(c, d_counts, s);
   dfree(c, idx, s);
   dfree(c, d_runs, s);
 
   trace("parent levels");
   // blocks of group_size cells (geometry.cpp:155-160); lookup maps; parity classes;
-  // expansions (cell-major, stride ldE, zero padding)
+  // expansions (cell-major, stride ldE, zero padding). The class offsets of every level
+  // and the error flag come back in one readback at the end.
+  uint32_t* d_offs = dalloc<uint32_t>(c, 9 * height + 1, s);
   for (int v = 0; v < height; ++v) {
     Level& V = c->lv[v];
     V.block_offsets.clear();
@@ -500,10 +546,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
       k_octant<<<blocks(V.n, 256), 256, 0, s>>>(V.code, V.n, oct, iota);
       FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, oct, oct_sorted, iota, V.cls_cells, static_cast<int>(V.n), 0, 3, s));
       FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, oct, oct_sorted, iota, V.cls_cells, static_cast<int>(V.n), 0, 3, s));
-      uint32_t* d_off = dalloc<uint32_t>(c, 9, s);
-      k_class_offsets<<<1, 32, 0, s>>>(oct_sorted, V.n, d_off);
-      std::memcpy(V.cls_off, readback(c, d_off, 9 * sizeof(uint32_t), s), 9 * sizeof(uint32_t));
-      dfree(c, d_off, s);
+      k_class_offsets<<<1, 32, 0, s>>>(oct_sorted, V.n, d_offs + 9 * v);
       dfree(c, oct, s);
       dfree(c, oct_sorted, s);
       dfree(c, iota, s);
@@ -538,8 +581,11 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     FMM_CUDA(cudaMemsetAsync(c->d_far, 0, 32 * n, s));
   }
 
-  int flag = 0;
-  flag = *static_cast<const int*>(readback(c, c->d_flag, 4, s));
+  k_copy_words<<<1, 32, 0, s>>>(reinterpret_cast<const uint32_t*>(c->d_flag), 1, d_offs + 9 * height);
+  const uint32_t* h_offs = static_cast<const uint32_t*>(readback(c, d_offs, (9 * height + 1) * sizeof(uint32_t), s));
+  for (int v = 2; v < height; ++v) std::memcpy(c->lv[v].cls_off, h_offs + 9 * v, 9 * sizeof(uint32_t));
+  const int flag = static_cast<int>(h_offs[9 * height]);
+  dfree(c, d_offs, s);
   trace("fields+flag sync");
   if (flag & 1) {
     tree_free(c);

@@ -88,8 +88,10 @@ int fmmgpu_m2l(fmmgpu_ctx* ctx, int level);         /* bench.cpp:288-299, level 
 int fmmgpu_l2l(fmmgpu_ctx* ctx, int parent_level);  /* bench.cpp:300-316, level 2..leaf-1 */
 int fmmgpu_l2p(fmmgpu_ctx* ctx);                    /* bench.cpp:317-336 */
 int fmmgpu_p2p(fmmgpu_ctx* ctx);                    /* bench.cpp:337-342: P2P + P2PREDUCE */
-/* reset, then the whole DAG as a level-synchronous two-stream schedule
- * (far field on one stream, near field concurrently on another). */
+/* The whole DAG (execute over the task graph, runtime.cpp:91-216) as a level-synchronous
+ * two-stream schedule: far field on one stream, near field concurrently on another. The
+ * result equals fmmgpu_reset followed by every operator; unpartitioned evaluations write
+ * each output once (same sums) instead of clearing and accumulating. */
 int fmmgpu_evaluate(fmmgpu_ctx* ctx);
 int fmmgpu_synchronize(fmmgpu_ctx* ctx);
 

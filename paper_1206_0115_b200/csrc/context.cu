@@ -384,7 +384,8 @@ void record(fmmgpu_ctx* c, cudaEvent_t e, cudaStream_t s) {
   else FMM_CUDA(cudaEventRecord(e, s));
 }
 
-// One evaluation: reset, then the DAG as a level-synchronous two-stream schedule.
+// One evaluation: the DAG as a level-synchronous two-stream schedule (unpartitioned:
+// every operator writes its output once; partitioned: clear, then accumulate).
 // trace span around one launch (eager evaluations with tracing on)
 struct Span {
   fmmgpu_ctx* c;

@@ -335,6 +335,9 @@ def run_ours(args, world, rank, local):
             "flop_convention": "reference ledger (bench.hpp:49-53): 15 flop per directional interaction "
                                "(the kernel issues 18 FP64 instructions per interaction, so frac <= 0.45 at "
                                "a saturated FP64 pipe)",
+            # the same launch against the FP64 instruction issue rate (DFMA peak / 2 flop):
+            # useful interactions x 18 DP instructions / duration
+            "fp64_instr_frac": (ledger["near_directional"] * 18 / (iso["P2P"] / 1e3)) / (FP64_DFMA_TFLOPS * 1e12 / 2),
             "m2l": {"bound": "tensor (FP64 DMMA)", "ms_all_levels": iso["M2L"], "ms_leaf": iso_m2l_leaf,
                     "achieved": per_op["M2L"]["tflops"], "peak": FP64_DMMA_TFLOPS,
                     "frac": per_op["M2L"]["frac"]},

@@ -229,6 +229,7 @@ struct GemmArgs {
   double* local;          // phase B output (local_own)
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
   int msplit;             // phase A M-split factor (coarse levels)
+  int cls_fast;           // phase A grid: parity class in blockIdx.x (else blockIdx.y)
   int ow;                 // phase B: write local_own instead of accumulating (evaluation)
   double* part;           // phase B split-K partials [ksplit][ncells][ldE]
   uint32_t ncells;
@@ -382,9 +383,12 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   __shared__ uint32_t col_cell[BN];
   __shared__ int col_ijk[BN][3];
 
-  const int cls = blockIdx.y;
+  // class-fastest CTA order (g.cls_fast): the 8 parity classes of one spatial block run
+  // back to back, so the neighbouring blocks of a target's Yt row (written by sources of
+  // different parities) are completed while their sectors are still in L2
+  const int cls = g.cls_fast ? blockIdx.x : blockIdx.y;
   const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
-  const uint32_t n0 = blockIdx.x * BN;
+  const uint32_t n0 = (g.cls_fast ? blockIdx.y : blockIdx.x) * BN;
   if (n0 >= ncls) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp / WN, wn = warp % WN;
@@ -716,7 +720,12 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       }();
       while (ms < mtiles && ncols * ms < waves * 2u * 148u) ++ms;
       g.msplit = ms;
-      dim3 grid((maxcls + bn - 1) / bn, 8, ms);
+      static const int cls_fast = [] {  // FMMGPU_M2L_CLS_FAST=0: class-slowest order (A/B aid)
+        const char* e = std::getenv("FMMGPU_M2L_CLS_FAST");
+        return e ? std::atoi(e) : 1;
+      }();
+      g.cls_fast = cls_fast;
+      dim3 grid = cls_fast ? dim3(8, (maxcls + bn - 1) / bn, ms) : dim3((maxcls + bn - 1) / bn, 8, ms);
       kern<<<grid, PA_THREADS, smem, s>>>(g);
       FMM_CUDA(cudaGetLastError());
     };

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python tools/eval_ab.py FMMGPU_M2L_CLS_FAST 0 1 0 1 > gpurun_out/eval_ab.log 2>&1
+timeout 600 python tools/op_variants.py FMMGPU_M2L_CLS_FAST M2L 6 0 1 > gpurun_out/op.log 2>&1

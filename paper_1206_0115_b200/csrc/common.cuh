@@ -157,8 +157,9 @@ struct M2LTables {
 // Device blocks of a context recycled across tree builds (cudaMallocAsync of the
 // 80-320 MB tree arrays costs 0.2-2 ms per call, occasionally far more)
 struct DevCache {
-  std::unordered_map<void*, size_t> live;  // block -> capacity
-  std::multimap<size_t, void*> idle;       // capacity -> free block
+  std::unordered_map<void*, size_t> live;                  // block -> capacity
+  std::multimap<size_t, std::pair<void*, uint64_t>> idle;  // capacity -> {free block, epoch freed}
+  uint64_t epoch = 0;                                      // one per tree build
 };
 
 struct Timing {
@@ -280,6 +281,9 @@ void* scratch(fmmgpu_ctx* c, size_t bytes);
 void* cache_alloc(fmmgpu_ctx* c, size_t bytes, cudaStream_t s);
 void cache_free(fmmgpu_ctx* c, void* p, cudaStream_t s);  // blocks it did not allocate: cudaFreeAsync
 void cache_trim(fmmgpu_ctx* c, cudaStream_t s);            // release the idle blocks
+// release the idle blocks freed before the current epoch (the previous tree's arrays
+// this build did not reuse); the build's own temporaries stay for the next build
+void cache_trim_old(fmmgpu_ctx* c, cudaStream_t s);
 constexpr size_t READBACK_CAP = 64 * 1024;
 // copies `bytes` (multiple of 4, <= READBACK_CAP) of device memory to host through the
 // mapped buffer, synchronizing s; the returned host pointer is valid until the next call

@@ -267,7 +267,7 @@ void* cache_alloc(fmmgpu_ctx* c, size_t bytes, cudaStream_t s) {
   auto& C = c->cache;
   auto it = C.idle.lower_bound(bytes);
   if (it != C.idle.end() && it->first <= bytes + bytes / 4 + (size_t(1) << 20)) {
-    void* p = it->second;
+    void* p = it->second.first;
     C.live[p] = it->first;
     C.idle.erase(it);
     return p;
@@ -290,13 +290,25 @@ void cache_free(fmmgpu_ctx* c, void* p, cudaStream_t s) {
     cudaFreeAsync(p, s);
     return;
   }
-  C.idle.emplace(it->second, p);
+  C.idle.emplace(it->second, std::make_pair(p, C.epoch));
   C.live.erase(it);
 }
 
 void cache_trim(fmmgpu_ctx* c, cudaStream_t s) {
-  for (auto& kv : c->cache.idle) cudaFreeAsync(kv.second, s);
+  for (auto& kv : c->cache.idle) cudaFreeAsync(kv.second.first, s);
   c->cache.idle.clear();
+}
+
+void cache_trim_old(fmmgpu_ctx* c, cudaStream_t s) {
+  auto& C = c->cache;
+  for (auto it = C.idle.begin(); it != C.idle.end();) {
+    if (it->second.second < C.epoch) {
+      cudaFreeAsync(it->second.first, s);
+      it = C.idle.erase(it);
+    } else {
+      ++it;
+    }
+  }
 }
 
 void* scratch(fmmgpu_ctx* c, size_t bytes) {
@@ -341,6 +353,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   partition_free(c);
   tree_free(c);
   lists_free(c);
+  ++c->cache.epoch;
   trace("free");
 
   // input -> device (input order); a pipelined run (fmmgpu_run_async) has already
@@ -596,7 +609,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     throw Error(FMMGPU_DOMAIN_ERROR, "GroupTree: coincident particles");
   }
   c->have_tree = true;
-  cache_trim(c, s);  // blocks of the previous tree this one did not reuse
+  cache_trim_old(c, s);  // blocks of the previous tree this one did not reuse
 }
 
 }  // namespace fmmgpu

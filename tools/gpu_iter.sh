@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python tools/eval_ab.py FMMGPU_M2L_CLS_FAST 0 1 0 1 > gpurun_out/eval_ab.log 2>&1
-timeout 600 python tools/op_variants.py FMMGPU_M2L_CLS_FAST M2L 6 0 1 > gpurun_out/op.log 2>&1
+FMMGPU_TRACE=1 PROBE_CFG=D timeout 600 python tools/e2e_probe.py > gpurun_out/e2e_probe_D.log 2>&1
+timeout 900 python bench.py --config D --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_D.json 2> gpurun_out/bench_D.err

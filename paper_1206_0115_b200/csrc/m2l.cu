@@ -364,8 +364,9 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
 // runs across M-tile boundaries, so the scatter epilogue of one M-tile overlaps the
 // loads of the next and no CTA pays a pipeline ramp per 64 x 64 tile.
 // Tiles: l <= 5: 64-row M-tiles, 4-stage ring, 64 resident columns (W 68 KB + ring 40 KB);
-// larger orders: 128-row M-tiles, 3 stages, 16 columns (l = 7: W 46 KB + ring 61 KB), so
-// two CTAs still fit on an SM. The epilogue tables are built for the M-tile in use.
+// l = 6, 7: 128-row M-tiles, 2 stages, 24 columns (l = 7: W 68 KB + ring 41 KB); larger
+// orders: 128-row M-tiles, 3 stages, 16 columns, so two CTAs still fit on an SM. The
+// epilogue tables are built for the M-tile in use.
 constexpr int PA_BK = 16, PA_THREADS = 256;
 constexpr int PA_SPAD = PA_BK + 4;  // == 4 (mod 16)
 
@@ -584,8 +585,10 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   }
   T.R = R;
   T.ldY = round_up(R, 32);
-  // 64-row M-tiles x 64 resident columns, 4-stage ring for l <= 5; 128 x 16, 3 stages
-  // above. Measured at the config-B leaf (phase A + B): 128 x 64 / 2 stages 15.9 ms,
+  // 64-row M-tiles x 64 resident columns, 4-stage ring for l <= 5; 128 x 24, 2 stages
+  // for l = 6, 7; 128 x 16, 3 stages above. Config C (l = 7) per evaluation: 128 x 16 / 3
+  // stages 96.9 ms, 64 x 32 / 2 stages 95.8 (16 x 16 warp tiles) or 95.1 (32 x 8), 128 x 24
+  // / 2 stages 94.0. Measured at the config-B leaf (phase A + B): 128 x 64 / 2 stages 15.9 ms,
   // 128 x 32 / 3 stages 12.6 ms, vs 11.9 ms for 64 x 64 / 4 stages.
   T.bmA = c->ldE <= 128 ? 64 : 128;
   T.rowsA = round_up(R, T.bmA);
@@ -730,6 +733,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       FMM_CUDA(cudaGetLastError());
     };
     if (T.bmA == 64) launch(k_m2l_phase_a<64, 4, 64, 2, 4>, 64, 64, 4);
+    else if (c->ldE <= 352) launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
     else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
   }
   g.cls_cells = L.tgtB ? L.tgtB : L.cls_cells;

@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
   const int wpad = g.K + 4;                       // == 4 (mod 16): conflict-free fragments
   double* Ws = smem;                              // [BN][wpad]
   double* As = smem + BN * wpad;                  // [PA_ST][PA_BM][PA_SPAD]
-  // [2][vtMax][BN] target cell of (vector of the M-tile, column), double-buffered by M-tile
+  // [vtMax][BN] target cell of (vector of the M-tile, column): filled at k-slice KT/2 of a
+  // tile, read by its epilogue; a __syncthreads separates that epilogue from the next fill
   uint32_t* tgt = reinterpret_cast<uint32_t*>(As + PA_ST * PA_BM * PA_SPAD);
   __shared__ uint32_t col_cell[BN];
   __shared__ int col_ijk[BN][3];
@@ -459,7 +460,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g)
     __syncthreads();
     if (t + PA_ST - 1 < TOTAL) load_next();
     cp_commit();
-    uint32_t* tg = tgt + (mt & 1) * g.vtMax * BN;
+    uint32_t* tg = tgt;
     if (kt == 0) {
 #pragma unroll
       for (int i = 0; i < MT; ++i) rowinfo[i] = __ldg(g.rowA + cls * g.rowsA + mt * PA_BM + wm * WTM + i * 8 + gq);
@@ -588,7 +589,8 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   // 64-row M-tiles x 64 resident columns, 4-stage ring for l <= 5; 128 x 24, 2 stages
   // for l = 6, 7; 128 x 16, 3 stages above. Config C (l = 7) per evaluation: 128 x 16 / 3
   // stages 96.9 ms, 64 x 32 / 2 stages 95.8 (16 x 16 warp tiles) or 95.1 (32 x 8), 128 x 24
-  // / 2 stages 94.0. Measured at the config-B leaf (phase A + B): 128 x 64 / 2 stages 15.9 ms,
+  // / 2 stages 94.0. Config B with 128 x 64 / 2 stages (32 x 32 warp tiles): 27.90 vs
+  // 27.78 ms per evaluation. Measured at the config-B leaf (phase A + B): 128 x 64 / 2 stages 15.9 ms,
   // 128 x 32 / 3 stages 12.6 ms, vs 11.9 ms for 64 x 64 / 4 stages.
   T.bmA = c->ldE <= 128 ? 64 : 128;
   T.rowsA = round_up(R, T.bmA);
@@ -711,7 +713,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
     auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST) {
       const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * PA_SPAD) +
-                          sizeof(uint32_t) * 2 * size_t(T.vtMax) * bn;
+                          sizeof(uint32_t) * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       // M-split so coarse levels still put >= 2 CTAs on every SM
       const uint32_t ncols = 8u * ((maxcls + bn - 1) / bn);

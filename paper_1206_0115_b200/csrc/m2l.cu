@@ -363,15 +363,16 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
 // M1_p (R rows) streams past them in BM x BK slices through a cp.async ring that
 // runs across M-tile boundaries, so the scatter epilogue of one M-tile overlaps the
 // loads of the next and no CTA pays a pipeline ramp per 64 x 64 tile.
-// Tiles: l <= 5: 64-row M-tiles, 4-stage ring, 64 resident columns (W 68 KB + ring 40 KB);
+// Tiles: l <= 5: 64-row M-tiles, 2-stage ring of 32-wide k-slices, 64 resident columns
+// (W 68 KB + ring 37 KB);
 // l = 6, 7: 128-row M-tiles, 2 stages, 24 columns (l = 7: W 68 KB + ring 41 KB); larger
 // orders: 128-row M-tiles, 3 stages, 16 columns, so two CTAs still fit on an SM. The
 // epilogue tables are built for the M-tile in use.
-constexpr int PA_BK = 16, PA_THREADS = 256;
-constexpr int PA_SPAD = PA_BK + 4;  // == 4 (mod 16)
+constexpr int PA_THREADS = 256;
 
-template <int PA_BM, int PA_ST, int BN, int WM, int WN>
+template <int PA_BM, int PA_ST, int BN, int WM, int WN, int PA_BK = 16>
 __global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g) {
+  constexpr int PA_SPAD = PA_BK + 4;  // == 4 (mod 16): conflict-free fragments
   static_assert(WM * WN * 32 == PA_THREADS, "8 warps");
   constexpr int WTM = PA_BM / WM, WTN = BN / WN;
   constexpr int MT = WTM / 8, NT = WTN / 8;
@@ -586,7 +587,8 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   }
   T.R = R;
   T.ldY = round_up(R, 32);
-  // 64-row M-tiles x 64 resident columns, 4-stage ring for l <= 5; 128 x 24, 2 stages
+  // 64-row M-tiles x 64 resident columns, 2-stage ring of 32-wide k-slices for l <= 5;
+  // 128 x 24, 2-stage ring of 16-wide slices
   // for l = 6, 7; 128 x 16, 3 stages above. Config C (l = 7) per evaluation: 128 x 16 / 3
   // stages 96.9 ms, 64 x 32 / 2 stages 95.8 (16 x 16 warp tiles) or 95.1 (32 x 8), 128 x 24
   // / 2 stages 94.0. Config B with 128 x 64 / 2 stages (32 x 32 warp tiles): 27.90 vs
@@ -711,8 +713,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.a_class_stride = size_t(T.rowsA) * c->ldE;
     g.K = c->ldE;
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
-    auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST) {
-      const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * PA_SPAD) +
+    auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST, int bk = 16) {
+      const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * (bk + 4)) +
                           sizeof(uint32_t) * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       // M-split so coarse levels still put >= 2 CTAs on every SM
@@ -734,7 +736,10 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       kern<<<grid, PA_THREADS, smem, s>>>(g);
       FMM_CUDA(cudaGetLastError());
     };
-    if (T.bmA == 64) launch(k_m2l_phase_a<64, 4, 64, 2, 4>, 64, 64, 4);
+    // l <= 5: 32-wide k-slices through a 2-stage ring (config B: 27.26 vs 27.81 ms per
+    // evaluation with 16-wide slices and 4 stages; a 3-stage 32-wide ring no longer fits
+    // two CTAs per SM)
+    if (T.bmA == 64) launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
     else if (c->ldE <= 352) launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
     else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
   }

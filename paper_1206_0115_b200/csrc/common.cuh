@@ -251,6 +251,12 @@ struct fmmgpu_ctx {
   uint32_t yt_keep_n[22] = {};
   uint64_t pipe_cap = 0;
   uint64_t pipe_k = 0;
+  // the D2H of the last enqueued step is issued after the NEXT step's tree build, so the
+  // build's small readbacks do not share the device->host PCIe direction with it
+  bool pipe_pend = false;
+  int pend_slot = 0;
+  uint64_t pend_n = 0, pend_k = 0;
+  double* pend_dst[4] = {};
 };
 
 namespace fmmgpu {

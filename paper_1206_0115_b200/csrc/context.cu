@@ -746,6 +746,21 @@ void pipe_trace_dump() {
 // work of one step is unchanged (tree build, evaluate, gather); only the PCIe copies
 // leave the critical path.
 namespace {
+// Issue the deferred D2H of the last enqueued step (if any).
+void pipe_issue_d2h(fmmgpu_ctx* c) {
+  if (!c->pipe_pend) return;
+  const int slot = c->pend_slot;
+  FMM_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_out_ready[slot], 0));
+  pipe_mark("d2h start", c->pend_k, c->s_d2h);
+  for (int i = 0; i < 4; ++i)
+    if (c->pend_dst[i])
+      FMM_CUDA(cudaMemcpyAsync(c->pend_dst[i], c->pipe_out[slot] + i * c->pend_n, 8 * c->pend_n,
+                               cudaMemcpyDeviceToHost, c->s_d2h));
+  FMM_CUDA(cudaEventRecord(c->ev_d2h_done[slot], c->s_d2h));
+  pipe_mark("d2h end", c->pend_k, c->s_d2h);
+  c->pipe_pend = false;
+}
+
 // One pipelined step on context c (its own copy streams, events and output slots).
 void pipe_step(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, int group, double* pot, double* fx,
                double* fy, double* fz) {
@@ -762,6 +777,7 @@ void pipe_step(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, int gr
     FMM_CUDA(cudaEventRecord(c->ev_in_free, c->s_far));
   }
   if (c->d_in_cap < n || c->pipe_cap < n) {  // grow: drain the pipeline first
+    pipe_issue_d2h(c);
     FMM_CUDA(cudaStreamSynchronize(c->s_h2d));
     FMM_CUDA(cudaStreamSynchronize(c->s_d2h));
     FMM_CUDA(cudaStreamSynchronize(c->s_near));
@@ -792,6 +808,7 @@ void pipe_step(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, int gr
   tree_build(c, reinterpret_cast<const double*>(c->d_in), n, true, height, group, nullptr);
   FMM_CUDA(cudaEventRecord(c->ev_in_free, c->s_far));
   pipe_mark("tree end", c->pipe_k, c->s_far);
+  pipe_issue_d2h(c);  // the previous step's fields, under this step's evaluation
   const int slot = static_cast<int>(c->pipe_k & 1);
   FMM_CUDA(cudaStreamWaitEvent(c->s_far, c->ev_d2h_done[slot], 0));
   double* own_out = c->d_out;
@@ -802,14 +819,14 @@ void pipe_step(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, int gr
   if (rc != FMMGPU_OK) throw Error(rc, c->err);
   FMM_CUDA(cudaEventRecord(c->ev_out_ready[slot], c->s_far));
   pipe_mark("eval end", c->pipe_k, c->s_far);
-  FMM_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_out_ready[slot], 0));
-  pipe_mark("d2h start", c->pipe_k, c->s_d2h);
-  double* dst[4] = {pot, fx, fy, fz};
-  for (int i = 0; i < 4; ++i)
-    if (dst[i])
-      FMM_CUDA(cudaMemcpyAsync(dst[i], c->pipe_out[slot] + i * n, 8 * n, cudaMemcpyDeviceToHost, c->s_d2h));
-  FMM_CUDA(cudaEventRecord(c->ev_d2h_done[slot], c->s_d2h));
-  pipe_mark("d2h end", c->pipe_k, c->s_d2h);
+  c->pipe_pend = true;
+  c->pend_slot = slot;
+  c->pend_n = n;
+  c->pend_k = c->pipe_k;
+  c->pend_dst[0] = pot;
+  c->pend_dst[1] = fx;
+  c->pend_dst[2] = fy;
+  c->pend_dst[3] = fz;
   ++c->pipe_k;
 }
 
@@ -828,6 +845,7 @@ int fmmgpu_run_async(fmmgpu_ctx* c, const double* xyzw, uint64_t n, int height, 
 int fmmgpu_run_wait(fmmgpu_ctx* c) {
   return guarded(c, [&] {
     FMM_CUDA(cudaSetDevice(c->device));
+    pipe_issue_d2h(c);
     if (c->s_d2h) FMM_CUDA(cudaStreamSynchronize(c->s_d2h));
     if (c->s_h2d) FMM_CUDA(cudaStreamSynchronize(c->s_h2d));
     FMM_CUDA(cudaStreamSynchronize(c->s_near));

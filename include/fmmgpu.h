@@ -94,6 +94,10 @@ int fmmgpu_p2p(fmmgpu_ctx* ctx);                    /* bench.cpp:337-342: P2P + 
  * each output once (same sums) instead of clearing and accumulating. */
 int fmmgpu_evaluate(fmmgpu_ctx* ctx);
 int fmmgpu_synchronize(fmmgpu_ctx* ctx);
+/* Replay evaluations from a captured CUDA graph (captured after one eager run; rebuilt
+ * after tree, partition or operator changes). Off by default (FMMGPU_GRAPH=1 turns it on
+ * for new contexts): eager launches on the two prioritised streams measured faster. */
+int fmmgpu_set_graph(fmmgpu_ctx* ctx, int on);
 
 /* FmmContext::gather (bench.cpp:350-365): fields in input order into HOST or DEVICE
  * arrays of n doubles each (any may be NULL). Synchronizes. */

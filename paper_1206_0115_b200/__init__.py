@@ -85,6 +85,7 @@ def lib():
         L.fmmgpu_run_async.argtypes = L.fmmgpu_run.argtypes
         L.fmmgpu_run_wait.argtypes = [c_void_p]
         L.fmmgpu_set_trace.argtypes = [c_void_p, c_int]
+        L.fmmgpu_set_graph.argtypes = [c_void_p, c_int]
         L.fmmgpu_trace_spans.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p]
         for name in ("fmmgpu_reset", "fmmgpu_p2m", "fmmgpu_l2p", "fmmgpu_p2p", "fmmgpu_evaluate",
                      "fmmgpu_synchronize", "fmmgpu_build_lists"):
@@ -422,6 +423,10 @@ class FmmContext:
 
     def run_wait(self):
         self._check(self._lib.fmmgpu_run_wait(self.h))
+
+    def set_graph(self, on: bool = True):
+        """Replay evaluations from a captured CUDA graph (fmmgpu_set_graph)."""
+        self._check(self._lib.fmmgpu_set_graph(self.h, 1 if on else 0))
 
     def set_trace(self, on: bool = True):
         """Per-launch device trace of the following evaluations (fmmgpu_set_trace)."""

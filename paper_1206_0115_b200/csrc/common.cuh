@@ -210,6 +210,7 @@ struct fmmgpu_ctx {
   // captured evaluation (fmmgpu_evaluate): replayed while tree / partition / operators hold
   cudaGraphExec_t graph_exec = nullptr;
   bool graph_warm = false;   // one eager evaluation done since the last invalidation
+  bool use_graph = false;    // replay evaluations as a captured graph (fmmgpu_set_graph)
   bool capturing = false;
   uint64_t graph_launches = 0;
   double* d_splitk = nullptr;  // M2L phase B split-K partials

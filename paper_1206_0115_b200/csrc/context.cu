@@ -133,6 +133,8 @@ void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx
   c->order = order;
   c->eps = eps;
   c->l3 = order * order * order;
+  const char* ge = std::getenv("FMMGPU_GRAPH");
+  c->use_graph = ge && std::atoi(ge) == 1;
   c->ldE = round_up(c->l3, 32);  // multiple of the GEMM k-slice (32)
   FMM_CUDA(cudaSetDevice(device));
   cudaMemPool_t pool;
@@ -486,18 +488,20 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
 
 extern "C" {
 
-// The evaluation's ~25 launches are captured once into a CUDA graph (after one eager
-// run, so every lazy allocation has happened) and replayed while the tree, partition
-// and operators are unchanged (the stream/event schedule as a
-// graph). FMMGPU_NO_GRAPH=1 keeps eager launches. Partitioned runs with an NCCL
-// communicator stay eager.
+// With fmmgpu_set_graph(ctx, 1) (or FMMGPU_GRAPH=1 for new contexts) the evaluation's ~25 launches are captured once into a CUDA graph
+// (after one eager run, so every lazy allocation has happened) and replayed while the
+// tree, partition and operators are unchanged (the stream/event
+// schedule as a graph). Off by default: at config B the replayed graph measured 27.20
+// ms per evaluation against 26.89 ms for eager launches on the two prioritised streams
+// (setting the kernel nodes' priorities after capture did not close the gap), and the
+// host launch cost of ~25 kernels hides under a 27 ms evaluation anyway. Partitioned
+// runs with an NCCL communicator are always eager.
 int fmmgpu_evaluate(fmmgpu_ctx* c) {
   return guarded(c, [&] {
     c->zero_pending = false;  // the evaluation clears its arrays itself
     need_tree(c);
     FMM_CUDA(cudaSetDevice(c->device));
-    static const bool no_graph = std::getenv("FMMGPU_NO_GRAPH") != nullptr;
-    const bool graphable = !no_graph && !(c->part_n > 1 && c->nccl) && !c->trace;
+    const bool graphable = c->use_graph && !(c->part_n > 1 && c->nccl) && !c->trace;
     if (graphable && c->graph_exec) {
       FMM_CUDA(cudaGraphLaunch(c->graph_exec, c->s_far));
       c->launches = c->graph_launches;
@@ -594,6 +598,13 @@ int fmmgpu_timings(const fmmgpu_ctx* cc, double* ms) {
 }
 
 uint64_t fmmgpu_last_launch_count(const fmmgpu_ctx* c) { return c ? c->launches : 0; }
+
+int fmmgpu_set_graph(fmmgpu_ctx* c, int on) {
+  return guarded(c, [&] {
+    c->use_graph = on != 0;
+    fmmgpu_invalidate_graph(c);
+  });
+}
 
 int fmmgpu_set_trace(fmmgpu_ctx* c, int on) {
   return guarded(c, [&] {

@@ -219,6 +219,7 @@ def test_deterministic(fmm):
     after the graph is invalidated by a new tree."""
     xyzw = make_particles(20000, "uniform", 1, True)
     c = ctx_for(fmm, xyzw, 5, 5)
+    c.set_graph(True)
     runs = []
     for _ in range(4):  # eager, eager + capture, replay, replay
         c.evaluate()
@@ -231,6 +232,11 @@ def test_deterministic(fmm):
     assert total > 0 and kinds["P2P"] > 0 and launches == 3 * c.launch_count()
     c.build_tree(xyzw, 5)  # new tree: graph rebuilt
     for _ in range(3):
+        c.evaluate()
+        for x, y in zip(runs[0], c.gather()):
+            assert np.array_equal(x, y)
+    c.set_graph(False)  # the default: eager launches
+    for _ in range(2):
         c.evaluate()
         for x, y in zip(runs[0], c.gather()):
             assert np.array_equal(x, y)

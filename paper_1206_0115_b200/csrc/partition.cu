@@ -22,6 +22,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fmmgpu {
@@ -104,6 +106,10 @@ void partition_free(fmmgpu_ctx* c) {
 
 void exchange_level(fmmgpu_ctx* c, int v, cudaStream_t s) {
   if (c->part_n <= 1 || v < std::max(2, c->part_align)) return;
+  // FMMGPU_PART_NO_EXCHANGE=1 (measurement aid only: wrong fields): time one rank's
+  // partitioned work on a single device without a communicator (tools/scaling_projection.py)
+  static const bool no_exchange = std::getenv("FMMGPU_PART_NO_EXCHANGE") != nullptr;
+  if (no_exchange) return;
   if (!c->nccl) throw Error(FMMGPU_LOGIC_ERROR, "partitioned evaluate needs a communicator (fmmgpu_comm_init) "
                                                 "or the stepped API with a host exchange");
   auto& api = nccl();

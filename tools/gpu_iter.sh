@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python tools/scaling_projection.py B > gpurun_out/scaling_B.json 2> gpurun_out/scaling_B.err
-timeout 1800 python tools/scaling_projection.py E > gpurun_out/scaling_E.json 2> gpurun_out/scaling_E.err
+timeout 900 python tools/eval_ab.py FMMGPU_M2L_PERSIST 0 1 2 0 1 > gpurun_out/eval_ab.log 2>&1
+timeout 600 python tools/op_variants.py FMMGPU_M2L_PERSIST M2L 6 0 1 > gpurun_out/op.log 2>&1

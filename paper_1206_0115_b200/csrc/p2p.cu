@@ -9,10 +9,11 @@
 // shared memory as {x,y,z,w} (8 loads per particle per evaluation instead of 27),
 // each position's segment padded so a child's 27 neighbours read as 9 contiguous runs
 // of whole groups of 4. Work units: every full 32-target pass of every child, then
-// each child's partial last pass; targets sit in registers (one per lane) and every
-// source is a broadcast LDS.128 pair. A partial pass of m < 32 targets splits the
-// sources of each run S = 32 / m ways and combines the S partial sums in a fixed order
-// through shared memory.
+// each child's partial last pass cut into chunks of 16, 8, 4, 2, 1 targets (largest
+// first); targets sit in registers (one per lane) and every source is a broadcast
+// LDS.128 pair. A chunk of m = 2^b targets splits the sources of each run S = 32 / m
+// ways, so every lane works, and combines the S partial sums in a fixed order through
+// shared memory. The evaluation writes near (first staging chunk) instead of adding.
 //
 // k_p2p runs one CTA (12 warps, 2 CTAs per SM) per parent. Neighbourhoods larger than
 // one staging buffer (non-uniform clouds) stream through shared memory in chunks

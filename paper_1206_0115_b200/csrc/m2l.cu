@@ -19,9 +19,11 @@
 //            M1_v over the 189 vectors admissible from a parity-p source; the
 //            epilogue scatters block v of source s to target s - v (if it exists)
 //            into Yt[t] (target-side stacking order);
-//   phase B  local_own[t] += scale * M2_q (l^3 x R) * Yt[t] for targets of parity q.
-//            Yt is one array per level, zeroed once at allocation; the blocks of
-//            absent sources t + v are never written, so they stay exactly zero.
+//   phase B  local_own[t] += scale * M2_q (l^3 x R) * Yt[t] for targets of parity q
+//            (= instead of += inside an evaluation).
+//            Yt is one array per level, zeroed once at allocation (and kept across
+//            tree rebuilds for full levels); the blocks of absent sources t + v are
+//            never written, so they stay exactly zero.
 // Same arithmetic as the reference (4 l^3 r per pair), on DMMA (mma.sync
 // m8n8k4 f64, the B200 FP64 tensor path: 37.2 TF/s measured, profiles/r01_fp64_peaks.txt).
 #include <cusolverDn.h>

@@ -1,12 +1,14 @@
 // Chebyshev transfers on the device (InterpolationEngine, chebyshev.cpp:57-229),
 // one launch per operator per level over all cells of that level:
-//   P2M  CTA per leaf cell; particles staged through shared memory in chunks of 128
-//        as their three 1-D interpolation vectors, then each thread owns l^3/128
-//        coefficients (chebyshev.cpp:116-136).
-//   M2M  CTA per parent: the <=8 children go through the three l x l passes of
-//        tensor_step in shared memory (chebyshev.cpp:181-220), summed in registers.
+//   P2M  warp per leaf cell; particles staged through shared memory in chunks of 32
+//        as their three 1-D interpolation vectors (particle-minor), then lane p owns
+//        the l coefficients of the pair p = (n1, n2) (chebyshev.cpp:116-136).
+//   M2M  CTA per parent, warp per child: the three l x l passes of tensor_step in
+//        shared memory (chebyshev.cpp:181-220), children summed in child order.
 //   L2L  CTA per parent: own+down staged once, pushed into each child
 //        (chebyshev.cpp:222-229, bench.cpp:300-316).
+//   In an evaluation every operator writes its output (P2M and M2M also the zero
+//   padding of the ldE stride) instead of accumulating into cleared arrays.
 //   L2P  thread per particle, the n3 reduction factored as
 //        sum_{n1,n2} (Sx Sy) * sum_{n3} L Sz (and the three gradient variants)
 //        (chebyshev.cpp:138-179, bench.cpp:317-336).

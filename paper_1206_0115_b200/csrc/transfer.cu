@@ -95,84 +95,14 @@ struct LeafArgs {
 constexpr int P2M_THREADS = 128;
 constexpr int P2M_WARPS = P2M_THREADS / 32;
 
-// P2M, warp per leaf cell: lanes evaluate the interpolation vectors of 32 particles
-// at a time into shared memory (a = w Sx, b = Sy, c = Sz, chebyshev.cpp:122-127), then
-// lane p owns the l coefficients W[n1][n2][0..l) of the pair p = (n1, n2) and adds
-// (a[n1] b[n2]) c[n3] for every particle -- the reference's wx, wxy, out += wxy sz
-// product order, l FMAs per pair per particle, with a and b read once per particle.
-template <int L>
-__global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp(LeafArgs a) {
-  constexpr int PP = (L * L + 31) / 32;  // (n1, n2) pairs per lane
-  __shared__ double tn[L * (L - 1) + 1];
-  __shared__ double S[P2M_WARPS][32][3 * L + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < L * (L - 1); i += P2M_THREADS) tn[i] = a.tn[i];
-  __syncthreads();
-  const uint32_t c = a.cell0 + blockIdx.x * P2M_WARPS + warp;
-  if (c >= a.ncells) return;
-  double ctr[3];
-  cell_center(a.geo, a.code[c], ctr);
-  const uint32_t first = a.first[c], cnt = a.count[c];
-  double* out = a.expansion + size_t(c) * a.ldE;
-  // issue the loads of the first two particle chunks and of the accumulated
-  // coefficients together (one memory round trip instead of three)
-  const double4 zero4 = make_double4(0, 0, 0, 0);
-  const double4 q0 = lane < cnt ? a.pw[first + lane] : zero4;
-  const double4 q1 = lane + 32 < cnt ? a.pw[first + 32 + lane] : zero4;
-  double acc[PP][L];
-#pragma unroll
-  for (int i = 0; i < PP; ++i)
-#pragma unroll
-    for (int n = 0; n < L; ++n) acc[i][n] = (!a.ow && lane + 32 * i < L * L) ? out[(lane + 32 * i) * L + n] : 0.0;
-  if (a.ow)
-    for (int i = L * L * L + lane; i < a.ldE; i += 32) out[i] = 0.0;
-  double(*sw)[3 * L + 1] = S[warp];
-  for (uint32_t base = 0; base < cnt; base += 32) {
-    if (base + lane < cnt) {
-      const double4 p = base == 0 ? q0 : base == 32 ? q1 : a.pw[first + base + lane];
-      double s[L];
-      eval_all<L>(tn, (p.x - ctr[0]) * a.geo.inv, s);
-#pragma unroll
-      for (int m = 0; m < L; ++m) sw[lane][m] = p.w * s[m];
-      eval_all<L>(tn, (p.y - ctr[1]) * a.geo.inv, s);
-#pragma unroll
-      for (int m = 0; m < L; ++m) sw[lane][L + m] = s[m];
-      eval_all<L>(tn, (p.z - ctr[2]) * a.geo.inv, s);
-#pragma unroll
-      for (int m = 0; m < L; ++m) sw[lane][2 * L + m] = s[m];
-    }
-    __syncwarp();
-    const int m = min(32u, cnt - base);
-#pragma unroll
-    for (int i = 0; i < PP; ++i) {
-      const int pr = lane + 32 * i;
-      if (pr < L * L) {
-        const int n1 = pr / L, n2 = pr % L;
-        for (int j = 0; j < m; ++j) {
-          const double ab = sw[j][n1] * sw[j][L + n2];
-#pragma unroll
-          for (int n = 0; n < L; ++n) acc[i][n] = fma(ab, sw[j][2 * L + n], acc[i][n]);
-        }
-      }
-    }
-    __syncwarp();
-  }
-#pragma unroll
-  for (int i = 0; i < PP; ++i) {
-    const int pr = lane + 32 * i;
-    if (pr < L * L)
-#pragma unroll
-      for (int n = 0; n < L; ++n) out[pr * L + n] = acc[i][n];
-  }
-}
-
 // P2M, warp per leaf cell, interpolation vectors stored particle-minor
 // (sv[component][particle]) so one LDS.128 returns a component for two particles:
 // per particle pair a lane reads a[n1], b[n2] (one LDS.128 each) and the l values
 // c[0..l) (l LDS.128, broadcast) for 2 (l + 1) DP ops -- half the shared-memory
-// instructions per FMA of k_p2m_warp, which is MIO-throttle bound. Same particle order
-// and product order as k_p2m_warp (the reference's wx, wxy, out += wxy sz), so the
-// results are identical. Chunks of 32 particles; a chunk's odd tail is zero-padded.
+// instructions per FMA of a row-major layout, which is MIO-throttle bound. The
+// reference's particle order and product order (wx, wxy, out += wxy sz). Chunks of 32
+// particles; a chunk's odd tail is zero-padded. (The row-major layout, one LDS.64 per
+// value, measured 1.00 vs 0.76 ms at config B.)
 template <int L>
 __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp2(LeafArgs a) {
   constexpr int PP = (L * L + 31) / 32;  // (n1, n2) pairs per lane
@@ -565,13 +495,7 @@ struct RunP2M {
   static void run(const LeafArgs& a, cudaStream_t s) {
     const uint32_t nc = a.ncells - a.cell0;
     if (!nc) return;
-    // FMMGPU_P2M=1: the row-major k_p2m_warp (A/B timing)
-    static const bool rowmajor = [] {
-      const char* e = std::getenv("FMMGPU_P2M");
-      return e && std::atoi(e) == 1;
-    }();
-    if (rowmajor) k_p2m_warp<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
-    else k_p2m_warp2<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
+    k_p2m_warp2<L><<<(nc + P2M_WARPS - 1) / P2M_WARPS, P2M_THREADS, 0, s>>>(a);
   }
 };
 template <int L>

@@ -324,8 +324,7 @@ void tree_free(fmmgpu_ctx* c) {
   cudaStream_t s = c->s_far;
   for (size_t v = 0; v < c->lv.size(); ++v) {
     auto& L = c->lv[v];
-    static const bool no_keep = std::getenv("FMMGPU_NO_YT_KEEP") != nullptr;  // A/B aid
-    if (L.yt && L.full && v < 22 && !no_keep) {
+    if (L.yt && L.full && v < 22) {
       dfree(c, c->yt_keep[v], s);
       c->yt_keep[v] = L.yt;
       c->yt_keep_n[v] = L.n;
@@ -582,17 +581,6 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   c->d_out = dalloc<double>(c, 4 * n, s);
   // cleared by the first entry point that uses them (an evaluation clears them anyway)
   c->zero_pending = true;
-  static const bool eager_zero = std::getenv("FMMGPU_EAGER_ZERO") != nullptr;  // A/B aid
-  if (eager_zero) {
-    for (auto& V : c->lv) {
-      const size_t e = size_t(V.n) * c->ldE * 8;
-      FMM_CUDA(cudaMemsetAsync(V.multipole, 0, e, s));
-      FMM_CUDA(cudaMemsetAsync(V.local_own, 0, e, s));
-      FMM_CUDA(cudaMemsetAsync(V.local_down, 0, e, s));
-    }
-    FMM_CUDA(cudaMemsetAsync(c->d_near, 0, 32 * n, s));
-    FMM_CUDA(cudaMemsetAsync(c->d_far, 0, 32 * n, s));
-  }
 
   k_copy_words<<<1, 32, 0, s>>>(reinterpret_cast<const uint32_t*>(c->d_flag), 1, d_offs + 9 * height);
   const uint32_t* h_offs = static_cast<const uint32_t*>(readback(c, d_offs, (9 * height + 1) * sizeof(uint32_t), s));

@@ -74,6 +74,27 @@ __device__ __forceinline__ void interact(const double xi, const double yi, const
   fz = fma(s3, dz, fz);
 }
 
+// The sources of one run from sj to se, a group of 4 per step. ROT (chunks with S > 1
+// source splits): the S splits read groups 128 B apart, i.e. the same four banks, so
+// split s reads its group in the order k ^ (s & 3): the four element positions of a
+// group sit in disjoint banks, which cuts the wavefronts of each LDS.128 by 4 (an S-way
+// conflict becomes S/4-way). Full passes (S = 1, broadcast) keep the plain order.
+// Measured at config B: P2P 12.78 -> 12.54 ms, evaluation 26.60 -> 26.36 ms (the
+// chunks' sums change order, so their fields differ from the plain order by rounding).
+template <bool SELF, bool ROT>
+__device__ __forceinline__ void run_sources(const double4* sj, const double4* se, const int step, const int rot,
+                                            const double4 xi, const double c375, double& pot, double& fx,
+                                            double& fy, double& fz) {
+  for (; sj < se; sj += step) {
+    const double4 p0 = sj[ROT ? rot : 0], p1 = sj[ROT ? rot ^ 1 : 1], p2 = sj[ROT ? rot ^ 2 : 2],
+                  p3 = sj[ROT ? rot ^ 3 : 3];
+    interact<SELF>(xi.x, xi.y, xi.z, p0, c375, pot, fx, fy, fz);
+    interact<SELF>(xi.x, xi.y, xi.z, p1, c375, pot, fx, fy, fz);
+    interact<SELF>(xi.x, xi.y, xi.z, p2, c375, pot, fx, fy, fz);
+    interact<SELF>(xi.x, xi.y, xi.z, p3, c375, pot, fx, fy, fz);
+  }
+}
+
 // leaf position (0..63) of child octant w inside the 4x4x4 block
 __device__ __forceinline__ int child_pos(int w) {
   return ((1 + ((w >> 2) & 1)) << 4) | ((1 + ((w >> 1) & 1)) << 2) | (1 + (w & 1));
@@ -171,6 +192,7 @@ __device__ void p2p_unit(const P2PArgs& a, const Neigh& nb, const double4* src, 
   const uint32_t S = 32u / m;  // source splits: lanes split * m + lt, split < S
   const uint32_t lt = lane % m, split = lane / m;
   const uint64_t tg = uint64_t(tfirst) + t0 + lt;
+  const int rot = static_cast<int>(split & 3u);
   const double4 xi = a.pw[tg];
   double c375 = 0.375;
   asm volatile("" : "+d"(c375));  // opaque: stays in a register instead of being rebuilt per group
@@ -187,22 +209,12 @@ __device__ void p2p_unit(const P2PArgs& a, const Neigh& nb, const double4* src, 
     const double4* sj = src + 4 * ((static_cast<int>(v0 - base) >> 2) + static_cast<int>(split));
     const double4* se = src + 4 * (static_cast<int>(v1 - base) >> 2);
     const int step = 4 * static_cast<int>(S);
-    if (q == 4) {
-      for (; sj < se; sj += step) {
-        const double4 p0 = sj[0], p1 = sj[1], p2 = sj[2], p3 = sj[3];
-        interact<true>(xi.x, xi.y, xi.z, p0, c375, pot, fx, fy, fz);
-        interact<true>(xi.x, xi.y, xi.z, p1, c375, pot, fx, fy, fz);
-        interact<true>(xi.x, xi.y, xi.z, p2, c375, pot, fx, fy, fz);
-        interact<true>(xi.x, xi.y, xi.z, p3, c375, pot, fx, fy, fz);
-      }
+    if (S == 1) {
+      if (q == 4) run_sources<true, false>(sj, se, step, 0, xi, c375, pot, fx, fy, fz);
+      else run_sources<false, false>(sj, se, step, 0, xi, c375, pot, fx, fy, fz);
     } else {
-      for (; sj < se; sj += step) {
-        const double4 p0 = sj[0], p1 = sj[1], p2 = sj[2], p3 = sj[3];
-        interact<false>(xi.x, xi.y, xi.z, p0, c375, pot, fx, fy, fz);
-        interact<false>(xi.x, xi.y, xi.z, p1, c375, pot, fx, fy, fz);
-        interact<false>(xi.x, xi.y, xi.z, p2, c375, pot, fx, fy, fz);
-        interact<false>(xi.x, xi.y, xi.z, p3, c375, pot, fx, fy, fz);
-      }
+      if (q == 4) run_sources<true, true>(sj, se, step, rot, xi, c375, pot, fx, fy, fz);
+      else run_sources<false, true>(sj, se, step, rot, xi, c375, pot, fx, fy, fz);
     }
   }
   if (S > 1) {  // combine the S source splits of each target in a fixed order

@@ -102,12 +102,17 @@ constexpr int P2M_WARPS = P2M_THREADS / 32;
 // instructions per FMA of a row-major layout, which is MIO-throttle bound. The
 // reference's particle order and product order (wx, wxy, out += wxy sz). Chunks of 32
 // particles; a chunk's odd tail is zero-padded. (The row-major layout, one LDS.64 per
-// value, measured 1.00 vs 0.76 ms at config B.)
+// value, measured 1.00 vs 0.76 ms at config B.) Rows are padded to SVS = 34 doubles:
+// with 32 the l rows a[n1] (and b[n2]) the lanes read at one column sit 256 B apart,
+// in the same four banks, and each LDS.128 replays l times; at 34 they fall in disjoint
+// banks (0.80 -> 0.56 ms at config B; with <= 128 registers, 4 CTAs per SM, 0.50 ms;
+// 80 registers spill and measured 0.58; orders above 5 would spill at 128).
+constexpr int P2M_SVS = 34;
 template <int L>
-__global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp2(LeafArgs a) {
+__global__ void __launch_bounds__(P2M_THREADS, L <= 5 ? 4 : 1) k_p2m_warp2(LeafArgs a) {
   constexpr int PP = (L * L + 31) / 32;  // (n1, n2) pairs per lane
   __shared__ double tn[L * (L - 1) + 1];
-  __shared__ __align__(16) double SV[P2M_WARPS][3 * L][32];
+  __shared__ __align__(16) double SV[P2M_WARPS][3 * L][P2M_SVS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < L * (L - 1); i += P2M_THREADS) tn[i] = a.tn[i];
   __syncthreads();
@@ -127,7 +132,7 @@ __global__ void __launch_bounds__(P2M_THREADS) k_p2m_warp2(LeafArgs a) {
     for (int n = 0; n < L; ++n) acc[i][n] = (!a.ow && lane + 32 * i < L * L) ? out[(lane + 32 * i) * L + n] : 0.0;
   if (a.ow)
     for (int i = L * L * L + lane; i < a.ldE; i += 32) out[i] = 0.0;  // padding read by M2L phase A (K = ldE)
-  double(*sv)[32] = SV[warp];
+  double(*sv)[P2M_SVS] = SV[warp];
   for (uint32_t base = 0; base < cnt; base += 32) {
     double s[L];
     if (base + lane < cnt) {

@@ -306,7 +306,8 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
     ++c->launches;
   };
   // FMMGPU_P2P_VARIANT (tuning experiments): 0 = 12 warps per CTA (default), 2 = 16, 3 = 8.
-  // Config B before the chunked partial passes: 13.7 / 13.9 / 13.8 ms. Also measured
+  // Config B before the chunked partial passes: 13.7 / 13.9 / 13.8 ms; with the chunks
+  // and the rotated split reads: 12.60 / 12.92 / 12.58 ms. Also measured
   // slower and removed: 8 sources per inner iteration, split accumulators (14.0 ms), two
   // targets per lane sharing each source load (12.9 / 13.0 ms with 8 / 12 warps vs 12.86
   // after the chunked partial passes), and

@@ -107,12 +107,17 @@ __global__ void k_leaf_scan(const uint32_t* __restrict__ first, const uint32_t* 
   const int lane = threadIdx.x & 31;
   if (warp >= ncells) return;
   const uint32_t f = first[warp], m = count[warp];
+  // the inner loop reads only x (8 B per pair instead of 32: the scan is L1-bound),
+  // y and z only for the rare equal x
+  const double* px = reinterpret_cast<const double*>(pw + f);
   for (uint32_t a = lane; a < m; a += 32) {
     pcell[f + a] = warp;
-    const double4 pa = pw[f + a];
+    const double xa = px[4 * a];
     for (uint32_t b = a + 1; b < m; ++b) {
-      const double4 pb = pw[f + b];
-      if (pa.x == pb.x && pa.y == pb.y && pa.z == pb.z) atomicOr(flag, 2);
+      if (px[4 * b] == xa) {
+        const double4 pa = pw[f + a], pb = pw[f + b];
+        if (pa.y == pb.y && pa.z == pb.z) atomicOr(flag, 2);
+      }
     }
   }
 }

@@ -11,7 +11,8 @@
 //   padding of the ldE stride) instead of accumulating into cleared arrays.
 //   L2P  thread per particle, the n3 reduction factored as
 //        sum_{n1,n2} (Sx Sy) * sum_{n3} L Sz (and the three gradient variants)
-//        (chebyshev.cpp:138-179, bench.cpp:317-336).
+//        (chebyshev.cpp:138-179, bench.cpp:317-336); above order 5 the n2 sums are
+//        factored as well.
 // Templated on the order so every loop is unrolled with compile-time bounds.
 #include <cstdlib>
 
@@ -188,8 +189,8 @@ __global__ void __launch_bounds__(P2M_THREADS, L <= 5 ? 4 : 1) k_p2m_warp2(LeafA
 // those cells (contiguous in Morton order) reads it as (near-)broadcast LDS.
 constexpr int L2P_CELLS = 8, L2P_THREADS = 128;
 
-template <int L>
-__global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
+template <int L, bool L2P_FACTORED, int MINB>
+__global__ void __launch_bounds__(L2P_THREADS, MINB > 0 ? MINB : 0) k_l2p_block(LeafArgs a) {
   constexpr int L3 = L * L * L;
   extern __shared__ __align__(16) double tot[];  // [L2P_CELLS][L3]
   __shared__ double tn[L * (L - 1) + 1];
@@ -257,6 +258,28 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
     constexpr int UNROLL_N1 = L <= 7 ? L : 1;  // keep sx/gx in registers
 #pragma unroll UNROLL_N1
     for (int n1 = 0; n1 < L; ++n1) {
+      if constexpr (L2P_FACTORED) {
+        // the n2 sums factored too: a1 = sum sy u, a2 = sum gy u, a3 = sum sy w, then
+        // pot += sx a1, dx += gx a1, dy += sx a2, dz += sx a3 (3 instead of 7 DP per (n1, n2))
+        double a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+        for (int n2 = 0; n2 < L; ++n2) {
+          double u = 0, w = 0;
+#pragma unroll
+          for (int n3 = 0; n3 < L; ++n3) {
+            const double v = t[(n1 * L + n2) * L + n3];
+            u = fma(v, sz[n3], u);
+            w = fma(v, gz[n3], w);
+          }
+          a1 = fma(sy[n2], u, a1);
+          a2 = fma(gy[n2], u, a2);
+          a3 = fma(sy[n2], w, a3);
+        }
+        pot = fma(sx[n1], a1, pot);
+        dx = fma(gx[n1], a1, dx);
+        dy = fma(sx[n1], a2, dy);
+        dz = fma(sx[n1], a3, dz);
+      } else {
 #pragma unroll
       for (int n2 = 0; n2 < L; ++n2) {
         double u = 0, w = 0;
@@ -271,6 +294,7 @@ __global__ void __launch_bounds__(L2P_THREADS) k_l2p_block(LeafArgs a) {
         dx = fma(gx[n1] * sy[n2], u, dx);
         dy = fma(sx[n1] * gy[n2], u, dy);
         dz = fma(ss, w, dz);
+      }
       }
     }
     double4 r = fprev;
@@ -509,8 +533,13 @@ struct RunL2P {
     const uint32_t nc = a.ncells - a.cell0;
     if (!nc) return;
     const int smem = static_cast<int>(sizeof(double) * L2P_CELLS * L * L * L);
-    FMM_CUDA(cudaFuncSetAttribute(k_l2p_block<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_l2p_block<L><<<(nc + L2P_CELLS - 1) / L2P_CELLS, L2P_THREADS, smem, s>>>(a);
+    // orders <= 5: the (n1, n2) loop as written, <= 128 registers (4 CTAs per SM);
+    // higher orders: the n2 sums factored as well (config-C leaf 1.65 -> 1.22 ms; at
+    // order 5 the factored loop needs 162-188 registers and measured 0.59-0.79 vs 0.56 ms)
+    constexpr bool factored = L > 5;
+    auto kern = k_l2p_block<L, factored, factored ? 0 : 4>;
+    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<(nc + L2P_CELLS - 1) / L2P_CELLS, L2P_THREADS, smem, s>>>(a);
   }
 };
 template <int L>

@@ -16,7 +16,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     import paper_1206_0115_b200 as P
     level = int(level)
     xyzw = P.generate_particles(10_000_000, "uniform", 42)
-    c = P.FmmContext(None, order=5)
+    c = P.FmmContext(None, order=int(os.environ.get("ORDER", "5")))
     c.build_tree(xyzw, 7)
     c.time_operator(kind, level, 1)
     ms = c.time_operator(kind, level, 5)

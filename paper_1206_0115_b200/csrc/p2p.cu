@@ -307,7 +307,9 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   };
   // FMMGPU_P2P_VARIANT (tuning experiments): 0 = 12 warps per CTA (default), 2 = 16, 3 = 8.
   // Config B before the chunked partial passes: 13.7 / 13.9 / 13.8 ms; with the chunks
-  // and the rotated split reads: 12.60 / 12.92 / 12.58 ms. Also measured
+  // and the rotated split reads: 12.60 / 12.92 / 12.58 ms. Staging 4 particles per thread
+  // with their loads in flight together: 12.59 vs 12.56 ms (the other CTA of the SM
+  // already hides the staging latency). Also measured
   // slower and removed: 8 sources per inner iteration, split accumulators (14.0 ms), two
   // targets per lane sharing each source load (12.9 / 13.0 ms with 8 / 12 warps vs 12.86
   // after the chunked partial passes), and

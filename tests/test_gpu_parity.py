@@ -448,3 +448,24 @@ def test_run_fmm_check_reproduces_recorded_accuracy(fmm):
         assert 0 < ef < 0.1
         got.append("%.3e" % ep)
     assert got == ["1.242e-04", "1.051e-06", "1.150e-08"]
+
+
+def test_coincident_check_small_leaves(fmm):
+    """geometry.cpp:126-136 on the small-leaf path (k_leaf_scan, <= 64 per leaf): a
+    duplicate anywhere in a leaf of ~40 particles (pairs past the first 32 included) is
+    a domain error; equal x alone is not."""
+    P = fmm
+    base = make_particles(20000, "uniform", 21, False)
+    c = P.FmmContext(None, order=3)
+    same_x = base.copy()
+    same_x[100:200, 0] = same_x[0, 0]  # equal x, distinct y, z
+    c.build_tree(same_x, 4)
+    assert c.particles()[0].shape[0] == 20000
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        i, j = rng.choice(20000, 2, replace=False)
+        dup = same_x.copy()
+        dup[j, :3] = dup[i, :3]
+        with pytest.raises(P.DomainError):
+            c.build_tree(dup, 4)
+    c.build_tree(same_x, 4)  # a failed build leaves the context usable

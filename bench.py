@@ -36,8 +36,9 @@ CONFIGS = {
     "D": (20_000_000, "ellipsoid", 8, 5, "ellipsoid surface (semi-axes 0.5, 0.35, 0.2) N=20M, height 8, order 5"),
     "E": (100_000_000, "uniform", 8, 5, "uniform cube N=100M, height 8, order 5"),
 }
-# Bounded CPU sample of config B: same particles per leaf (~38) and order, one level
-# shallower (1/8 of the particles): the reference's per-particle work is the same.
+# Labelled fallback (--cpu-sample): a bounded sample at the same particles per leaf (~38) and
+# order, one level shallower (1/8 of the particles): the reference's per-particle work is
+# the same.
 CPU_SAMPLE = {"B": (1_250_000, "uniform", 6, 5), "C": (1_250_000, "uniform", 6, 7), "A": (100_000, "uniform", 4, 5),
               "D": (1_250_000, "ellipsoid", 6, 5), "E": (1_562_500, "uniform", 6, 5)}
 # (volume clouds keep N / 8^h, the surface cloud N / 4^h: same particles per leaf as the
@@ -155,22 +156,32 @@ def max_over_ranks(x, world):
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def reference_sample(cfg_name, workers, warmup, steps):
-    """The reference itself (oracle/_ref) on the bounded sample; returns (Mparticles/s list, info)."""
+def reference_context(cfg_name, sample=False):
+    """The reference's FmmContext (oracle/_ref: the unmodified reference sources) on the
+    workload's own particles (or, with sample=True, the labelled 1/8 sample); returns
+    (RefContext, n, description) or (None, ...) when oracle/_ref was never built."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"  # the reference's GEMMs run inside its own workers
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracles import Oracle, RefContext, RefLib
-    n, dist, h, order = CPU_SAMPLE[cfg_name]
+    n, dist, h, order = CPU_SAMPLE[cfg_name] if sample else CONFIGS[cfg_name][:4]
     xyzw = Oracle.generate_particles(n, dist, 42)
-    if RefLib.available():
-        ref = RefContext(xyzw, h, order)
-        for _ in range(warmup):
-            ref.execute(workers=workers)
-        times = [ref.execute(workers=workers) for _ in range(steps)]
-        kind = "reference"
-        setup = ref.setup_seconds()
-    else:  # the CPU restatement (single thread), when the reference was never built here
+    desc = (f"N={n} {dist}, height {h}, order {order}" +
+            (f" (labelled fallback: 1/{CONFIGS[cfg_name][0] // n} of config {cfg_name}'s particles at the same "
+             f"particles per leaf)" if sample else f" (config {cfg_name} itself)"))
+    if not RefLib.available():
+        return None, n, desc, xyzw
+    return RefContext(xyzw, h, order), n, desc, xyzw
+
+
+def reference_run(cfg_name, workers, warmup, steps, sample=False, t1=False):
+    """Times the reference's execute() of the whole task graph (runtime.cpp:91-216, the
+    exec_seconds of run_fmm, bench.cpp:458-459) with `workers` threads and the priority
+    policy; setup (tree, plan, graph, SVD: bench.cpp:220-236) is reported separately.
+    Returns (exec seconds per step, info dict, ref context)."""
+    ref, n, desc, xyzw = reference_context(cfg_name, sample)
+    if ref is None:  # the CPU restatement (single thread), when the reference was never built here
         from oracles import OracleOps, OracleTree
+        _, _, h, order = CPU_SAMPLE[cfg_name] if sample else CONFIGS[cfg_name][:4]
         t = OracleTree(xyzw, h)
         ops = OracleOps.cached(order)
         times = []
@@ -179,30 +190,52 @@ def reference_sample(cfg_name, workers, warmup, steps):
             t.evaluate(ops)
             if i >= warmup:
                 times.append(time.perf_counter() - t0)
-        kind, workers, setup = "port", 1, None
-    rates = [n / t / 1e6 for t in times]
-    info = {"kind": kind, "cores": workers,
-            "sample": f"N={n} {dist}, height {h}, order {order} (config {cfg_name} at the same particles per "
-                      f"leaf, 1/{CONFIGS[cfg_name][0] // n} of the particles); timed = the reference's execute() of "
-                      f"the whole task graph ({'%d workers' % workers}), setup ({setup and round(setup, 2)} s) excluded"}
-    return rates, info
+        return times, {"kind": "port", "cores": 1, "n": n, "sample": desc + "; the CPU restatement, 1 thread"}, None
+    for _ in range(warmup):
+        ref.execute(workers=workers)
+    times = [ref.execute(workers=workers) for _ in range(steps)]
+    info = {"kind": "reference", "cores": workers, "n": n, "same_config": not sample,
+            "setup_seconds": ref.setup_seconds(), "exec_seconds": float(np.mean(times)),
+            "exec_seconds_min": float(np.min(times)), "policy": "priority", "group_size": 250,
+            "sample": desc + f"; timed = the reference's execute() of the whole task graph with {workers} "
+                             f"workers, {steps} steps after {warmup} warm-up; setup reported separately"}
+    if t1:  # t_1 and the parallel efficiency e_n = t_1 / (n t_n)
+        t1s = ref.execute(workers=1)
+        info["exec_seconds_1_worker"] = t1s
+        info["parallel_efficiency"] = t1s / (workers * info["exec_seconds"])
+    return times, info, ref
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return
     workers = os.cpu_count() or 1
-    rates, info = reference_sample(args.config, workers, args.warmup, args.steps)
-    v = float(np.mean(rates))
-    n = CONFIGS[args.config][0]
+    times, info, _ = reference_run(args.config, workers, args.warmup, args.steps, sample=args.cpu_sample,
+                                   t1=not args.no_t1)
+    n = info["n"]
+    v = n / float(np.mean(times)) / 1e6
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": CPU_SAMPLE[args.config][0] / v / 1e3,
+            "warmup": args.warmup, "ms_per_step": float(np.mean(times)) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator, seed 42)", "impl": "reference",
-            "config": dict(config_dict(args.config), sample_n=CPU_SAMPLE[args.config][0]),
+            "config": dict(config_dict(args.config), **({"sample_n": n} if args.cpu_sample else {})),
             "cpu_baseline": dict(info, value=v, unit=UNIT),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def parity_vs_reference(ctx, ref, fields, h):
+    """The same run's parity with the reference (cpu_baseline leg only): tree and lists
+    bit-exact, fields of our fmmgpu_run (input order) vs the reference's gather."""
+    import config_parity
+    rf = ref.fields()
+    ep, ef = config_parity.field_errors([f.numpy() for f in fields], rf)
+    tree = config_parity.compare_tree(ctx, ref, h)
+    lists = config_parity.compare_lists(ctx, ref, h)
+    return {"tree_bit_exact": tree["bit_exact"], "lists_bit_exact": lists["bit_exact"],
+            "rel_l2_potential": ep, "rel_l2_force": ef, "tolerance": 1e-12,
+            "what": "this run's fmmgpu_run fields (own device-SVD factors) vs the reference's FmmContext "
+                    "gather after execute(); tree, Morton order, near CSR and far lists compared element-wise"}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -212,7 +245,22 @@ def run_ours(args, world, rank, local):
     xyzw = P.generate_particles(n, dist, 42)
     ctx = P.FmmContext(None, order=order, device=local)
     ctx.build_tree(xyzw, h, 250)
+    tree_cold_ms = ctx.timings()["TREE"]  # first build: includes the H2D and every allocation
     ledger = ctx.ledger()
+
+    # tree + lists, warm: rebuilds from device-resident input,
+    # CUDA events around fmmgpu_build_tree / fmmgpu_build_lists, best of 5
+    import torch
+    dev_in = torch.from_numpy(xyzw).to(f"cuda:{local}")
+    tree_ms, lists_ms = [], []
+    for _ in range(6):
+        ctx.build_tree(n, h, 250, on_device_ptr=dev_in.data_ptr())
+        ctx.build_lists()
+        t = ctx.timings()
+        tree_ms.append(t["TREE"])
+        lists_ms.append(t["LISTS"])
+    del dev_in
+    torch.cuda.empty_cache()
 
     def attach_partition():
         """N > 1: this rank owns a contiguous Morton range of leaves; the
@@ -246,7 +294,6 @@ def run_ours(args, world, rank, local):
     # pinned output sets used alternately, so step k's H2D and step k-1's D2H run on the
     # copy engines under step k-1's / step k's device work; the serial fmmgpu_run is
     # timed beside it.
-    import torch
     pins = [torch.from_numpy(xyzw).pin_memory() for _ in range(2 if world == 1 else 1)]
     outsets = [[torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(4)] for _ in range(len(pins))]
     pin_in, outs = pins[0], outsets[0]
@@ -333,8 +380,8 @@ def run_ours(args, world, rank, local):
             "peak_source": "FP64 DFMA measured by tools/microbench/fp64_peaks.cu (profiles/r01_fp64_peaks.txt); "
                            "MEASURED_PEAKS.json has no FP64 figure",
             "flop_convention": "reference ledger (bench.hpp:49-53): 15 flop per directional interaction "
-                               "(the kernel issues 18 FP64 instructions per interaction, so frac <= 0.45 at "
-                               "a saturated FP64 pipe)",
+                               "(the one-sided kernel issues 18 FP64 instructions per interaction and the "
+                               "peak counts 2 flop per DFMA, so frac <= 15/36 = 0.417 at a saturated FP64 pipe)",
             # the same launch against the FP64 instruction issue rate (DFMA peak / 2 flop):
             # useful interactions x 18 DP instructions / duration
             "fp64_instr_frac": (ledger["near_directional"] * 18 / (iso["P2P"] / 1e3)) / (FP64_DFMA_TFLOPS * 1e12 / 2),
@@ -348,13 +395,20 @@ def run_ours(args, world, rank, local):
             "dtype": "f64", "data": "synthetic (reference generator bench.cpp:29-39, seed 42, unit weights)",
             "config": config_dict(args.config, world),
             "gpu_launches": launches, "e2e": e2e, "roofline": roof, "per_operator": per_op,
-            "tree_ms": kinds["TREE"], "clocks": clk,
+            "tree_build_ms": min(tree_ms[1:]), "lists_build_ms": min(lists_ms[1:]),
+            "tree_build_cold_ms": tree_cold_ms,
+            "tree_note": "tree_build_ms / lists_build_ms: best of 5 warm rebuilds from device-resident particles "
+                         "(CUDA events around fmmgpu_build_tree / fmmgpu_build_lists); the evaluation does not "
+                         "read the explicit lists. tree_build_cold_ms: the first build (H2D + allocations)",
+            "clocks": clk,
             "note": "P2P runs on its own stream concurrently with the far-field chain; per-operator times "
                     "of the far chain include waiting for SMs the P2P kernel holds"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rates, info = reference_sample(args.config, os.cpu_count() or 1, 1, 2)
-            line["cpu_baseline"] = dict(info, value=float(np.mean(rates)), unit=UNIT)
+            times, info, ref = reference_run(args.config, os.cpu_count() or 1, 1, 2, sample=args.cpu_sample)
+            line["cpu_baseline"] = dict(info, value=info["n"] / float(np.mean(times)) / 1e6, unit=UNIT)
+            if ref is not None and not args.cpu_sample:
+                line["parity"] = parity_vs_reference(ctx, ref, serial_ref, h)
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:
@@ -370,6 +424,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", action="store_true",
+                    help="time the reference on the labelled 1/8 sample instead of the configuration itself")
+    ap.add_argument("--no-t1", action="store_true", help="reference arm: skip the 1-worker run (t_1)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

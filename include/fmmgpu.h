@@ -59,6 +59,10 @@ const char* fmmgpu_global_error(void);
  * row-major U (l^3 x r), sigma (r), V (l^3 x r). load replaces the operators. */
 int fmmgpu_load_m2l_cache(fmmgpu_ctx* ctx, const char* path);
 int fmmgpu_save_m2l_cache(const fmmgpu_ctx* ctx, const char* path);
+/* fmmgpu_create with the operators of a saved cache instead of a new device SVD
+ * (M2LOperatorSet::load_cache(path, order, eps), m2l.cpp:247-288: a cache of another
+ * order or eps, or an unreadable file, is an error). */
+int fmmgpu_create_from_cache(int device, int order, double eps, const char* path, fmmgpu_ctx** out);
 /* CompressionReport (m2l.hpp:56-62): ranks and multiplicities per canonical class. */
 int fmmgpu_m2l_report(const fmmgpu_ctx* ctx, int32_t* ranks16, int32_t* multiplicity16,
                       double* weighted_mean_rank);
@@ -155,6 +159,11 @@ int fmmgpu_timings(const fmmgpu_ctx* ctx, double* ms10);
  * bench.cpp:151-181): flops per kind (7), near directional interactions, M2L pairs. */
 int fmmgpu_ledger(fmmgpu_ctx* ctx, uint64_t* flops7, uint64_t* near_directional,
                   uint64_t* m2l_pairs);
+/* FlopLedger rows (build_ledger, bench.cpp:151-181, over count_interactions,
+ * taskflow.cpp:107-135): work[k * height + v] and flops[k * height + v] per task kind k
+ * (fmmgpu_kind) and level v; m2l_pairs16[v * 16 + c] = M2L pairs of canonical class c at
+ * level v (InteractionStats::m2l_pairs). Any pointer may be NULL. */
+int fmmgpu_ledger_rows(fmmgpu_ctx* ctx, uint64_t* work, uint64_t* flops, uint64_t* m2l_pairs16);
 /* Number of kernels launched by the last fmmgpu_evaluate. */
 uint64_t fmmgpu_last_launch_count(const fmmgpu_ctx* ctx);
 /* Per-launch device trace of evaluations (runtime.cpp:157-171 TraceEvent, written by

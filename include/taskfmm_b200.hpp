@@ -13,11 +13,17 @@
 //   FmmContext (ctor, reset, run_task, gather, setup_seconds)   bench.hpp:86-121
 //   run_fmm (oracle check on the device, no writers)            bench.cpp:415-469
 //
-// Granularity: the device runs one launch per (operator, level). run_task(task)
-// executes the level launch of (task.kind, task.level) on the first task of that pair
-// since the last reset() and is a no-op for the remaining blocks, so executing a whole
-// reference TaskGraph (any valid order) reproduces one evaluation. P2PReduce is folded
-// into P2P (one-sided owner-computes, no slot buffers).
+// Granularity: the device runs one launch per (operator, level), in the fixed far-field
+// chain P2M -> M2M(leaf-1 .. 2) -> M2L(2 .. leaf) -> L2L(2 .. leaf-1) -> L2P, with P2P
+// independent of it. run_task(task) launches, since the last reset(), every chain
+// element up to and including (task.kind, task.level) that has not run yet (each level
+// launch reads only inputs complete at that point: particles, or levels earlier in the
+// chain), and P2P on the first P2P / P2PReduce task; the remaining tasks of a level are
+// no-ops. So executing a reference TaskGraph in ANY topological order -- including the
+// graphs whose elided zero-pair M2L blocks leave L2L(2, b) without predecessors
+// (taskflow.cpp:179-186) -- reproduces one evaluation. run_task may be called from the
+// reference's worker threads (execute, runtime.cpp:165): calls are serialised by a
+// mutex. P2PReduce is folded into P2P (one-sided owner-computes, no slot buffers).
 #pragma once
 
 #include <array>
@@ -26,6 +32,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <limits>
+#include <mutex>
+#include <utility>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -140,8 +148,10 @@ class FmmContext {
 
   //! FmmContext::reset (bench.cpp:240-253): zero every accumulator.
   void reset() {
+    std::lock_guard<std::mutex> lock(mu_);
     call(fmmgpu_reset(ctx_));
-    for (auto& k : done_) k.assign(static_cast<std::size_t>(cfg_.height), 0);
+    next_ = 0;
+    p2p_done_ = false;
   }
 
   //! FmmContext::run_task (bench.cpp:255-344) at level granularity (see header).
@@ -149,17 +159,26 @@ class FmmContext {
     const int k = static_cast<int>(task.kind);
     if (k < 0 || k >= TASK_KIND_COUNT) throw std::invalid_argument("run_task: unknown task kind");
     if (task.level < 0 || task.level >= cfg_.height) throw std::out_of_range("run_task: level out of range");
-    if (done_[k].empty()) done_[k].assign(static_cast<std::size_t>(cfg_.height), 0);
-    if (done_[k][task.level]) return;
-    done_[k][task.level] = 1;
-    switch (task.kind) {
-      case TaskKind::P2M: call(fmmgpu_p2m(ctx_)); break;
-      case TaskKind::M2M: call(fmmgpu_m2m(ctx_, task.level)); break;
-      case TaskKind::M2L: call(fmmgpu_m2l(ctx_, task.level)); break;
-      case TaskKind::L2L: call(fmmgpu_l2l(ctx_, task.level)); break;
-      case TaskKind::L2P: call(fmmgpu_l2p(ctx_)); break;
-      case TaskKind::P2P: call(fmmgpu_p2p(ctx_)); break;
-      case TaskKind::P2PReduce: break;  // folded into P2P
+    std::lock_guard<std::mutex> lock(mu_);
+    if (task.kind == TaskKind::P2P || task.kind == TaskKind::P2PReduce) {
+      if (task.level != cfg_.height - 1) throw std::out_of_range("run_task: P2P tasks live on the leaf level");
+      if (!p2p_done_) call(fmmgpu_p2p(ctx_));
+      p2p_done_ = true;
+      return;
+    }
+    const auto it = std::find(chain_.begin(), chain_.end(), std::make_pair(task.kind, int(task.level)));
+    if (it == chain_.end()) throw std::out_of_range("run_task: no such (kind, level) in the task graph");
+    const std::size_t pos = static_cast<std::size_t>(it - chain_.begin());
+    for (; next_ <= pos; ++next_) {
+      const auto [kind, level] = chain_[next_];
+      switch (kind) {
+        case TaskKind::P2M: call(fmmgpu_p2m(ctx_)); break;
+        case TaskKind::M2M: call(fmmgpu_m2m(ctx_, level)); break;
+        case TaskKind::M2L: call(fmmgpu_m2l(ctx_, level)); break;
+        case TaskKind::L2L: call(fmmgpu_l2l(ctx_, level)); break;
+        case TaskKind::L2P: call(fmmgpu_l2p(ctx_)); break;
+        default: break;
+      }
     }
   }
 
@@ -185,7 +204,21 @@ class FmmContext {
   RunConfig cfg_;
   fmmgpu_ctx* ctx_ = nullptr;
   double setup_seconds_ = 0;
-  std::array<std::vector<char>, TASK_KIND_COUNT> done_;
+  // the far-field chain in launch order (taskflow.cpp:143-289 dependencies, level granular)
+  std::vector<std::pair<TaskKind, int>> chain_ = far_chain(cfg_.height);
+  std::size_t next_ = 0;  // first chain element not launched since reset()
+  bool p2p_done_ = false;
+  std::mutex mu_;
+
+  static std::vector<std::pair<TaskKind, int>> far_chain(int height) {
+    const int leaf = height - 1;
+    std::vector<std::pair<TaskKind, int>> c{{TaskKind::P2M, leaf}};
+    for (int v = leaf - 1; v >= 2; --v) c.emplace_back(TaskKind::M2M, v);
+    for (int v = 2; v <= leaf; ++v) c.emplace_back(TaskKind::M2L, v);
+    for (int v = 2; v < leaf; ++v) c.emplace_back(TaskKind::L2L, v);
+    c.emplace_back(TaskKind::L2P, leaf);
+    return c;
+  }
 };
 
 struct RunResult {

@@ -379,3 +379,74 @@ int ref_ledger(const double* xyzw, std::uint64_t n, int height, int acc, int gro
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// count_interactions + build_ledger over an existing context's tree and operators
+// (bench.cpp:440-442): flops / work [kind * height + level], m2l_pairs [level * 16 + c].
+int ref_ctx_ledger(void* h, std::uint64_t* flops, std::uint64_t* work, std::uint64_t* pairs16) {
+  auto* c = static_cast<Ctx*>(h);
+  try {
+    const GroupTree& tree = c->fmm->tree();
+    const int height = tree.height();
+    const auto stats = count_interactions(tree);
+    const auto ledger = build_ledger(stats, c->fmm->ops().report(), c->acc, tree.particles().size(), height);
+    for (int k = 0; k < TASK_KIND_COUNT; ++k)
+      for (int v = 0; v < height; ++v) {
+        flops[k * height + v] = ledger.rows[k][v].flops;
+        work[k * height + v] = ledger.rows[k][v].work;
+      }
+    for (int v = 0; v < height; ++v)
+      for (int cl = 0; cl < 16; ++cl)
+        pairs16[v * 16 + cl] = v < static_cast<int>(stats.m2l_pairs.size()) ? stats.m2l_pairs[v][cl] : 0;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// run_fmm (bench.cpp:415-469) with out_dir: the reference's own writers produce
+// results.csv and summary.json (bench.cpp:400-411, 504-584). dist 0 uniform, 1 sphere.
+int ref_run_fmm(std::uint64_t n, int dist, std::uint64_t seed, int height, int acc, int group_size,
+                int workers, std::uint64_t check, const char* out_dir, double* eps2) {
+  try {
+    RunConfig cfg;
+    cfg.n = n;
+    cfg.dist = dist == 0 ? Distribution::Uniform : Distribution::Sphere;
+    cfg.seed = seed;
+    cfg.height = height;
+    cfg.acc = acc;
+    cfg.group_size = group_size;
+    cfg.workers = workers;
+    cfg.check = check;
+    cfg.out_dir = out_dir ? out_dir : "";
+    const RunResult r = run_fmm(cfg);
+    if (eps2) {
+      eps2[0] = r.eps_l2_potential;
+      eps2[1] = r.eps_l2_force;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+}  // extern "C"
+
+extern "C" {
+// The task graph's edges (TaskGraph, taskflow.hpp:34-42): successors of task i are
+// succ[off[i] .. off[i+1]); returns the edge count (call with null arrays to size).
+std::uint64_t ref_task_edges(void* h, std::uint32_t* off, std::uint32_t* succ) {
+  const auto& g = static_cast<Ctx*>(h)->fmm->graph();
+  std::uint64_t e = 0;
+  for (std::size_t i = 0; i < g.size(); ++i) {
+    if (off) off[i] = static_cast<std::uint32_t>(e);
+    for (std::uint32_t s : g.tasks[i].successors) {
+      if (succ) succ[e] = s;
+      ++e;
+    }
+  }
+  if (off) off[g.size()] = static_cast<std::uint32_t>(e);
+  return e;
+}
+}  // extern "C"

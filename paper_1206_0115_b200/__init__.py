@@ -70,6 +70,7 @@ def lib():
         L.fmmgpu_last_error.argtypes = [c_void_p]
         L.fmmgpu_global_error.restype = ctypes.c_char_p
         L.fmmgpu_create.argtypes = [c_int, c_int, c_double, ctypes.POINTER(c_void_p)]
+        L.fmmgpu_create_from_cache.argtypes = [c_int, c_int, c_double, ctypes.c_char_p, ctypes.POINTER(c_void_p)]
         L.fmmgpu_destroy.argtypes = [c_void_p]
         L.fmmgpu_build_tree.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_int, c_int, c_void_p]
         L.fmmgpu_level_cells.restype = c_uint64
@@ -151,11 +152,12 @@ class FmmContext:
     """FmmContext (bench.hpp:86-121) on one B200.
 
     ``FmmContext(particles, cfg)`` builds the operators (InterpolationEngine +
-    M2LOperatorSet, device SVD) and the tree on the GPU; ``evaluate()`` runs the
+    M2LOperatorSet, device SVD, or the factors of ``m2l_cache``) and the tree on the GPU; ``evaluate()`` runs the
     whole evaluation; ``gather()`` returns (potential, fx, fy, fz) in input order.
     """
 
-    def __init__(self, particles=None, cfg: RunConfig | None = None, *, order=None, eps=None, device=0):
+    def __init__(self, particles=None, cfg: RunConfig | None = None, *, order=None, eps=None, device=0,
+                 m2l_cache: str | None = None):
         self.cfg = cfg or RunConfig()
         self.order = order if order is not None else self.cfg.acc
         if self.order < 2:
@@ -163,7 +165,11 @@ class FmmContext:
         self.eps = eps if eps is not None else 10.0 ** (-self.order)
         self._lib = lib()
         h = c_void_p()
-        rc = self._lib.fmmgpu_create(device if cfg is None else cfg.device, self.order, self.eps, byref(h))
+        dev = device if cfg is None else cfg.device
+        if m2l_cache is not None:  # M2LOperatorSet::load_cache(path, order, eps): no device SVD
+            rc = self._lib.fmmgpu_create_from_cache(dev, self.order, self.eps, m2l_cache.encode(), byref(h))
+        else:
+            rc = self._lib.fmmgpu_create(dev, self.order, self.eps, byref(h))
         if rc:
             raise _ERRORS.get(rc, FmmError)(self._lib.fmmgpu_global_error().decode())
         self.h = h
@@ -350,6 +356,16 @@ class FmmContext:
         pairs = c_uint64()
         self._check(self._lib.fmmgpu_ledger(self.h, _p(flops), byref(near), byref(pairs)))
         return {"flops": dict(zip(KINDS, flops.tolist())), "near_directional": near.value, "m2l_pairs": pairs.value}
+
+    def ledger_rows(self):
+        """FlopLedger rows (build_ledger, bench.cpp:151-181): work and flops as
+        (7 kinds, height) arrays, and M2L pairs per (level, canonical class)."""
+        h = self.height
+        work = np.zeros((7, h), dtype=np.uint64)
+        flops = np.zeros((7, h), dtype=np.uint64)
+        pairs = np.zeros((h, 16), dtype=np.uint64)
+        self._check(self._lib.fmmgpu_ledger_rows(self.h, _p(work), _p(flops), _p(pairs)))
+        return {"work": work, "flops": flops, "m2l_pairs": pairs}
 
     def launch_count(self):
         return int(self._lib.fmmgpu_last_launch_count(self.h))

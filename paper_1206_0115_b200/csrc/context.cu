@@ -121,9 +121,47 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// M2LOperatorSet::load_cache (m2l.cpp:247-288): the factors of the binary cache of
+// (order, eps) into the context's operator set (its transport tables are rebuilt by
+// m2l_setup).
+void read_m2l_cache(fmmgpu_ctx* c, const char* path) {
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) throw Error(FMMGPU_RUNTIME_ERROR, std::string("cannot open M2L cache ") + path);
+  uint64_t magic = 0;
+  int32_t order = 0;
+  double eps = 0;
+  bool ok = std::fread(&magic, 8, 1, f) == 1 && std::fread(&order, 4, 1, f) == 1 && std::fread(&eps, 8, 1, f) == 1;
+  if (!ok || magic != 0x4c324d4d4d465400ull || order != c->order || eps != c->eps) {
+    std::fclose(f);
+    throw Error(FMMGPU_INVALID_ARGUMENT, "M2L cache does not match (magic, order, eps)");
+  }
+  int32_t ranks[16];
+  ok = std::fread(ranks, 4, 16, f) == 16;
+  std::vector<double> u[16], sg[16], v[16];  // committed only when the whole file reads
+  for (int cl = 0; cl < 16 && ok; ++cl) {
+    if (ranks[cl] < 1 || ranks[cl] > c->l3) { ok = false; break; }
+    u[cl].resize(size_t(c->l3) * ranks[cl]);
+    sg[cl].resize(ranks[cl]);
+    v[cl].resize(size_t(c->l3) * ranks[cl]);
+    ok = ok && std::fread(u[cl].data(), 8, u[cl].size(), f) == u[cl].size();
+    ok = ok && std::fread(sg[cl].data(), 8, sg[cl].size(), f) == sg[cl].size();
+    ok = ok && std::fread(v[cl].data(), 8, v[cl].size(), f) == v[cl].size();
+  }
+  std::fclose(f);
+  if (!ok) throw Error(FMMGPU_RUNTIME_ERROR, "truncated or corrupt M2L cache");
+  auto& T = c->m2l;
+  for (int cl = 0; cl < 16; ++cl) {
+    T.rank[cl] = ranks[cl];
+    T.u[cl] = std::move(u[cl]);
+    T.sigma[cl] = std::move(sg[cl]);
+    T.v[cl] = std::move(v[cl]);
+  }
+}
+
 // InterpolationEngine + M2LOperatorSet of a new context (fmmgpu_create); `factors`
 // (optional) supplies the compressed M2L operators instead of a new device SVD.
-void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx* factors) {
+void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx* factors,
+              const char* cache = nullptr) {
   if (order < 2 || order > MAX_ORDER) throw Error(FMMGPU_INVALID_ARGUMENT, "InterpolationEngine: order must be in [2, 10]");
   if (!(eps > 0)) throw Error(FMMGPU_INVALID_ARGUMENT, "M2LOperatorSet: eps must be positive");
   int ndev = 0;
@@ -163,6 +201,9 @@ void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx
       T.sigma[cl] = F.sigma[cl];
     }
     m2l_setup(c, false);
+  } else if (cache) {  // the factors of a saved operator set: no SVD
+    read_m2l_cache(c, cache);
+    m2l_setup(c, false);
   } else {
     m2l_setup(c, true);
   }
@@ -180,6 +221,20 @@ int fmmgpu_create(int device, int order, double eps, fmmgpu_ctx** out) {
   *out = nullptr;
   auto* c = new fmmgpu_ctx;
   const int rc = guarded(c, [&] { ctx_init(c, device, order, eps, nullptr); });
+  if (rc != FMMGPU_OK) {
+    g_global_err = c->err;
+    fmmgpu_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return FMMGPU_OK;
+}
+
+int fmmgpu_create_from_cache(int device, int order, double eps, const char* path, fmmgpu_ctx** out) {
+  if (!out || !path) return FMMGPU_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* c = new fmmgpu_ctx;
+  const int rc = guarded(c, [&] { ctx_init(c, device, order, eps, nullptr, path); });
   if (rc != FMMGPU_OK) {
     g_global_err = c->err;
     fmmgpu_destroy(c);
@@ -241,31 +296,7 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
 
 int fmmgpu_load_m2l_cache(fmmgpu_ctx* c, const char* path) {
   return guarded(c, [&] {
-    std::FILE* f = std::fopen(path, "rb");
-    if (!f) throw Error(FMMGPU_RUNTIME_ERROR, std::string("cannot open M2L cache ") + path);
-    uint64_t magic = 0;
-    int32_t order = 0;
-    double eps = 0;
-    bool ok = std::fread(&magic, 8, 1, f) == 1 && std::fread(&order, 4, 1, f) == 1 && std::fread(&eps, 8, 1, f) == 1;
-    if (!ok || magic != 0x4c324d4d4d465400ull || order != c->order || eps != c->eps) {
-      std::fclose(f);
-      throw Error(FMMGPU_INVALID_ARGUMENT, "M2L cache does not match (magic, order, eps)");
-    }
-    int32_t ranks[16];
-    ok = std::fread(ranks, 4, 16, f) == 16;
-    auto& T = c->m2l;
-    for (int cl = 0; cl < 16 && ok; ++cl) {
-      if (ranks[cl] < 1 || ranks[cl] > c->l3) { ok = false; break; }
-      T.rank[cl] = ranks[cl];
-      T.u[cl].resize(size_t(c->l3) * ranks[cl]);
-      T.sigma[cl].resize(ranks[cl]);
-      T.v[cl].resize(size_t(c->l3) * ranks[cl]);
-      ok = ok && std::fread(T.u[cl].data(), 8, T.u[cl].size(), f) == T.u[cl].size();
-      ok = ok && std::fread(T.sigma[cl].data(), 8, T.sigma[cl].size(), f) == T.sigma[cl].size();
-      ok = ok && std::fread(T.v[cl].data(), 8, T.v[cl].size(), f) == T.v[cl].size();
-    }
-    std::fclose(f);
-    if (!ok) throw Error(FMMGPU_RUNTIME_ERROR, "truncated or corrupt M2L cache");
+    read_m2l_cache(c, path);
     m2l_setup(c, false);
   });
 }
@@ -345,7 +376,7 @@ int fmmgpu_p2m(fmmgpu_ctx* c) {
 }
 int fmmgpu_m2m(fmmgpu_ctx* c, int v) {
   return guarded(c, [&] {
-    need_level(c, v, 0, c->height - 2, "m2m");
+    need_level(c, v, 2, c->height - 2, "m2m");  // parent levels 2..leaf-1 (taskflow.cpp:190-199)
     launch_m2m(c, v, c->s_far);
   });
 }
@@ -357,7 +388,7 @@ int fmmgpu_m2l(fmmgpu_ctx* c, int v) {
 }
 int fmmgpu_l2l(fmmgpu_ctx* c, int v) {
   return guarded(c, [&] {
-    need_level(c, v, 0, c->height - 2, "l2l");
+    need_level(c, v, 2, c->height - 2, "l2l");
     launch_l2l(c, v, c->s_far);
   });
 }
@@ -428,10 +459,17 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
     ~OwReset() { c->ow = false; }
   } ow_reset{c};
   c->ow = c->part_n == 1;
-  if (c->ow) {  // only level 2's local_down is read without being written (L2L's first parent level)
-    if (c->height > 2) {
-      const Level& L2 = c->lv[2];
-      FMM_CUDA(cudaMemsetAsync(L2.local_down, 0, size_t(L2.n) * c->ldE * sizeof(double), s));
+  if (c->ow) {  // only level 2's local_down is read without being written (L2L's first parent
+    // level); levels 0 and 1 (<= 9 cells) are never touched by an evaluation and read as zero
+    // like the reference's (GroupTree::allocate_expansions, geometry.cpp:199-206)
+    for (int v = 0; v <= std::min(2, c->height - 1); ++v) {
+      const Level& L = c->lv[v];
+      const size_t e = size_t(L.n) * c->ldE * sizeof(double);
+      if (v < 2) {
+        FMM_CUDA(cudaMemsetAsync(L.multipole, 0, e, s));
+        FMM_CUDA(cudaMemsetAsync(L.local_own, 0, e, s));
+      }
+      FMM_CUDA(cudaMemsetAsync(L.local_down, 0, e, s));
     }
   } else {
     reset_arrays(c, s);
@@ -993,34 +1031,61 @@ int fmmgpu_download_far(fmmgpu_ctx* c, int v, uint32_t* target, uint32_t* source
   });
 }
 
-int fmmgpu_ledger(fmmgpu_ctx* c, uint64_t* flops7, uint64_t* near_dir, uint64_t* m2l_pairs) {
+// count_interactions + build_ledger (taskflow.cpp:107-135, bench.cpp:151-181) from the
+// device lists: per (kind, level) work and flops, kind-major [7][height], and the M2L
+// pairs per (level, canonical class) [height][16].
+int fmmgpu_ledger_rows(fmmgpu_ctx* c, uint64_t* work, uint64_t* flops, uint64_t* m2l_pairs16) {
   return guarded(c, [&] {
+    need_tree(c);
     if (!c->have_lists) lists_build(c);
     const uint64_t l = c->order, n = c->n;
-    const int leaf = c->height - 1;
-    uint64_t transfers = 0, m2l = 0, pairs = 0;
-    for (int v = 2; v < leaf; ++v) transfers += c->lv[v + 1].n;  // taskflow.cpp:131-133
+    const int h = c->height, leaf = h - 1;
+    std::vector<uint64_t> W(size_t(7) * h, 0), F(size_t(7) * h, 0), P(size_t(16) * h, 0);
+    auto at = [&](int k, int v) { return size_t(k) * h + v; };
+    W[at(FMMGPU_P2M, leaf)] = n;
+    F[at(FMMGPU_P2M, leaf)] = n * (4 * l * l * l + 15 * l);  // bench.cpp:104-122
+    W[at(FMMGPU_L2P, leaf)] = n;
+    F[at(FMMGPU_L2P, leaf)] = n * (16 * l * l * l + 30 * l);
+    W[at(FMMGPU_P2P, leaf)] = c->near_directional;
+    F[at(FMMGPU_P2P, leaf)] = c->near_directional * 15;
+    W[at(FMMGPU_P2PREDUCE, leaf)] = n;
+    for (int v = 2; v < leaf; ++v) {  // transfers[v] = children at v + 1 (taskflow.cpp:131-133)
+      const uint64_t t = c->lv[v + 1].n;
+      W[at(FMMGPU_M2M, v)] = W[at(FMMGPU_L2L, v)] = t;
+      F[at(FMMGPU_M2M, v)] = F[at(FMMGPU_L2L, v)] = t * 6 * l * l * l * l;
+    }
     for (int v = 2; v <= leaf; ++v) {
       const Level& L = c->lv[v];
       const uint64_t ng = (L.block_offsets.size() - 1) * 16;
       std::vector<uint64_t> go(ng + 1);
       FMM_CUDA(cudaMemcpy(go.data(), L.far_group_off, 8 * (ng + 1), cudaMemcpyDeviceToHost));
-      for (uint64_t g = 0; g < ng; ++g) {
-        const uint64_t cnt = go[g + 1] - go[g];
-        const uint64_t r = c->m2l.rank[g % 16];
-        m2l += cnt * (4 * l * l * l * r + r * r);  // bench.cpp:119-122
-        pairs += cnt;
+      for (uint64_t g = 0; g < ng; ++g) P[size_t(v) * 16 + g % 16] += go[g + 1] - go[g];
+      for (int cl = 0; cl < 16; ++cl) {
+        const uint64_t cnt = P[size_t(v) * 16 + cl], r = c->m2l.rank[cl];
+        W[at(FMMGPU_M2L, v)] += cnt;
+        F[at(FMMGPU_M2L, v)] += cnt * (4 * l * l * l * r + r * r);
       }
     }
-    if (flops7) {
-      flops7[0] = n * (4 * l * l * l + 15 * l);
-      flops7[1] = transfers * 6 * l * l * l * l;
-      flops7[2] = m2l;
-      flops7[3] = transfers * 6 * l * l * l * l;
-      flops7[4] = n * (16 * l * l * l + 30 * l);
-      flops7[5] = c->near_directional * 15;
-      flops7[6] = 0;
+    if (work) std::copy(W.begin(), W.end(), work);
+    if (flops) std::copy(F.begin(), F.end(), flops);
+    if (m2l_pairs16) std::copy(P.begin(), P.end(), m2l_pairs16);
+  });
+}
+
+int fmmgpu_ledger(fmmgpu_ctx* c, uint64_t* flops7, uint64_t* near_dir, uint64_t* m2l_pairs) {
+  return guarded(c, [&] {
+    need_tree(c);
+    const int h = c->height;
+    std::vector<uint64_t> W(size_t(7) * h), F(size_t(7) * h);
+    const int rc = fmmgpu_ledger_rows(c, W.data(), F.data(), nullptr);
+    if (rc != FMMGPU_OK) throw Error(rc, c->err);
+    for (int k = 0; k < 7; ++k) {
+      uint64_t f = 0;
+      for (int v = 0; v < h; ++v) f += F[size_t(k) * h + v];
+      if (flops7) flops7[k] = f;
     }
+    uint64_t pairs = 0;
+    for (int v = 0; v < h; ++v) pairs += W[size_t(FMMGPU_M2L) * h + v];
     if (near_dir) *near_dir = c->near_directional;
     if (m2l_pairs) *m2l_pairs = pairs;
   });

@@ -132,19 +132,13 @@ __global__ void k_leaf_scan(const uint32_t* __restrict__ first, const uint32_t* 
     }
     return;
   }
-  for (uint32_t a = lane; a < m; a += 32) {
-    const double xa = px[4 * a];
-    for (uint32_t b = a + 1; b < m; ++b) {
-      if (px[4 * b] == xa) {
-        const double4 pa = pw[f + a], pb = pw[f + b];
-        if (pa.y == pb.y && pa.z == pb.z) atomicOr(flag, 2);
-      }
-    }
-  }
+  // a leaf of more than 64 particles: checked afterwards by the sorted fine-key pass
+  // (one warp would need O(m^2 / 32) steps for it)
+  if (lane == 0) atomicOr(flag, 4);
 }
 
-// Large leaves (mean > 64 particles, e.g. config D's surface cloud): the pairwise
-// per-leaf scan is O(m^2). Instead every particle gets its Morton key at level 21
+// Large leaves (mean > 64 particles, e.g. config D's surface cloud, or any leaf above 64
+// particles found by k_leaf_scan): the pairwise per-leaf scan is O(m^2). Instead every particle gets its Morton key at level 21
 // (equal positions => equal keys), the keys are sorted, and runs of equal keys (tiny:
 // distinct positions share a key only within 2^-21 of the root width) are compared
 // pairwise on the exact positions. Same answer as geometry.cpp:126-136 (equal
@@ -490,13 +484,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   FMM_CUDA(cudaMemsetAsync(L.child_count, 0, 4ull * runs, s));
   FMM_CUDA(cudaMemsetAsync(L.parent, 0, 4ull * runs, s));
   c->d_pcell = dalloc<uint32_t>(c, n, s);
-  if (n <= 64ull * runs) {
-    k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs, c->d_pw,
-                                                                 c->d_pcell, c->d_flag);
-    FMM_CUDA(cudaGetLastError());
-  } else {
-    k_leaf_cells<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs,
-                                                                  c->d_pcell);
+  // exact duplicates via level-21 keys: sort, then compare runs of equal keys
+  auto fine_key_check = [&] {
     uint64_t* fk = dalloc<uint64_t>(c, n, s);
     uint64_t* fks = dalloc<uint64_t>(c, n, s);
     uint32_t* fi = dalloc<uint32_t>(c, n, s);
@@ -510,6 +499,17 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     dfree(c, fks, s);
     dfree(c, fi, s);
     dfree(c, fis, s);
+  };
+  if (n <= 64ull * runs) {
+    // small leaves on average; a leaf above 64 raises flag bit 4 and the sorted check
+    // runs after the readback below (clustered inputs)
+    k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs, c->d_pw,
+                                                                 c->d_pcell, c->d_flag);
+    FMM_CUDA(cudaGetLastError());
+  } else {
+    k_leaf_cells<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs,
+                                                                  c->d_pcell);
+    fine_key_check();
   }
 
   trace("leaf level");
@@ -611,7 +611,11 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   k_copy_words<<<1, 32, 0, s>>>(reinterpret_cast<const uint32_t*>(c->d_flag), 1, d_offs + 9 * height);
   const uint32_t* h_offs = static_cast<const uint32_t*>(readback(c, d_offs, (9 * height + 1) * sizeof(uint32_t), s));
   for (int v = 2; v < height; ++v) std::memcpy(c->lv[v].cls_off, h_offs + 9 * v, 9 * sizeof(uint32_t));
-  const int flag = static_cast<int>(h_offs[9 * height]);
+  int flag = static_cast<int>(h_offs[9 * height]);
+  if ((flag & 4) && !(flag & 3)) {  // a leaf above 64 particles: the sorted fine-key check
+    fine_key_check();
+    flag = *static_cast<const int*>(readback(c, c->d_flag, sizeof(int), s));
+  }
   dfree(c, d_offs, s);
   trace("fields+flag sync");
   if (flag & 1) {

@@ -1,11 +1,17 @@
 // C++ drop-in check of include/taskfmm_b200.hpp (the reference-API mirror over the
 // C ABI). Built and run by tests/test_cpp_adapter.py on a GPU box:
-//   adapter_main <n> <height> <acc> <seed> <out.bin>
-// Runs the evaluation twice — once task by task in a valid reference DAG order
-// (run_task, bench.cpp:255-344), once as evaluate() — writes both field sets, and
-// checks the reference exception classes.
+//   adapter_main <n> <height> <acc> <seed> <out.bin> [<group> <dist> <order.bin>]
+// Runs the evaluation task by task in a valid reference DAG order (run_task,
+// bench.cpp:255-344) and as evaluate(); with an order file (the reference's own task
+// graph for these particles, int32 {kind, level, block} per task, in a topological
+// order that runs the most downstream ready task first) also that order on one thread
+// and the same task list pulled by 8 threads at once (the reference's execute() calls
+// run_task from its workers, runtime.cpp:165). Writes every field set, and checks the
+// reference exception classes.
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <thread>
 #include <stdexcept>
 #include <vector>
 
@@ -27,12 +33,16 @@ static int expect_throw(const char* what, auto&& f, auto tag) {
 }
 
 int main(int argc, char** argv) {
-  if (argc != 6) return 2;
+  if (argc != 6 && argc != 9) return 2;
   RunConfig cfg;
   cfg.n = std::strtoull(argv[1], nullptr, 10);
   cfg.height = std::atoi(argv[2]);
   cfg.acc = std::atoi(argv[3]);
   cfg.seed = std::strtoull(argv[4], nullptr, 10);
+  if (argc == 9) {
+    cfg.group_size = std::atoi(argv[6]);
+    cfg.dist = std::atoi(argv[7]) ? Distribution::Sphere : Distribution::Uniform;
+  }
   auto particles = generate_particles(cfg.n, cfg.dist, cfg.seed);
   FmmContext ctx(particles, cfg);
   const int leaf = cfg.height - 1;
@@ -53,10 +63,33 @@ int main(int argc, char** argv) {
   const auto a = ctx.gather();
   ctx.evaluate();
   const auto b = ctx.gather();
+  std::vector<FmmContext::Fields> sets{a, b};
+  if (argc == 9) {
+    std::vector<Task> tasks;
+    std::FILE* o = std::fopen(argv[8], "rb");
+    if (!o) return 4;
+    std::int32_t t[3];
+    while (std::fread(t, 4, 3, o) == 3)
+      tasks.push_back(Task{static_cast<std::uint32_t>(tasks.size()), static_cast<TaskKind>(t[0]),
+                           static_cast<std::int16_t>(t[1]), static_cast<std::uint32_t>(t[2]), 0});
+    std::fclose(o);
+    ctx.reset();
+    for (const Task& task : tasks) ctx.run_task(task);
+    sets.push_back(ctx.gather());
+    ctx.reset();
+    std::atomic<std::size_t> next{0};
+    std::vector<std::thread> workers;
+    for (int w = 0; w < 8; ++w)
+      workers.emplace_back([&] {
+        for (std::size_t i; (i = next.fetch_add(1)) < tasks.size();) ctx.run_task(tasks[i]);
+      });
+    for (auto& th : workers) th.join();
+    sets.push_back(ctx.gather());
+  }
   std::FILE* f = std::fopen(argv[5], "wb");
   if (!f) return 3;
-  for (const auto* fs : {&a, &b})
-    for (const auto* v : {&fs->potential, &fs->fx, &fs->fy, &fs->fz}) std::fwrite(v->data(), 8, v->size(), f);
+  for (const auto& fs : sets)
+    for (const auto* v : {&fs.potential, &fs.fx, &fs.fy, &fs.fz}) std::fwrite(v->data(), 8, v->size(), f);
   std::fclose(f);
 
   int bad = 0;

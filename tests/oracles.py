@@ -321,6 +321,42 @@ class RefContext:
         self.L.ref_m2l_ranks(self.h, _p(r))
         return r
 
+    def task_graph(self):
+        """TaskGraph (taskflow.hpp:34-42): kind, level, block per task and the successor
+        CSR (off, succ)."""
+        L = self.L
+        L.ref_task_edges.restype = c_uint64
+        nt = L.ref_task_count(self.h)
+        kind = np.zeros(nt, np.uint8)
+        lev = np.zeros(nt, np.int16)
+        blk = np.zeros(nt, np.uint32)
+        work = np.zeros(nt, np.uint64)
+        L.ref_task_info(self.h, _p(kind), _p(lev), _p(blk), _p(work))
+        ne = L.ref_task_edges(self.h, None, None)
+        off = np.zeros(nt + 1, np.uint32)
+        succ = np.zeros(max(ne, 1), np.uint32)
+        L.ref_task_edges(self.h, _p(off), _p(succ))
+        return kind, lev, blk, off, succ[:ne]
+
+    def ledger_rows(self):
+        """count_interactions + build_ledger of this context (bench.cpp:440-442)."""
+        h = self.height
+        work = np.zeros((7, h), dtype=np.uint64)
+        flops = np.zeros((7, h), dtype=np.uint64)
+        pairs = np.zeros((h, 16), dtype=np.uint64)
+        RefLib.check(self.L.ref_ctx_ledger(self.h, _p(flops), _p(work), _p(pairs)))
+        return {"work": work, "flops": flops, "m2l_pairs": pairs}
+
+
+def ref_run_fmm(n, dist, seed, height, acc, out_dir, group_size=250, workers=1, check=1000):
+    """The reference's run_fmm with out_dir (its own results.csv / summary.json writers);
+    returns (eps_potential, eps_force)."""
+    L = RefLib.lib()
+    eps = np.zeros(2)
+    RefLib.check(L.ref_run_fmm(c_uint64(n), {"uniform": 0, "sphere": 1}[dist], c_uint64(seed), height, acc,
+                               group_size, workers, c_uint64(check), out_dir.encode(), _p(eps)))
+    return float(eps[0]), float(eps[1])
+
 
 def relative_l2_error(est, ref):
     """bench.cpp:91-100"""

@@ -43,7 +43,7 @@ for N in (1, 2, 4, 8):
         if r == 0 and N > 1:
             info = c.partition_info()
             a = max(2, info["align_level"])
-            ld = 128 if order <= 5 else 352
+            ld = ((order ** 3 + 31) // 32) * 32  # round_up(l^3, 32), the padded row (csrc ldE)
             for v in range(a, h):
                 cells = c.level(v)[0].shape[0]
                 gather_bytes += (N - 1) / N * cells * ld * 8

@@ -13,6 +13,9 @@ L2 <= 1e-12 of the reference at the same order).
 Config E (100M) is covered by tools/parity_report.py (the reference needs ~80 GB of
 host memory and minutes of setup). The reference runs with all host threads.
 """
+import json
+import os
+
 import pytest
 
 from oracles import RefLib
@@ -46,6 +49,11 @@ def _check(res, shared_tol=1e-13):
 @pytest.mark.parametrize("name", ["A", "H7", "B", "C", "D"])
 def test_config_parity_with_reference(P, name):
     res = config_parity.run(name, P)
+    out = os.environ.get("FMMGPU_PARITY_OUT")
+    if out:  # evidence for BASELINE.md section 4 (tools/parity_report.py writes the same)
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, f"parity_{name}.json"), "w") as f:
+            json.dump(dict(res, host_cpus=os.cpu_count()), f, indent=1)
     print(res)
     _check(res)
 

@@ -115,9 +115,15 @@ void reset_arrays(fmmgpu_ctx* c, cudaStream_t s) {
   FMM_CUDA(cudaMemsetAsync(c->d_far, 0, 32 * c->n, s));
 }
 
+// Event pair -> ms; 0 for a pair that was never recorded (e.g. evaluation timings read
+// before the first evaluation). The failed query's error is consumed here so it cannot
+// surface at an unrelated cudaGetLastError later.
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
-  cudaEventElapsedTime(&ms, a, b);
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0.0f;
+  }
   return ms;
 }
 
@@ -620,7 +626,7 @@ int fmmgpu_synchronize(fmmgpu_ctx* c) {
 int fmmgpu_timings(const fmmgpu_ctx* cc, double* ms) {
   auto* c = const_cast<fmmgpu_ctx*>(cc);
   return guarded(c, [&] {
-    FMM_CUDA(cudaEventSynchronize(c->ev_t[10]));
+    if (cudaEventSynchronize(c->ev_t[10]) != cudaSuccess) (void)cudaGetLastError();  // no evaluation yet
     cudaEvent_t* e = c->ev_t;
     ms[FMMGPU_P2M] = elapsed(e[1], e[2]);
     ms[FMMGPU_M2M] = elapsed(e[2], e[3]);

@@ -17,6 +17,10 @@ from ctypes import c_double, c_int, c_uint, c_uint64, c_void_p, byref
 
 import numpy as np
 
+# the reference's Eigen-shim GEMMs call OpenBLAS inside its own worker threads: one BLAS
+# thread each (read when the library loads), as bench.py's reference arm runs it
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "_build", "liboracle.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libtaskfmm_ref.so")

@@ -34,7 +34,10 @@ def P():
     return P
 
 
-def _check(res, shared_tol=1e-13):
+def _check(res, shared_tol=TOL):
+    # with the reference's own factors the difference is the same to 3 digits (force
+    # 2.3e-13 at B, 4.3e-13 at C): it is summation order (GEMM association, near-field
+    # accumulation order), not the SVD
     assert res["tree"]["bit_exact"], res["tree"]
     if "lists" in res:
         assert res["lists"]["bit_exact"], res["lists"]

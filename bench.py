@@ -373,18 +373,28 @@ def run_ours(args, world, rank, local):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"{args.config}:P2P")
     p2p_tf = flops["P2P"] / (iso["P2P"] / 1e3) / 1e12
-    roof = {"bound": "fp64", "kernel": "k_p2p (P2P, FP64 DFMA/DMUL pipe)", "achieved": p2p_tf,
+    mutual = os.environ.get("FMMGPU_P2P_ONESIDED", "0") != "1"
+    # DP instructions per directional interaction: 12 for the mutual kernel (24 per pair,
+    # both directions), 18 for the one-sided kernel; the ledger counts 15 flop per
+    # directional interaction and the peak 2 flop per DFMA
+    dp_per_dir = 12 if mutual else 18
+    roof = {"bound": "fp64",
+            "kernel": ("k_p2p_mutual + k_p2p_drain (P2P with P2PBuffers slots and ordered reduce, FP64 pipe)"
+                       if mutual else "k_p2p (one-sided P2P, FP64 pipe)"),
+            "achieved": p2p_tf,
             "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s", "frac": p2p_tf / FP64_DFMA_TFLOPS, "traffic": traffic,
             "flops_per_launch": flops["P2P"], "ms_per_launch": iso["P2P"],
             "share_of_step": iso["P2P"] / ms_step,
             "peak_source": "FP64 DFMA measured by tools/microbench/fp64_peaks.cu (profiles/r01_fp64_peaks.txt); "
                            "MEASURED_PEAKS.json has no FP64 figure",
-            "flop_convention": "reference ledger (bench.hpp:49-53): 15 flop per directional interaction "
-                               "(the one-sided kernel issues 18 FP64 instructions per interaction and the "
-                               "peak counts 2 flop per DFMA, so frac <= 15/36 = 0.417 at a saturated FP64 pipe)",
+            "flop_convention": "reference ledger (bench.hpp:49-53): 15 flop per directional interaction; the "
+                               f"kernel issues {dp_per_dir} FP64 instructions per directional interaction and the "
+                               f"peak counts 2 flop per DFMA, so frac <= 15/{2 * dp_per_dir} = "
+                               f"{15 / (2 * dp_per_dir):.3f} at a saturated FP64 pipe",
             # the same launch against the FP64 instruction issue rate (DFMA peak / 2 flop):
-            # useful interactions x 18 DP instructions / duration
-            "fp64_instr_frac": (ledger["near_directional"] * 18 / (iso["P2P"] / 1e3)) / (FP64_DFMA_TFLOPS * 1e12 / 2),
+            # useful interactions x DP instructions per interaction / duration
+            "fp64_instr_frac": (ledger["near_directional"] * dp_per_dir / (iso["P2P"] / 1e3))
+                               / (FP64_DFMA_TFLOPS * 1e12 / 2),
             "m2l": {"bound": "tensor (FP64 DMMA)", "ms_all_levels": iso["M2L"], "ms_leaf": iso_m2l_leaf,
                     "achieved": per_op["M2L"]["tflops"], "peak": FP64_DMMA_TFLOPS,
                     "frac": per_op["M2L"]["frac"]},

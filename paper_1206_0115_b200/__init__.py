@@ -87,6 +87,7 @@ def lib():
         L.fmmgpu_run_wait.argtypes = [c_void_p]
         L.fmmgpu_set_trace.argtypes = [c_void_p, c_int]
         L.fmmgpu_set_graph.argtypes = [c_void_p, c_int]
+        L.fmmgpu_set_p2p_mode.argtypes = [c_void_p, c_int]
         L.fmmgpu_trace_spans.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p]
         for name in ("fmmgpu_reset", "fmmgpu_p2m", "fmmgpu_l2p", "fmmgpu_p2p", "fmmgpu_evaluate",
                      "fmmgpu_synchronize", "fmmgpu_build_lists"):
@@ -443,6 +444,11 @@ class FmmContext:
     def set_graph(self, on: bool = True):
         """Replay evaluations from a captured CUDA graph (fmmgpu_set_graph)."""
         self._check(self._lib.fmmgpu_set_graph(self.h, 1 if on else 0))
+
+    def set_p2p_mode(self, mutual: bool = True):
+        """Near field kernel: mutual (p2p_block(mutual=true) + slots + ordered reduce,
+        direct.cpp:63-92, 151-200) or one-sided (fmmgpu_set_p2p_mode)."""
+        self._check(self._lib.fmmgpu_set_p2p_mode(self.h, 1 if mutual else 0))
 
     def set_trace(self, on: bool = True):
         """Per-launch device trace of the following evaluations (fmmgpu_set_trace)."""

@@ -199,6 +199,11 @@ struct fmmgpu_ctx {
   uint32_t* d_pcell = nullptr;   // leaf cell per Morton slot
   uint32_t* d_inv = nullptr;     // Morton slot per input index (inverse of d_id)
   double* d_near = nullptr;      // near-field fields [n] x {pot,fx,fy,fz} (Morton order)
+  // mutual P2P (p2p.cu): the j-side sums of each leaf's 13 upper half-shell neighbours,
+  // [13][n] x {pot,fx,fy,fz} (the reference's P2PBuffers slots), and the leaf counter
+  bool p2p_mutual = true;
+  double* d_slot = nullptr;
+  uint32_t* d_ctr = nullptr;
   double* d_far = nullptr;       // far-field fields [n] x {pot,fx,fy,fz} (Morton order)
   double* d_out = nullptr;       // gathered fields [4][n] (input order)
   // partition: this context is rank part_rank of part_n; levels below
@@ -277,6 +282,7 @@ void launch_l2l(fmmgpu_ctx* c, int parent_level, cudaStream_t s);
 void launch_l2p(fmmgpu_ctx* c, cudaStream_t s);
 void launch_m2l(fmmgpu_ctx* c, int level, cudaStream_t s);
 void launch_p2p(fmmgpu_ctx* c, cudaStream_t s);
+void ensure_p2p_slots(fmmgpu_ctx* c);  // allocates the mutual P2P slots of the current tree (s_far)
 void launch_gather(fmmgpu_ctx* c, cudaStream_t s);
 void partition_free(fmmgpu_ctx* c);
 }  // namespace fmmgpu

@@ -196,6 +196,11 @@ void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx
   FMM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   for (auto& e : c->ev_t) FMM_CUDA(cudaEventCreate(&e));
   FMM_CUDA(cudaMalloc(&c->d_flag, sizeof(int)));
+  FMM_CUDA(cudaMalloc(&c->d_ctr, 256));
+  {  // FMMGPU_P2P_ONESIDED=1: new contexts start with the one-sided kernel (fmmgpu_set_p2p_mode)
+    const char* pe = std::getenv("FMMGPU_P2P_ONESIDED");
+    c->p2p_mutual = !(pe && std::atoi(pe) == 1);
+  }
   interp_setup(c);
   if (factors) {  // share the operators of an existing context (no second SVD)
     auto& T = c->m2l;
@@ -288,6 +293,7 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
   if (c->nccl) fmmgpu_comm_destroy(c);
   if (c->d_interp) cudaFree(c->d_interp);
   if (c->d_flag) cudaFree(c->d_flag);
+  if (c->d_ctr) cudaFree(c->d_ctr);
   if (c->d_canon) cudaFree(c->d_canon);
   if (c->h_rb) cudaFreeHost(c->h_rb);
   for (auto e : c->tr_ev) cudaEventDestroy(e);
@@ -647,6 +653,14 @@ int fmmgpu_set_graph(fmmgpu_ctx* c, int on) {
   return guarded(c, [&] {
     c->use_graph = on != 0;
     fmmgpu_invalidate_graph(c);
+  });
+}
+
+int fmmgpu_set_p2p_mode(fmmgpu_ctx* c, int mutual) {
+  return guarded(c, [&] {
+    c->p2p_mutual = mutual != 0;
+    fmmgpu_invalidate_graph(c);
+    ensure_p2p_slots(c);
   });
 }
 

@@ -22,6 +22,7 @@
 //
 // Per interaction: 3 DADD (d) + 3 DP (r^2) + MUFU.RSQ64H and 5 DP (Newton)
 // + 1 DMUL (w/r) + 1 DADD (pot) + 2 DMUL (w/r^3) + 3 DFMA (force) = 18 DP ops.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -289,12 +290,323 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
   }
 }
 
+// ================================================================== mutual P2P
+// p2p_block(mutual=true) (direct.cpp:151-184) with the reference's P2PBuffers slots and
+// ordered p2p_reduce (direct.cpp:63-92, 187-200) restated for the GPU: each pair of a
+// leaf c and one of its 13 upper half-shell neighbours q = c + d (d > 0 in (x, y, z)
+// lexicographic order, MU_UP) is evaluated ONCE; c's side accumulates in the warp that
+// owns c, q's side is written to slot s(d) of q's particles ([13][n] double4, single
+// writer) and drained into near[] by k_p2p_drain in the fixed slot order. A leaf's own
+// pairs are evaluated one-sided (i != j), like every pair with a neighbour this rank
+// does not own (partitioned runs), so no slot ever crosses a rank.
+//
+// Warp layout (tools/microbench/p2p_mutual_ceiling.cu "subring"): 4 sub-rings of 8
+// lanes. Each lane holds TS <= 4 SOURCES of c's stream (own leaf, then the half-shell
+// leaves, then non-owned lower neighbours) in registers with their j-side sums; a tile
+// of 8 TARGETS of c rotates around each sub-ring (positions re-read from shared memory,
+// the 4 accumulators moved by SHFL one lane per step), so after 8 steps every lane's
+// sources met all 8 targets and each target's sums are back in their home lane; the
+// 4 sub-rings' partial target sums are then combined by a fixed 2-level butterfly.
+// Per pair: 24 DP instructions + 1 MUFU.RSQ64H for both directions (12 per directional
+// interaction against 18 one-sided).
+//
+// One warp owns a leaf from start to end (targets in chunks of MU_TCAP, every chunk
+// streams all sources; later chunks add into the slots the first one wrote), leaves are
+// pulled from a global counter: results do not depend on which warp ran a leaf, so
+// evaluations stay bitwise reproducible.
+constexpr int MU_WARPS = 8;
+constexpr int MU_TCAP = 64;  // targets per chunk (staged per warp)
+constexpr int MU_TS = 4;     // sources per lane per pass
+constexpr int MU_NUP = 13;
+constexpr int MU_MAXSEG = 27;
+
+// slot s -> upper direction d (s = 0: (0,0,1); 1..3: (0,1,-1..1); 4..12: (1,-1..1,-1..1))
+__device__ __forceinline__ void mu_up(int s, int d[3]) {
+  d[0] = s >= 4 ? 1 : 0;
+  d[1] = s >= 4 ? (s - 4) / 3 - 1 : (s >= 1 ? 1 : 0);
+  d[2] = s >= 4 ? (s - 4) % 3 - 1 : (s >= 1 ? s - 2 : 1);
+}
+
+struct MuArgs {
+  LevelView leaf;
+  const uint32_t* first;
+  const uint32_t* count;
+  const double4* pw;
+  double4* near;
+  double4* slot;      // [13][n]
+  uint64_t n;
+  uint32_t c0, c1;    // leaves this launch processes / drains (the owned range)
+  uint32_t* ctr;      // leaf counter (zeroed before the launch)
+  int ow;             // evaluation: write near instead of adding
+};
+
+struct MuWarp {
+  double4 tpos[MU_TCAP];
+  double4 iacc[MU_TCAP];
+  uint32_t seg_off[MU_MAXSEG + 1];
+  uint32_t seg_first[MU_MAXSEG];
+  int32_t seg_slot[MU_MAXSEG];  // slot index (mutual) or -1 (one-sided)
+};
+
+__device__ __forceinline__ double4 mu_dummy_target() { return make_double4(-1e100, -1e100, -1e100, 0.0); }
+
+// One pair, both directions (direct.cpp:156-169): d = x_t - x_s; the target gets
+// +w_s (inv, inv^3 d), the source +w_t inv and -w_t inv^3 d. The target side is formed
+// exactly as interact() forms it. SELF: i == j (r^2 = +0) contributes nothing.
+template <bool SELF>
+__device__ __forceinline__ void mu_pair(const double4 pt, const double4 ps, const double c375, double4& at,
+                                        double4& as) {
+  const double dx = pt.x - ps.x, dy = pt.y - ps.y, dz = pt.z - ps.z;
+  const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  const double t = r2 * y;
+  const double e = fma(-t, y, 1.0);
+  double inv = fma(y, e * fma(e, c375, 0.5), y);
+  if constexpr (SELF) inv = __double2hiint(r2) != 0 ? inv : 0.0;
+  const double inv2 = inv * inv;
+  const double ws = ps.w * inv, wt = pt.w * inv;
+  at.x += ws;
+  as.x += wt;
+  const double st = ws * inv2, ss = wt * inv2;
+  at.y = fma(st, dx, at.y);
+  at.z = fma(st, dy, at.z);
+  at.w = fma(st, dz, at.w);
+  as.y = fma(-ss, dx, as.y);
+  as.z = fma(-ss, dy, as.z);
+  as.w = fma(-ss, dz, as.w);
+}
+
+__device__ __forceinline__ void add4(double4& a, const double4 b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+
+// One pass: TS sources per lane (stream entries base + lane + 32 m) against every target
+// tile of the staged chunk; then the sources' j-side sums go to their slots.
+template <int TS, bool SELF>
+__device__ __forceinline__ void mu_pass(const MuArgs& a, MuWarp& w, const uint32_t nseg, const uint32_t base,
+                                        const uint32_t total, const int ntile, const bool first_chunk,
+                                        const int lane, const double c375) {
+  double4 ps[TS], as[TS];
+  uint64_t dst[TS];
+#pragma unroll
+  for (int m = 0; m < TS; ++m) {
+    const uint32_t v = base + static_cast<uint32_t>(lane + 32 * m);
+    as[m] = make_double4(0, 0, 0, 0);
+    dst[m] = ~0ull;
+    if (v < total) {
+      int lo = 0, hi = static_cast<int>(nseg) - 1;  // last segment with seg_off <= v
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (w.seg_off[mid] <= v) lo = mid; else hi = mid - 1;
+      }
+      const uint64_t j = uint64_t(w.seg_first[lo]) + (v - w.seg_off[lo]);
+      ps[m] = a.pw[j];
+      const int sl = w.seg_slot[lo];
+      if (sl >= 0) dst[m] = uint64_t(sl) * a.n + j;
+    } else {
+      ps[m] = dummy_source();
+    }
+  }
+  const int l8 = lane & 7;
+  const int nxt = (lane & ~7) | ((l8 + 1) & 7);
+#pragma unroll 1
+  for (int t = 0; t < ntile; ++t) {
+    const double4* tp = w.tpos + 8 * t;
+    double4 at = make_double4(0, 0, 0, 0);
+#pragma unroll 2
+    for (int s = 0; s < 8; ++s) {
+      const double4 pt = tp[(l8 + s) & 7];
+#pragma unroll
+      for (int m = 0; m < TS; ++m) mu_pair<SELF>(pt, ps[m], c375, at, as[m]);
+      at.x = __shfl_sync(0xffffffffu, at.x, nxt);
+      at.y = __shfl_sync(0xffffffffu, at.y, nxt);
+      at.z = __shfl_sync(0xffffffffu, at.z, nxt);
+      at.w = __shfl_sync(0xffffffffu, at.w, nxt);
+    }
+    // lane l of every sub-ring now holds its partial sums of target 8t + l; combine the
+    // four sub-rings (commutative pairs: every lane forms the bitwise same total)
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      at.x += __shfl_xor_sync(0xffffffffu, at.x, o);
+      at.y += __shfl_xor_sync(0xffffffffu, at.y, o);
+      at.z += __shfl_xor_sync(0xffffffffu, at.z, o);
+      at.w += __shfl_xor_sync(0xffffffffu, at.w, o);
+    }
+    if (lane < 8) add4(w.iacc[8 * t + lane], at);
+  }
+#pragma unroll
+  for (int m = 0; m < TS; ++m) {
+    if (dst[m] != ~0ull) {
+      double4 r = as[m];
+      if (!first_chunk) {
+        const double4 o = a.slot[dst[m]];
+        r = make_double4(o.x + r.x, o.y + r.y, o.z + r.z, o.w + r.w);
+      }
+      a.slot[dst[m]] = r;
+    }
+  }
+}
+
+template <bool SELF>
+__device__ __forceinline__ void mu_pass_ts(const int ts, const MuArgs& a, MuWarp& w, const uint32_t nseg,
+                                           const uint32_t base, const uint32_t total, const int ntile,
+                                           const bool first_chunk, const int lane, const double c375) {
+  switch (ts) {
+    case 1: mu_pass<1, SELF>(a, w, nseg, base, total, ntile, first_chunk, lane, c375); break;
+    case 2: mu_pass<2, SELF>(a, w, nseg, base, total, ntile, first_chunk, lane, c375); break;
+    case 3: mu_pass<3, SELF>(a, w, nseg, base, total, ntile, first_chunk, lane, c375); break;
+    default: mu_pass<4, SELF>(a, w, nseg, base, total, ntile, first_chunk, lane, c375); break;
+  }
+}
+
+__global__ void __launch_bounds__(MU_WARPS * 32, 2) k_p2p_mutual(const MuArgs a) {
+  __shared__ MuWarp sw[MU_WARPS];
+  const int lane = threadIdx.x & 31;
+  MuWarp& w = sw[threadIdx.x >> 5];
+  double c375 = 0.375;
+  asm volatile("" : "+d"(c375));
+  for (;;) {
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(a.ctr, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0) + a.c0;
+    if (c >= a.c1) break;
+    int ijk[3];
+    demorton(a.leaf.code[c], ijk);
+    const uint32_t cf = a.first[c], cn = a.count[c];
+    // segments after the own leaf: lanes 0..12 the upper neighbours (mutual when owned,
+    // else one-sided), lanes 13..25 the lower neighbours this rank does not own
+    bool use = false;
+    int sl = -1;
+    uint32_t q = NPOS;
+    if (lane < 2 * MU_NUP) {
+      const int s = lane < MU_NUP ? lane : lane - MU_NUP;
+      const int sg = lane < MU_NUP ? 1 : -1;
+      int d[3];
+      mu_up(s, d);
+      q = find_ijk(a.leaf, ijk[0] + sg * d[0], ijk[1] + sg * d[1], ijk[2] + sg * d[2]);
+      const bool owned = q != NPOS && q >= a.c0 && q < a.c1;
+      use = lane < MU_NUP ? q != NPOS : (q != NPOS && !owned);
+      sl = (lane < MU_NUP && owned) ? s : -1;
+    }
+    const uint32_t mask = __ballot_sync(0xffffffffu, use);
+    const uint32_t cnt = use ? a.count[q] : 0u;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total = cn + __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t nseg = 1u + __popc(mask);
+    if (use) {
+      const int k = 1 + __popc(mask & ((1u << lane) - 1u));
+      w.seg_off[k] = cn + incl - cnt;
+      w.seg_first[k] = a.first[q];
+      w.seg_slot[k] = sl;
+    }
+    if (lane == 0) {
+      w.seg_off[0] = 0;
+      w.seg_first[0] = cf;
+      w.seg_slot[0] = -1;
+      w.seg_off[nseg] = total;
+    }
+    for (uint32_t tc0 = 0; tc0 < cn; tc0 += MU_TCAP) {
+      const uint32_t tcn = min(static_cast<uint32_t>(MU_TCAP), cn - tc0);
+      const int ntile = static_cast<int>((tcn + 7) / 8);
+      __syncwarp();
+      for (int i = lane; i < 8 * ntile; i += 32) {
+        w.tpos[i] = i < static_cast<int>(tcn) ? a.pw[cf + tc0 + i] : mu_dummy_target();
+        w.iacc[i] = make_double4(0, 0, 0, 0);
+      }
+      __syncwarp();
+      for (uint32_t base = 0; base < total; base += 32 * MU_TS) {
+        const int ts = static_cast<int>(min(static_cast<uint32_t>(MU_TS), (total - base + 31) / 32));
+        if (base < cn) mu_pass_ts<true>(ts, a, w, nseg, base, total, ntile, tc0 == 0, lane, c375);
+        else mu_pass_ts<false>(ts, a, w, nseg, base, total, ntile, tc0 == 0, lane, c375);
+        __syncwarp();
+      }
+      for (uint32_t i = lane; i < tcn; i += 32) {
+        const uint64_t tg = uint64_t(cf) + tc0 + i;
+        double4 r = w.iacc[i];
+        if (!a.ow) {
+          const double4 o = a.near[tg];
+          r = make_double4(o.x + r.x, o.y + r.y, o.z + r.z, o.w + r.w);
+        }
+        a.near[tg] = r;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// p2p_reduce (direct.cpp:187-200): near[j] += slot[s][j] in slot order, for every slot
+// whose writer (the leaf q - d(s)) exists and is owned. One warp per leaf.
+__global__ void __launch_bounds__(256) k_p2p_drain(const MuArgs a) {
+  const uint64_t wid = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= a.c1 - a.c0) return;
+  const uint32_t q = a.c0 + static_cast<uint32_t>(wid);
+  int ijk[3];
+  demorton(a.leaf.code[q], ijk);
+  bool has = false;
+  if (lane < MU_NUP) {
+    int d[3];
+    mu_up(lane, d);
+    const uint32_t c = find_ijk(a.leaf, ijk[0] - d[0], ijk[1] - d[1], ijk[2] - d[2]);
+    has = c != NPOS && c >= a.c0 && c < a.c1;
+  }
+  const uint32_t mask = __ballot_sync(0xffffffffu, has);
+  if (!mask) return;
+  const uint32_t qf = a.first[q], qn = a.count[q];
+  for (uint32_t i = lane; i < qn; i += 32) {
+    const uint64_t j = uint64_t(qf) + i;
+    double4 r = a.near[j];
+#pragma unroll
+    for (int s = 0; s < MU_NUP; ++s)
+      if ((mask >> s) & 1u) add4(r, a.slot[uint64_t(s) * a.n + j]);
+    a.near[j] = r;
+  }
+}
+
 }  // namespace
+
+void ensure_p2p_slots(fmmgpu_ctx* c) {
+  const size_t need = size_t(MU_NUP) * 32 * c->n;
+  if (!c->p2p_mutual || !c->have_tree || c->d_slot) return;
+  c->d_slot = static_cast<double*>(cache_alloc(c, need, c->s_far));
+}
 
 void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const int leaf = c->height - 1;
   const Level& L = c->lv[leaf];
   const Level& P = c->lv[leaf - 1];
+  if (c->p2p_mutual) {
+    if (!c->d_slot) throw Error(FMMGPU_LOGIC_ERROR, "mutual P2P: slot array not allocated");
+    const uint32_t nl = L.own1 - L.own0;
+    if (nl == 0) return;
+    MuArgs a{L.view(leaf), L.first_particle, L.particle_count, c->d_pw, reinterpret_cast<double4*>(c->d_near),
+             reinterpret_cast<double4*>(c->d_slot), c->n, L.own0, L.own1, c->d_ctr, c->ow ? 1 : 0};
+    static int blocks_per_sm = [] {
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_p2p_mutual, MU_WARPS * 32, 0) != cudaSuccess) b = 1;
+      return b > 0 ? b : 1;
+    }();
+    int sms = 148;
+    FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    const uint32_t grid = std::min<uint32_t>(static_cast<uint32_t>(sms * blocks_per_sm), (nl + MU_WARPS - 1) / MU_WARPS);
+    FMM_CUDA(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint32_t), s));
+    k_p2p_mutual<<<grid, MU_WARPS * 32, 0, s>>>(a);
+    FMM_CUDA(cudaGetLastError());
+    const uint64_t dthreads = uint64_t(nl) * 32;
+    k_p2p_drain<<<static_cast<unsigned>((dthreads + 255) / 256), 256, 0, s>>>(a);
+    FMM_CUDA(cudaGetLastError());
+    c->launches += 2;
+    return;
+  }
   const uint32_t np = P.own1 - P.own0;
   if (np == 0) return;
   P2PArgs a{L.view(leaf), P.code, P.own0, np, 1, L.first_particle, L.particle_count, c->d_pw,

@@ -355,6 +355,7 @@ void tree_free(fmmgpu_ctx* c) {
   c->lv.clear();
   dfree(c, c->d_pw, s); dfree(c, c->d_id, s); dfree(c, c->d_inv, s); dfree(c, c->d_pcell, s);
   dfree(c, c->d_near, s); dfree(c, c->d_far, s); dfree(c, c->d_out, s);
+  dfree(c, c->d_slot, s);
   c->have_tree = false;
 }
 
@@ -627,6 +628,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     throw Error(FMMGPU_DOMAIN_ERROR, "GroupTree: coincident particles");
   }
   c->have_tree = true;
+  ensure_p2p_slots(c);
   cache_trim_old(c, s);  // blocks of the previous tree this one did not reuse
 }
 

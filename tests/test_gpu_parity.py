@@ -163,16 +163,42 @@ def test_operators_per_level(fmm, case, tmp_path):
     assert force_error(*far[1:], *ofar[1:]) <= 1e-13
 
 
+@pytest.mark.parametrize("mutual", [True, False], ids=["mutual", "onesided"])
 @pytest.mark.parametrize("case", CASES, ids=[f"n{c[0]}_h{c[1]}_l{c[2]}_{c[3]}{'_w' if c[5] else ''}" for c in CASES])
-def test_p2p_near_field(fmm, case):
+def test_p2p_near_field(fmm, case, mutual):
+    """Both near-field kernels (p2p_block mutual=true with slots + ordered reduce, and
+    one-sided) against the oracle's mutual P2P + ordered slot drain (direct.cpp:151-200),
+    standalone (accumulating) and inside an evaluation (writing), bitwise reproducible."""
     n, h, l, dist, seed, rw = case
     xyzw = make_particles(n, dist, seed, rw)
     _, near = _oracle_eval(xyzw, h, l, 32)  # mutual P2P + ordered slot drain
     c = ctx_for(fmm, xyzw, h, l)
+    c.set_p2p_mode(mutual)
     c.run_kinds({"P2P"})
     g = c.gather()
     assert relative_l2_error(g[0], near[0]) <= 1e-14
     assert force_error(*g[1:], *near[1:]) <= 1e-13
+    c.run_kinds({"P2P"})  # accumulate mode: reset + P2P again gives the same bits
+    g2 = c.gather()
+    for x, y in zip(g, g2):
+        assert np.array_equal(x, y)
+
+
+def test_p2p_mutual_matches_onesided_in_evaluation(fmm):
+    """Evaluation with the mutual kernel vs the one-sided kernel: same far field (bitwise),
+    near fields equal to rounding; the mutual run is bitwise reproducible."""
+    xyzw = make_particles(60000, "uniform", 21, True)
+    c = ctx_for(fmm, xyzw, 5, 5)
+    out = {}
+    for mode in (False, True, True):
+        c.set_p2p_mode(mode)
+        c.evaluate()
+        out.setdefault(mode, []).append(c.gather())
+    a, b = out[False][0], out[True][0]
+    assert relative_l2_error(b[0], a[0]) <= 1e-15
+    assert force_error(*b[1:], *a[1:]) <= 1e-14
+    for x, y in zip(out[True][0], out[True][1]):
+        assert np.array_equal(x, y)
 
 
 @pytest.mark.parametrize("case", CASES, ids=[f"n{c[0]}_h{c[1]}_l{c[2]}_{c[3]}{'_w' if c[5] else ''}" for c in CASES])

@@ -25,7 +25,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfmmgpu.so")
+# FMMGPU_LIB: another in-tree build of the library (compile-time variants for A/B timing)
+LIB_PATH = os.path.join(_HERE, os.path.basename(os.environ.get("FMMGPU_LIB", "libfmmgpu.so")))
 
 KINDS = ("P2M", "M2M", "M2L", "L2L", "L2P", "P2P", "P2PREDUCE")
 DISTS = {"uniform": 0, "sphere": 1, "ellipsoid": 2}

@@ -204,6 +204,11 @@ struct fmmgpu_ctx {
   bool p2p_mutual = true;
   double* d_slot = nullptr;
   uint32_t* d_ctr = nullptr;
+  // non-full leaf levels: leaves by decreasing work (+ sort buffers), valid for the owned
+  // leaf range p2p_order_range = {own0, own1 + 1} (0, 0 = not computed)
+  uint32_t* d_p2p_order = nullptr;
+  size_t p2p_order_tmp = 0;
+  uint32_t p2p_order_range[2] = {0, 0};
   double* d_far = nullptr;       // far-field fields [n] x {pot,fx,fy,fz} (Morton order)
   double* d_out = nullptr;       // gathered fields [4][n] (input order)
   // partition: this context is rank part_rank of part_n; levels below

@@ -22,6 +22,8 @@
 //
 // Per interaction: 3 DADD (d) + 3 DP (r^2) + MUFU.RSQ64H and 5 DP (Newton)
 // + 1 DMUL (w/r) + 1 DADD (pot) + 2 DMUL (w/r^3) + 3 DFMA (force) = 18 DP ops.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -310,12 +312,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
 // Per pair: 24 DP instructions + 1 MUFU.RSQ64H for both directions (12 per directional
 // interaction against 18 one-sided).
 //
-// One warp owns a leaf from start to end (targets in chunks of MU_TCAP, every chunk
+// One warp owns a leaf from start to end (targets in chunks of TCAP, every chunk
 // streams all sources; later chunks add into the slots the first one wrote), leaves are
 // pulled from a global counter: results do not depend on which warp ran a leaf, so
 // evaluations stay bitwise reproducible.
 constexpr int MU_WARPS = 8;
-constexpr int MU_TCAP = 64;  // targets per chunk (staged per warp)
 constexpr int MU_TS = 4;     // sources per lane per pass
 constexpr int MU_NUP = 13;
 constexpr int MU_MAXSEG = 27;
@@ -337,12 +338,17 @@ struct MuArgs {
   uint64_t n;
   uint32_t c0, c1;    // leaves this launch processes / drains (the owned range)
   uint32_t* ctr;      // leaf counter (zeroed before the launch)
+  const uint32_t* order;  // leaves by decreasing work (non-uniform trees), nullptr = c0 ..
   int ow;             // evaluation: write near instead of adding
 };
 
+// per-warp shared memory; TCAP = targets per chunk (64 on full leaf levels, 128 else:
+// config B 11.07 ms with 64 against 13.5 with 128 -- the larger CTA leaves less L1 for
+// the source loads -- and config D 192 -> 163 ms with 128 and the largest-first order)
+template <int TCAP>
 struct MuWarp {
-  double4 tpos[MU_TCAP];
-  double4 iacc[MU_TCAP];
+  double4 tpos[TCAP];
+  double4 iacc[TCAP];
   uint32_t seg_off[MU_MAXSEG + 1];
   uint32_t seg_first[MU_MAXSEG];
   int32_t seg_slot[MU_MAXSEG];  // slot index (mutual) or -1 (one-sided)
@@ -384,12 +390,58 @@ __device__ __forceinline__ void add4(double4& a, const double4 b) {
   a.w += b.w;
 }
 
-// One pass: TS sources per lane (stream entries base + lane + 32 m) against every target
-// tile of the staged chunk; then the sources' j-side sums go to their slots.
-template <int TS, bool SELF>
-__device__ __forceinline__ void mu_pass(const MuArgs& a, MuWarp& w, const uint32_t nseg, const uint32_t base,
-                                        const uint32_t total, const int ntile, const bool first_chunk,
+// One target tile of RING (8, or 4 for a leaf's last 1..4 targets) at targets
+// tpos[t0 .. t0+RING) against the lane's TS sources: each step every lane meets one target
+// (TS pairs), then the target accumulators move one lane on around the lane's sub-ring;
+// after RING steps lane l of every sub-ring holds its partial sums of target t0 + l, and
+// the 32 / RING sub-rings are combined by a fixed butterfly (commutative pairs: every
+// lane forms the bitwise same total).
+template <int TS, int RING, bool SELF, class W>
+__device__ __forceinline__ void mu_tile(W& w, const int t0, const double4 (&ps)[TS], double4 (&as)[TS],
                                         const int lane, const double c375) {
+  const int lr = lane & (RING - 1);
+  const int nxt = (lane & ~(RING - 1)) | ((lr + 1) & (RING - 1));
+  const double4* tp = w.tpos + t0;
+  double4 at = make_double4(0, 0, 0, 0);
+#pragma unroll 2
+  for (int s = 0; s < RING; ++s) {
+    const double4 pt = tp[(lr + s) & (RING - 1)];
+#pragma unroll
+    for (int m = 0; m < TS; ++m) mu_pair<SELF>(pt, ps[m], c375, at, as[m]);
+    at.x = __shfl_sync(0xffffffffu, at.x, nxt);
+    at.y = __shfl_sync(0xffffffffu, at.y, nxt);
+    at.z = __shfl_sync(0xffffffffu, at.z, nxt);
+    at.w = __shfl_sync(0xffffffffu, at.w, nxt);
+  }
+#pragma unroll
+  for (int o = RING; o < 32; o <<= 1) {
+    at.x += __shfl_xor_sync(0xffffffffu, at.x, o);
+    at.y += __shfl_xor_sync(0xffffffffu, at.y, o);
+    at.z += __shfl_xor_sync(0xffffffffu, at.z, o);
+    at.w += __shfl_xor_sync(0xffffffffu, at.w, o);
+  }
+  if (lane < RING) add4(w.iacc[t0 + lane], at);
+}
+
+// stream entry v -> (global particle index, slot index or -1)
+template <class W>
+__device__ __forceinline__ uint64_t mu_locate(const W& w, const uint32_t nseg, const uint32_t v, int& sl) {
+  int lo = 0, hi = static_cast<int>(nseg) - 1;  // last segment with seg_off <= v
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (w.seg_off[mid] <= v) lo = mid; else hi = mid - 1;
+  }
+  sl = w.seg_slot[lo];
+  return uint64_t(w.seg_first[lo]) + (v - w.seg_off[lo]);
+}
+
+// One pass: TS sources per lane (stream entries base + lane + 32 m) against the tcn staged
+// targets; then the sources' j-side sums go to their slots (the first target chunk
+// writes them, later chunks of a large leaf add).
+template <int TS, bool SELF, class W>
+__device__ __forceinline__ void mu_pass(const MuArgs& a, W& w, const uint32_t nseg, const uint32_t base,
+                                        const uint32_t total, const int tcn, const bool first_chunk, const int lane,
+                                        const double c375) {
   double4 ps[TS], as[TS];
   uint64_t dst[TS];
 #pragma unroll
@@ -398,46 +450,23 @@ __device__ __forceinline__ void mu_pass(const MuArgs& a, MuWarp& w, const uint32
     as[m] = make_double4(0, 0, 0, 0);
     dst[m] = ~0ull;
     if (v < total) {
-      int lo = 0, hi = static_cast<int>(nseg) - 1;  // last segment with seg_off <= v
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (w.seg_off[mid] <= v) lo = mid; else hi = mid - 1;
-      }
-      const uint64_t j = uint64_t(w.seg_first[lo]) + (v - w.seg_off[lo]);
+      int sl;
+      const uint64_t j = mu_locate(w, nseg, v, sl);
       ps[m] = a.pw[j];
-      const int sl = w.seg_slot[lo];
       if (sl >= 0) dst[m] = uint64_t(sl) * a.n + j;
     } else {
       ps[m] = dummy_source();
     }
   }
-  const int l8 = lane & 7;
-  const int nxt = (lane & ~7) | ((l8 + 1) & 7);
+  // 8-target tiles, and a last tile of 4 when only 1..4 targets remain
+  const int n8 = (tcn & 7) > 4 ? (tcn + 7) & ~7 : tcn & ~7;
 #pragma unroll 1
-  for (int t = 0; t < ntile; ++t) {
-    const double4* tp = w.tpos + 8 * t;
-    double4 at = make_double4(0, 0, 0, 0);
-#pragma unroll 2
-    for (int s = 0; s < 8; ++s) {
-      const double4 pt = tp[(l8 + s) & 7];
-#pragma unroll
-      for (int m = 0; m < TS; ++m) mu_pair<SELF>(pt, ps[m], c375, at, as[m]);
-      at.x = __shfl_sync(0xffffffffu, at.x, nxt);
-      at.y = __shfl_sync(0xffffffffu, at.y, nxt);
-      at.z = __shfl_sync(0xffffffffu, at.z, nxt);
-      at.w = __shfl_sync(0xffffffffu, at.w, nxt);
-    }
-    // lane l of every sub-ring now holds its partial sums of target 8t + l; combine the
-    // four sub-rings (commutative pairs: every lane forms the bitwise same total)
-#pragma unroll
-    for (int o = 8; o < 32; o <<= 1) {
-      at.x += __shfl_xor_sync(0xffffffffu, at.x, o);
-      at.y += __shfl_xor_sync(0xffffffffu, at.y, o);
-      at.z += __shfl_xor_sync(0xffffffffu, at.z, o);
-      at.w += __shfl_xor_sync(0xffffffffu, at.w, o);
-    }
-    if (lane < 8) add4(w.iacc[8 * t + lane], at);
-  }
+  for (int t0 = 0; t0 < n8; t0 += 8) mu_tile<TS, 8, SELF>(w, t0, ps, as, lane, c375);
+#ifndef FMMGPU_MU_NO_RING4
+  if (tcn > n8) mu_tile<TS, 4, SELF>(w, n8, ps, as, lane, c375);
+#else
+  if (tcn > n8) mu_tile<TS, 8, SELF>(w, n8, ps, as, lane, c375);
+#endif
 #pragma unroll
   for (int m = 0; m < TS; ++m) {
     if (dst[m] != ~0ull) {
@@ -451,29 +480,32 @@ __device__ __forceinline__ void mu_pass(const MuArgs& a, MuWarp& w, const uint32
   }
 }
 
-template <bool SELF>
-__device__ __forceinline__ void mu_pass_ts(const int ts, const MuArgs& a, MuWarp& w, const uint32_t nseg,
-                                           const uint32_t base, const uint32_t total, const int ntile,
+template <bool SELF, class W>
+__device__ __forceinline__ void mu_pass_ts(const int ts, const MuArgs& a, W& w, const uint32_t nseg,
+                                           const uint32_t base, const uint32_t total, const int tcn,
                                            const bool first_chunk, const int lane, const double c375) {
   switch (ts) {
-    case 1: mu_pass<1, SELF>(a, w, nseg, base, total, ntile, first_chunk, lane, c375); break;
-    case 2: mu_pass<2, SELF>(a, w, nseg, base, total, ntile, first_chunk, lane, c375); break;
-    case 3: mu_pass<3, SELF>(a, w, nseg, base, total, ntile, first_chunk, lane, c375); break;
-    default: mu_pass<4, SELF>(a, w, nseg, base, total, ntile, first_chunk, lane, c375); break;
+    case 1: mu_pass<1, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
+    case 2: mu_pass<2, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
+    case 3: mu_pass<3, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
+    default: mu_pass<MU_TS, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
   }
 }
 
+template <int TCAP>
 __global__ void __launch_bounds__(MU_WARPS * 32, 2) k_p2p_mutual(const MuArgs a) {
-  __shared__ MuWarp sw[MU_WARPS];
+  extern __shared__ __align__(16) unsigned char mu_smem[];
   const int lane = threadIdx.x & 31;
-  MuWarp& w = sw[threadIdx.x >> 5];
+  MuWarp<TCAP>& w = reinterpret_cast<MuWarp<TCAP>*>(mu_smem)[threadIdx.x >> 5];
   double c375 = 0.375;
   asm volatile("" : "+d"(c375));
+  const uint32_t nl = a.c1 - a.c0;
   for (;;) {
-    uint32_t c = 0;
-    if (lane == 0) c = atomicAdd(a.ctr, 1u);
-    c = __shfl_sync(0xffffffffu, c, 0) + a.c0;
-    if (c >= a.c1) break;
+    uint32_t u = 0;
+    if (lane == 0) u = atomicAdd(a.ctr, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nl) break;
+    const uint32_t c = a.order ? a.order[u] : a.c0 + u;
     int ijk[3];
     demorton(a.leaf.code[c], ijk);
     const uint32_t cf = a.first[c], cn = a.count[c];
@@ -514,22 +546,21 @@ __global__ void __launch_bounds__(MU_WARPS * 32, 2) k_p2p_mutual(const MuArgs a)
       w.seg_slot[0] = -1;
       w.seg_off[nseg] = total;
     }
-    for (uint32_t tc0 = 0; tc0 < cn; tc0 += MU_TCAP) {
-      const uint32_t tcn = min(static_cast<uint32_t>(MU_TCAP), cn - tc0);
-      const int ntile = static_cast<int>((tcn + 7) / 8);
+    for (uint32_t tc0 = 0; tc0 < cn; tc0 += TCAP) {
+      const int tcn = static_cast<int>(min(static_cast<uint32_t>(TCAP), cn - tc0));
       __syncwarp();
-      for (int i = lane; i < 8 * ntile; i += 32) {
-        w.tpos[i] = i < static_cast<int>(tcn) ? a.pw[cf + tc0 + i] : mu_dummy_target();
+      for (int i = lane; i < ((tcn + 7) & ~7); i += 32) {
+        w.tpos[i] = i < tcn ? a.pw[cf + tc0 + i] : mu_dummy_target();
         w.iacc[i] = make_double4(0, 0, 0, 0);
       }
       __syncwarp();
       for (uint32_t base = 0; base < total; base += 32 * MU_TS) {
         const int ts = static_cast<int>(min(static_cast<uint32_t>(MU_TS), (total - base + 31) / 32));
-        if (base < cn) mu_pass_ts<true>(ts, a, w, nseg, base, total, ntile, tc0 == 0, lane, c375);
-        else mu_pass_ts<false>(ts, a, w, nseg, base, total, ntile, tc0 == 0, lane, c375);
+        if (base < cn) mu_pass_ts<true>(ts, a, w, nseg, base, total, tcn, tc0 == 0, lane, c375);
+        else mu_pass_ts<false>(ts, a, w, nseg, base, total, tcn, tc0 == 0, lane, c375);
         __syncwarp();
       }
-      for (uint32_t i = lane; i < tcn; i += 32) {
+      for (int i = lane; i < tcn; i += 32) {
         const uint64_t tg = uint64_t(cf) + tc0 + i;
         double4 r = w.iacc[i];
         if (!a.ow) {
@@ -574,11 +605,67 @@ __global__ void __launch_bounds__(256) k_p2p_drain(const MuArgs a) {
 
 }  // namespace
 
-void ensure_p2p_slots(fmmgpu_ctx* c) {
-  const size_t need = size_t(MU_NUP) * 32 * c->n;
-  if (!c->p2p_mutual || !c->have_tree || c->d_slot) return;
-  c->d_slot = static_cast<double*>(cache_alloc(c, need, c->s_far));
+namespace {
+// work estimate of a leaf (its targets x its stream), complemented so an ascending radix
+// sort puts the heaviest leaves first
+__global__ void k_mu_work(const LevelView leaf, const uint32_t* __restrict__ count, const uint32_t c0,
+                          const uint32_t nl, uint64_t* __restrict__ key, uint32_t* __restrict__ idx) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nl) return;
+  const uint32_t c = c0 + i;
+  int ijk[3];
+  demorton(leaf.code[c], ijk);
+  uint64_t tot = count[c];
+  for (int s = 0; s < MU_NUP; ++s) {
+    int d[3];
+    mu_up(s, d);
+    const uint32_t q = find_ijk(leaf, ijk[0] + d[0], ijk[1] + d[1], ijk[2] + d[2]);
+    if (q != NPOS) tot += count[q];
+  }
+  key[i] = ~(uint64_t(count[c]) * tot);
+  idx[i] = c;
 }
+}  // namespace
+
+// The slot array of the current tree and, for trees with a non-full leaf level (clustered
+// clouds, config D), the buffers of the largest-first leaf order: allocated with the tree
+// on s_far (ordered before any evaluation's fork).
+void ensure_p2p_slots(fmmgpu_ctx* c) {
+  if (!c->p2p_mutual || !c->have_tree || c->d_slot) return;
+  c->d_slot = static_cast<double*>(cache_alloc(c, size_t(MU_NUP) * 32 * c->n, c->s_far));
+  c->p2p_order_range[0] = c->p2p_order_range[1] = 0;
+  const Level& L = c->lv[c->height - 1];
+  if (L.full) return;
+  size_t tmp = 0;
+  FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, static_cast<const uint64_t*>(nullptr),
+                                           static_cast<uint64_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                           static_cast<uint32_t*>(nullptr), static_cast<int>(L.n)));
+  c->p2p_order_tmp = tmp;
+  c->d_p2p_order = static_cast<uint32_t*>(cache_alloc(c, (24 + 1) * size_t(L.n) + tmp + 256, c->s_far));
+}
+
+namespace {
+// the largest-first order of the owned leaves (recomputed when the owned range changed)
+const uint32_t* p2p_order(fmmgpu_ctx* c, const Level& L, cudaStream_t s) {
+  if (!c->d_p2p_order) return nullptr;
+  if (c->p2p_order_range[0] == L.own0 && c->p2p_order_range[1] == L.own1 + 1) return c->d_p2p_order;
+  const uint32_t nl = L.own1 - L.own0;
+  auto* base = reinterpret_cast<unsigned char*>(c->d_p2p_order);
+  uint32_t* out = c->d_p2p_order;                                   // [n] sorted leaves
+  auto* idx = reinterpret_cast<uint32_t*>(base + 4 * size_t(L.n));  // [n]
+  auto* key = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(base + 8 * size_t(L.n)) + 7) & ~uintptr_t(7));
+  uint64_t* key2 = key + L.n;
+  void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(key2 + L.n) + 255) & ~uintptr_t(255));
+  k_mu_work<<<(nl + 255) / 256, 256, 0, s>>>(L.view(c->height - 1), L.particle_count, L.own0, nl, key, idx);
+  FMM_CUDA(cudaGetLastError());
+  size_t tb = c->p2p_order_tmp;
+  FMM_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, idx, out, static_cast<int>(nl), 0, 64, s));
+  c->launches += 2;
+  c->p2p_order_range[0] = L.own0;
+  c->p2p_order_range[1] = L.own1 + 1;
+  return out;
+}
+}  // namespace
 
 void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const int leaf = c->height - 1;
@@ -589,17 +676,25 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
     const uint32_t nl = L.own1 - L.own0;
     if (nl == 0) return;
     MuArgs a{L.view(leaf), L.first_particle, L.particle_count, c->d_pw, reinterpret_cast<double4*>(c->d_near),
-             reinterpret_cast<double4*>(c->d_slot), c->n, L.own0, L.own1, c->d_ctr, c->ow ? 1 : 0};
-    static int blocks_per_sm = [] {
-      int b = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_p2p_mutual, MU_WARPS * 32, 0) != cudaSuccess) b = 1;
-      return b > 0 ? b : 1;
-    }();
+             reinterpret_cast<double4*>(c->d_slot), c->n, L.own0, L.own1, c->d_ctr, p2p_order(c, L, s), c->ow ? 1 : 0};
+    // Measured alternatives at config B (P2P 11.07 ms with 4 sources per lane, the rotation
+    // unrolled twice, 8-warp CTAs, 2 per SM at 128 registers): 2 or 3 sources per lane with
+    // two target tiles interleaved per step (11.72 / 12.23 ms), 3 CTAs per SM at 80
+    // registers (11.77 ms, spills), 4-warp CTAs with 20 warps per SM (11.5 ms), the rotation
+    // unrolled 4 / 8 times (12.3 / 17.8 ms, register pressure), the slot addresses
+    // recomputed instead of held (11.36 ms).
     int sms = 148;
     FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-    const uint32_t grid = std::min<uint32_t>(static_cast<uint32_t>(sms * blocks_per_sm), (nl + MU_WARPS - 1) / MU_WARPS);
-    FMM_CUDA(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint32_t), s));
-    k_p2p_mutual<<<grid, MU_WARPS * 32, 0, s>>>(a);
+    auto go = [&](auto kern, int smem) {
+      int b = 0;
+      FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, MU_WARPS * 32, smem) != cudaSuccess || b < 1) b = 1;
+      const uint32_t grid = std::min<uint32_t>(static_cast<uint32_t>(sms * b), (nl + MU_WARPS - 1) / MU_WARPS);
+      FMM_CUDA(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint32_t), s));
+      kern<<<grid, MU_WARPS * 32, smem, s>>>(a);
+    };
+    if (L.full) go(k_p2p_mutual<64>, static_cast<int>(MU_WARPS * sizeof(MuWarp<64>)));
+    else go(k_p2p_mutual<128>, static_cast<int>(MU_WARPS * sizeof(MuWarp<128>)));
     FMM_CUDA(cudaGetLastError());
     const uint64_t dthreads = uint64_t(nl) * 32;
     k_p2p_drain<<<static_cast<unsigned>((dthreads + 255) / 256), 256, 0, s>>>(a);

@@ -356,6 +356,7 @@ void tree_free(fmmgpu_ctx* c) {
   dfree(c, c->d_pw, s); dfree(c, c->d_id, s); dfree(c, c->d_inv, s); dfree(c, c->d_pcell, s);
   dfree(c, c->d_near, s); dfree(c, c->d_far, s); dfree(c, c->d_out, s);
   dfree(c, c->d_slot, s);
+  dfree(c, c->d_p2p_order, s);
   c->have_tree = false;
 }
 

@@ -6,7 +6,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
 h = int(sys.argv[2]) if len(sys.argv) > 2 else 7
 l = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 evals = int(sys.argv[4]) if len(sys.argv) > 4 else 2
-xyzw = P.generate_particles(n, "uniform", 42)
+dist = sys.argv[5] if len(sys.argv) > 5 else "uniform"
+xyzw = P.generate_particles(n, dist, 42)
 c = P.FmmContext(None, order=l)
 c.build_tree(xyzw, h)
 for _ in range(evals):

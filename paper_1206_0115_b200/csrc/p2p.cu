@@ -575,7 +575,10 @@ __global__ void __launch_bounds__(MU_WARPS * 32, 2) k_p2p_mutual(const MuArgs a)
 }
 
 // p2p_reduce (direct.cpp:187-200): near[j] += slot[s][j] in slot order, for every slot
-// whose writer (the leaf q - d(s)) exists and is owned. One warp per leaf.
+// whose writer (the leaf q - d(s)) exists and is owned. One warp per leaf. A separate
+// HBM-bound pass (0.77 ms at config B, 6 TB/s): draining inside k_p2p_mutual by the warp
+// that completes a leaf's writer count (release atomics, L2 reads) measured slower
+// (config B P2P 10.93 -> 14.07 ms, D 163 -> 177 ms).
 __global__ void __launch_bounds__(256) k_p2p_drain(const MuArgs a) {
   const uint64_t wid = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;

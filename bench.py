@@ -70,7 +70,7 @@ def config_dict(name, world=1):
     """The workload description shared by both arms' JSON lines."""
     n, dist, h, order, desc = CONFIGS[name]
     return {"workload": desc, "n": n, "height": h, "order": order, "eps": 10.0 ** -order, "group_size": 250,
-            "parallelism": f"morton-range partition x{world}, NCCL multipole all-gather per upward level"
+            "parallelism": f"morton-range partition x{world}; NCCL exchange per upward level: all-gather at the alignment level, per-peer halo send/recv below"
                            if world > 1 else "single",
             "l2": "inputs (32 B/particle + 1 KB per leaf expansion array) exceed the 126 MB L2"}
 

@@ -207,10 +207,23 @@ int fmmgpu_direct(fmmgpu_ctx* ctx, const uint32_t* targets, uint64_t k, double* 
  * contiguous Morton ranges aligned to the cells of an alignment level and balanced by
  * estimated work; levels below it are replicated. Evaluations then compute only the
  * owned targets (gathered fields are zero for other particles), with one exchange per
- * upward level >= the alignment level: an all-gather of that level's multipoles, done
- * by an attached NCCL communicator inside fmmgpu_evaluate, or by the host between
- * fmmgpu_upward_level calls (stepped API). nranks = 1 restores the full evaluation. */
+ * upward level >= the alignment level (fmmgpu_exchange_plan): the alignment level's
+ * multipoles are all-gathered when the replicated levels above it need them, deeper
+ * levels exchange only the halo the M2L of each rank reads (per-peer send / receive).
+ * An attached NCCL communicator does it inside fmmgpu_evaluate; without one the host
+ * does it between fmmgpu_upward_level calls (stepped API). nranks = 1 restores the full
+ * evaluation; 1 <= nranks <= 64. */
 int fmmgpu_partition(fmmgpu_ctx* ctx, int rank, int nranks);
+/* Exchange after the upward step of `level`: *kind = 0 none, 1 all-gather of every rank's
+ * owned rows (fmmgpu_partition_ranges), 2 halo. For kind 2: the cells (ascending row
+ * indices of the level) this rank sends to `peer` and receives from `peer`; arrays may be
+ * NULL to query the counts. A rank's receive list from p equals p's send list to it. */
+int fmmgpu_exchange_plan(const fmmgpu_ctx* ctx, int level, int peer, int* kind, uint32_t* send_cells,
+                         uint32_t* send_count, uint32_t* recv_cells, uint32_t* recv_count);
+/* Measurement aid (tools/scaling_projection.py): skip_exchange = 1 times one rank's
+ * partitioned work on a single device without its peers; fields downloaded while it is
+ * set are refused (FMMGPU_LOGIC_ERROR). */
+int fmmgpu_set_measurement(fmmgpu_ctx* ctx, int skip_exchange);
 /* first owned cell of every rank at `level` (nranks + 1 entries, last = cell count) */
 int fmmgpu_partition_ranges(const fmmgpu_ctx* ctx, int level, uint32_t* begins);
 int fmmgpu_partition_info(const fmmgpu_ctx* ctx, int* rank, int* nranks, int* align_level,

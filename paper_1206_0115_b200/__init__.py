@@ -103,6 +103,8 @@ def lib():
         L.fmmgpu_comm_init.argtypes = [c_void_p, ctypes.c_char_p, c_int, c_int]
         L.fmmgpu_comm_destroy.argtypes = [c_void_p]
         L.fmmgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
+        L.fmmgpu_exchange_plan.argtypes = [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+        L.fmmgpu_set_measurement.argtypes = [c_void_p, c_int]
         _lib = L
     return _lib
 
@@ -406,6 +408,23 @@ class FmmContext:
         out = np.zeros(n + 1, dtype=np.uint32)
         self._check(self._lib.fmmgpu_partition_ranges(self.h, level, _p(out)))
         return out
+
+    def exchange_plan(self, level: int, peer: int = 0):
+        """(kind, send_cells, recv_cells) of the exchange after the upward step of `level`
+        with `peer`: kind 0 none, 1 all-gather of the owned rows, 2 halo (fmmgpu_exchange_plan)."""
+        kind = c_int()
+        sc, rc = ctypes.c_uint32(), ctypes.c_uint32()
+        self._check(self._lib.fmmgpu_exchange_plan(self.h, level, peer, byref(kind), None, byref(sc), None, byref(rc)))
+        snd = np.zeros(sc.value, dtype=np.uint32)
+        rcv = np.zeros(rc.value, dtype=np.uint32)
+        if kind.value == 2:
+            self._check(self._lib.fmmgpu_exchange_plan(self.h, level, peer, byref(kind), _p(snd), byref(sc), _p(rcv),
+                                                       byref(rc)))
+        return kind.value, snd, rcv
+
+    def set_measurement(self, skip_exchange: bool = True):
+        """Measurement aid: partitioned evaluations skip the exchange (fields then refused)."""
+        self._check(self._lib.fmmgpu_set_measurement(self.h, 1 if skip_exchange else 0))
 
     def comm_init(self, uid: bytes, nranks: int, rank: int):
         self._check(self._lib.fmmgpu_comm_init(self.h, uid, nranks, rank))

@@ -122,6 +122,12 @@ struct Level {
   uint32_t srcA_off[9] = {};
   uint32_t* tgtB = nullptr;
   uint32_t tgtB_off[9] = {};
+  // exchange after this level's upward step (partitioned runs): 0 none, 1 all-gather of
+  // the owned rows, 2 halo -- rows sent to / received from every peer (host lists with
+  // per-peer offsets, device indices: sends then receives)
+  int xkind = 0;
+  std::vector<uint32_t> halo_send, halo_recv, halo_send_off, halo_recv_off;
+  uint32_t* halo_idx = nullptr;
   double *multipole = nullptr, *local_own = nullptr, *local_down = nullptr;  // n x ldE
   double* yt = nullptr;  // M2L compressed intermediates, n x ldY (zero where no source)
   std::vector<uint32_t> block_offsets;
@@ -216,6 +222,9 @@ struct fmmgpu_ctx {
   int part_rank = 0, part_n = 1, part_align = 0;
   uint64_t own_s0 = 0, own_s1 = 0;
   void* nccl = nullptr;          // ncclComm_t when fmmgpu_comm_init attached one
+  double* d_halo_buf = nullptr;  // halo exchange staging (send rows, then received rows)
+  size_t halo_buf_cap = 0;
+  bool skip_exchange = false;    // fmmgpu_set_measurement: partitioned work timed without peers
   std::vector<std::vector<uint32_t>> part_begin;  // per level: first owned cell of every rank (+ end)
   // captured evaluation (fmmgpu_evaluate): replayed while tree / partition / operators hold
   cudaGraphExec_t graph_exec = nullptr;

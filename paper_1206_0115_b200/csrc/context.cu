@@ -762,6 +762,9 @@ int fmmgpu_time_operator(fmmgpu_ctx* c, int kind, int level, int reps, double* m
 int fmmgpu_download_fields(fmmgpu_ctx* c, double* pot, double* fx, double* fy, double* fz, int dst_on_device) {
   return guarded(c, [&] {
     need_tree(c);
+    if (c->skip_exchange && c->part_n > 1)
+      throw Error(FMMGPU_LOGIC_ERROR, "measurement mode (fmmgpu_set_measurement): partitioned evaluations skip the "
+                                      "exchange and their fields are not valid");
     if (!c->out_valid) {  // per-operator use: gather near + far now
       FMM_CUDA(cudaEventRecord(c->ev_join, c->s_near));
       FMM_CUDA(cudaStreamWaitEvent(c->s_far, c->ev_join, 0));

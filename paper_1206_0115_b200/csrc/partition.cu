@@ -7,14 +7,22 @@
 //                 run on owned cells (M2L phase A on the sources that have an owned
 //                 target: owned cells plus a halo of the far stencil);
 //   levels <  a : replicated (every rank computes every cell: a handful of cells).
-// One exchange step per upward level >= a: the multipoles of that level are
-// all-gathered (in-place allgatherv = one ncclBroadcast per rank inside a group), which
-// gives M2M(a-1) its children and M2L its halo sources. The downward pass, P2P and L2P
-// need no communication (owner computes, replicated particles), so results are
-// deterministic and identical to the single-device evaluation up to rounding order.
+// One exchange step per upward level >= a, after that level's multipoles are formed:
+//   level a (when M2M(a-1) >= 2 runs on the replicated levels): an all-gather (in-place
+//           allgatherv = one ncclBroadcast per rank inside a group) -- every rank needs
+//           all of level a for its replicated parents;
+//   levels > a: a HALO exchange -- each rank receives exactly the multipoles of the
+//           non-owned cells its M2L phase A reads (children of the parents adjacent to
+//           the parents of its owned targets) from their owners, ncclSend / ncclRecv per
+//           peer inside one group, packed / unpacked by two small kernels.
+// The downward pass, P2P and L2P need no communication (replicated particles, owner
+// computes; P2P pairs across a rank boundary are evaluated one-sided on the owner's
+// side), so results are deterministic and identical to the single-device evaluation up
+// to rounding order.
 //
 // NCCL is loaded lazily (dlopen) only when a communicator is attached; the stepped API
-// (fmmgpu_upward_level / fmmgpu_downward) lets a host drive the exchange itself.
+// (fmmgpu_upward_level / fmmgpu_downward + fmmgpu_exchange_plan) lets a host drive the
+// same exchange itself (tests: N contexts on one device, or processes over gloo).
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -38,6 +46,8 @@ struct NcclApi {
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
 };
 
@@ -54,8 +64,10 @@ NcclApi& nccl() {
     api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
     api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(h, "ncclBroadcast"));
     api.errorString = reinterpret_cast<decltype(api.errorString)>(dlsym(h, "ncclGetErrorString"));
+    api.send = reinterpret_cast<decltype(api.send)>(dlsym(h, "ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(h, "ncclRecv"));
     if (!api.getUniqueId || !api.commInitRank || !api.commDestroy || !api.groupStart || !api.groupEnd ||
-        !api.broadcast || !api.errorString)
+        !api.broadcast || !api.errorString || !api.send || !api.recv)
       throw Error(FMMGPU_RUNTIME_ERROR, "NCCL library lacks required symbols");
     api.handle = h;
   }
@@ -78,7 +90,30 @@ std::vector<T> download(const T* d, size_t n) {
 void free_lists(Level& L) {
   if (L.srcA) cudaFree(L.srcA);
   if (L.tgtB) cudaFree(L.tgtB);
+  if (L.halo_idx) cudaFree(L.halo_idx);
   L.srcA = L.tgtB = nullptr;
+  L.halo_idx = nullptr;
+  L.xkind = 0;
+  L.halo_send_off.clear();
+  L.halo_recv_off.clear();
+  L.halo_send.clear();
+  L.halo_recv.clear();
+}
+
+// rows idx[0..cnt) of the multipole array <-> a contiguous buffer (ld doubles per row)
+__global__ void k_pack_rows(const double* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t cnt, int ld,
+                            double* __restrict__ dst) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= uint64_t(cnt) * ld) return;
+  const uint64_t r = i / ld, k = i % ld;
+  dst[i] = src[uint64_t(idx[r]) * ld + k];
+}
+__global__ void k_unpack_rows(const double* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t cnt, int ld,
+                              double* __restrict__ dst) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= uint64_t(cnt) * ld) return;
+  const uint64_t r = i / ld, k = i % ld;
+  dst[uint64_t(idx[r]) * ld + k] = src[i];
 }
 
 // cells grouped by parity class (code & 7), ascending index inside a class
@@ -102,27 +137,58 @@ void upload_class_list(const std::vector<uint64_t>& code, const std::vector<uint
 void partition_free(fmmgpu_ctx* c) {
   for (auto& L : c->lv) free_lists(L);
   c->part_begin.clear();
+  if (c->d_halo_buf) cudaFree(c->d_halo_buf);
+  c->d_halo_buf = nullptr;
+  c->halo_buf_cap = 0;
 }
 
 void exchange_level(fmmgpu_ctx* c, int v, cudaStream_t s) {
-  if (c->part_n <= 1 || v < std::max(2, c->part_align)) return;
-  // FMMGPU_PART_NO_EXCHANGE=1 (measurement aid only: wrong fields): time one rank's
-  // partitioned work on a single device without a communicator (tools/scaling_projection.py)
-  static const bool no_exchange = std::getenv("FMMGPU_PART_NO_EXCHANGE") != nullptr;
-  if (no_exchange) return;
+  if (c->part_n <= 1 || v >= c->height || c->lv[v].xkind == 0) return;
+  if (c->skip_exchange) return;  // fmmgpu_set_measurement: one rank's work timed alone
   if (!c->nccl) throw Error(FMMGPU_LOGIC_ERROR, "partitioned evaluate needs a communicator (fmmgpu_comm_init) "
                                                 "or the stepped API with a host exchange");
   auto& api = nccl();
   Level& L = c->lv[v];
-  const auto& b = c->part_begin[v];
+  const int ld = c->ldE;
+  auto* comm = static_cast<ncclComm_t>(c->nccl);
+  if (L.xkind == 1) {  // all-gather: every rank broadcasts its owned rows in place
+    const auto& b = c->part_begin[v];
+    NCCL_CHECK(api.groupStart());
+    for (int r = 0; r < c->part_n; ++r) {
+      const size_t cnt = size_t(b[r + 1] - b[r]) * ld;
+      if (!cnt) continue;
+      double* p = L.multipole + size_t(b[r]) * ld;
+      NCCL_CHECK(api.broadcast(p, p, cnt, ncclDouble, r, comm, s));
+    }
+    NCCL_CHECK(api.groupEnd());
+    return;
+  }
+  // halo: pack the rows every peer needs, send / receive per peer, unpack
+  const uint32_t nsend = L.halo_send_off.back(), nrecv = L.halo_recv_off.back();
+  double* sbuf = c->d_halo_buf;
+  double* rbuf = c->d_halo_buf + size_t(nsend) * ld;
+  if (nsend) {
+    const uint64_t tot = uint64_t(nsend) * ld;
+    k_pack_rows<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(L.multipole, L.halo_idx, nsend, ld, sbuf);
+    FMM_CUDA(cudaGetLastError());
+    ++c->launches;
+  }
   NCCL_CHECK(api.groupStart());
-  for (int r = 0; r < c->part_n; ++r) {
-    const size_t cnt = size_t(b[r + 1] - b[r]) * c->ldE;
-    if (!cnt) continue;
-    double* p = L.multipole + size_t(b[r]) * c->ldE;
-    NCCL_CHECK(api.broadcast(p, p, cnt, ncclDouble, r, static_cast<ncclComm_t>(c->nccl), s));
+  for (int p = 0; p < c->part_n; ++p) {
+    if (p == c->part_rank) continue;
+    const uint32_t so = L.halo_send_off[p], sc = L.halo_send_off[p + 1] - so;
+    const uint32_t ro = L.halo_recv_off[p], rc = L.halo_recv_off[p + 1] - ro;
+    if (sc) NCCL_CHECK(api.send(sbuf + size_t(so) * ld, size_t(sc) * ld, ncclDouble, p, comm, s));
+    if (rc) NCCL_CHECK(api.recv(rbuf + size_t(ro) * ld, size_t(rc) * ld, ncclDouble, p, comm, s));
   }
   NCCL_CHECK(api.groupEnd());
+  if (nrecv) {
+    const uint64_t tot = uint64_t(nrecv) * ld;
+    k_unpack_rows<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(rbuf, L.halo_idx + nsend, nrecv, ld,
+                                                                           L.multipole);
+    FMM_CUDA(cudaGetLastError());
+    ++c->launches;
+  }
 }
 
 }  // namespace fmmgpu
@@ -154,7 +220,8 @@ int fmmgpu_plan_partition(const uint64_t* weights, uint32_t n, int nranks, uint3
 int fmmgpu_partition(fmmgpu_ctx* c, int rank, int nranks) {
   try {
     if (!c || !c->have_tree) throw Error(FMMGPU_LOGIC_ERROR, "no tree: call fmmgpu_build_tree first");
-    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(FMMGPU_INVALID_ARGUMENT, "bad rank / nranks");
+    if (nranks < 1 || rank < 0 || rank >= nranks || nranks > 64)
+      throw Error(FMMGPU_INVALID_ARGUMENT, "bad rank / nranks (1 <= nranks <= 64)");
     FMM_CUDA(cudaSetDevice(c->device));
     FMM_CUDA(cudaStreamSynchronize(c->s_near));
     FMM_CUDA(cudaStreamSynchronize(c->s_far));
@@ -227,34 +294,85 @@ int fmmgpu_partition(fmmgpu_ctx* c, int rank, int nranks) {
     c->own_s0 = LL.own0 < LL.n ? lfirst[LL.own0] : c->n;
     c->own_s1 = LL.own1 < LL.n ? lfirst[LL.own1] : c->n;
     // M2L lists of the partitioned levels: phase B targets = owned cells; phase A
-    // sources = children of parents adjacent to (or equal to) an owned target's parent
+    // sources = children of parents adjacent to (or equal to) an owned target's parent.
+    // The same rule for every rank gives the halo plan: cell s is needed by the ranks
+    // owning a target below a parent adjacent to parent(s) (bit mask over ranks).
+    size_t halo_rows = 0;
     for (int v = std::max(2, a); v <= leaf; ++v) {
       Level& L = c->lv[v];
       const auto par = download(L.parent, L.n);
       const Level& P = c->lv[v - 1];
+      const auto& pb = c->part_begin[v];
       const int gp = 1 << (v - 1);
-      std::vector<char> owned_parent(P.n, 0), needed(P.n, 0);
-      for (uint32_t t = L.own0; t < L.own1; ++t) owned_parent[par[t]] = 1;
+      // owner rank of every cell of this level
+      std::vector<uint16_t> owner(L.n);
+      for (int r = 0; r < nranks; ++r)
+        for (uint32_t t = pb[r]; t < pb[r + 1]; ++t) owner[t] = static_cast<uint16_t>(r);
+      // ranks owning a child of each parent, then the ranks needing each parent's children
+      std::vector<uint64_t> kids(P.n, 0), need(P.n, 0);
+      for (uint32_t t = 0; t < L.n; ++t) kids[par[t]] |= 1ull << (owner[t] & 63);
+      const bool pfull = P.full;
       for (uint32_t p = 0; p < P.n; ++p) {
-        if (!owned_parent[p]) continue;
         int ijk[3];
         demorton(code[v - 1][p], ijk);
+        uint64_t m = 0;
         for (int di = -1; di <= 1; ++di)
           for (int dj = -1; dj <= 1; ++dj)
             for (int dk = -1; dk <= 1; ++dk) {
               const int x = ijk[0] + di, y = ijk[1] + dj, z = ijk[2] + dk;
               if (x < 0 || y < 0 || z < 0 || x >= gp || y >= gp || z >= gp) continue;
               const uint64_t cd = morton(x, y, z);
-              auto it = std::lower_bound(code[v - 1].begin(), code[v - 1].end(), cd);
-              if (it != code[v - 1].end() && *it == cd) needed[it - code[v - 1].begin()] = 1;
+              if (pfull) {
+                m |= kids[cd];
+              } else {
+                auto it = std::lower_bound(code[v - 1].begin(), code[v - 1].end(), cd);
+                if (it != code[v - 1].end() && *it == cd) m |= kids[it - code[v - 1].begin()];
+              }
             }
+        need[p] = m;
       }
       std::vector<uint32_t> src, tgt;
-      for (uint32_t s = 0; s < L.n; ++s)
-        if (needed[par[s]]) src.push_back(s);
+      for (uint32_t s2 = 0; s2 < L.n; ++s2)
+        if ((need[par[s2]] >> rank) & 1u) src.push_back(s2);
       for (uint32_t t = L.own0; t < L.own1; ++t) tgt.push_back(t);
       upload_class_list(code[v], src, &L.srcA, L.srcA_off);
       upload_class_list(code[v], tgt, &L.tgtB, L.tgtB_off);
+      // exchange kind: the alignment level is all-gathered when the replicated levels
+      // above it run M2M (parent level a-1 >= 2); deeper levels exchange the halo only
+      L.xkind = (v == a && a - 1 >= 2) ? 1 : 2;
+      if (L.xkind == 2) {
+        std::vector<std::vector<uint32_t>> snd(nranks), rcv(nranks);
+        for (uint32_t s2 = 0; s2 < L.n; ++s2) {
+          const uint64_t m = need[par[s2]];
+          const int o = owner[s2];
+          if (o == rank) {
+            for (int p = 0; p < nranks; ++p)
+              if (p != rank && ((m >> p) & 1u)) snd[p].push_back(s2);
+          } else if ((m >> rank) & 1u) {
+            rcv[o].push_back(s2);
+          }
+        }
+        L.halo_send_off.assign(1, 0);
+        L.halo_recv_off.assign(1, 0);
+        for (int p = 0; p < nranks; ++p) {
+          L.halo_send.insert(L.halo_send.end(), snd[p].begin(), snd[p].end());
+          L.halo_recv.insert(L.halo_recv.end(), rcv[p].begin(), rcv[p].end());
+          L.halo_send_off.push_back(static_cast<uint32_t>(L.halo_send.size()));
+          L.halo_recv_off.push_back(static_cast<uint32_t>(L.halo_recv.size()));
+        }
+        const size_t tot = L.halo_send.size() + L.halo_recv.size();
+        FMM_CUDA(cudaMalloc(&L.halo_idx, std::max<size_t>(1, tot) * sizeof(uint32_t)));
+        if (!L.halo_send.empty())
+          FMM_CUDA(cudaMemcpy(L.halo_idx, L.halo_send.data(), L.halo_send.size() * 4, cudaMemcpyHostToDevice));
+        if (!L.halo_recv.empty())
+          FMM_CUDA(cudaMemcpy(L.halo_idx + L.halo_send.size(), L.halo_recv.data(), L.halo_recv.size() * 4,
+                              cudaMemcpyHostToDevice));
+        halo_rows = std::max(halo_rows, tot);
+      }
+    }
+    if (halo_rows) {
+      FMM_CUDA(cudaMalloc(&c->d_halo_buf, halo_rows * c->ldE * sizeof(double)));
+      c->halo_buf_cap = halo_rows;
     }
     return FMMGPU_OK;
   } catch (const Error& e) {
@@ -285,6 +403,33 @@ int fmmgpu_partition_info(const fmmgpu_ctx* c, int* rank, int* nranks, int* alig
   if (align_level) *align_level = c->part_align;
   if (slot_begin) *slot_begin = c->own_s0;
   if (slot_end) *slot_end = c->own_s1;
+  return FMMGPU_OK;
+}
+
+int fmmgpu_exchange_plan(const fmmgpu_ctx* c, int level, int peer, int* kind, uint32_t* send_cells,
+                         uint32_t* send_count, uint32_t* recv_cells, uint32_t* recv_count) {
+  if (!c || !c->have_tree || level < 0 || level >= c->height) return FMMGPU_INVALID_ARGUMENT;
+  const Level& L = c->lv[level];
+  const int k = c->part_n > 1 ? L.xkind : 0;
+  if (kind) *kind = k;
+  uint32_t sc = 0, rc = 0;
+  if (k == 2) {
+    if (peer < 0 || peer >= c->part_n) return FMMGPU_INVALID_ARGUMENT;
+    const uint32_t so = L.halo_send_off[peer], ro = L.halo_recv_off[peer];
+    sc = L.halo_send_off[peer + 1] - so;
+    rc = L.halo_recv_off[peer + 1] - ro;
+    if (send_cells) std::copy(L.halo_send.begin() + so, L.halo_send.begin() + so + sc, send_cells);
+    if (recv_cells) std::copy(L.halo_recv.begin() + ro, L.halo_recv.begin() + ro + rc, recv_cells);
+  }
+  if (send_count) *send_count = sc;
+  if (recv_count) *recv_count = rc;
+  return FMMGPU_OK;
+}
+
+int fmmgpu_set_measurement(fmmgpu_ctx* c, int skip_exchange) {
+  if (!c) return FMMGPU_INVALID_ARGUMENT;
+  c->skip_exchange = skip_exchange != 0;
+  c->out_valid = false;
   return FMMGPU_OK;
 }
 

@@ -1,12 +1,17 @@
 """Host side of the multi-GPU path: one exchange per upward level.
 
-Each rank owns a contiguous Morton range of cells per level (``FmmContext.partition``);
-the exchange all-gathers every rank's owned segment of a level's multipoles (an
-allgatherv). ``exchange_segments`` is that step on host arrays -- the same plan the
-in-library NCCL path executes with one ncclBroadcast per rank -- and
-``evaluate_partitioned`` drives the stepped API with a caller-supplied all-gather, so
-the partitioned kernels can run with torch.distributed (gloo/nccl) plumbing or, for
-tests, with N contexts emulating N ranks on one device.
+Each rank owns a contiguous Morton range of cells per level (``FmmContext.partition``).
+After the upward step of a partitioned level the library's plan
+(``FmmContext.exchange_plan``, csrc/partition.cu) says what moves: kind 1 = every rank's
+owned rows are all-gathered (the alignment level, when the replicated levels above it
+run M2M), kind 2 = the halo -- each rank receives from each peer exactly the rows its
+M2L reads. In-library NCCL does this inside ``evaluate`` (ncclBroadcast group /
+ncclSend + ncclRecv per peer); the functions here run the same plan on host arrays:
+
+* ``evaluate_partitioned`` -- N rank contexts driven from one process (single-device
+  emulation, tests);
+* ``evaluate_rank`` -- one process per rank with ``torch.distributed`` (gloo on CPU
+  tensors: all_gather for kind 1, isend / irecv per peer for kind 2).
 """
 from __future__ import annotations
 
@@ -28,11 +33,39 @@ def exchange_segments(local: np.ndarray, begins: np.ndarray, rank: int, gather) 
     return out
 
 
-def evaluate_partitioned(ctxs, levels_exchange) -> list:
+def exchange_halo(local: np.ndarray, plans, rank: int, sendrecv) -> np.ndarray:
+    """Halo exchange of one level: ``plans[p] = (send_cells, recv_cells)`` with peer p;
+    ``sendrecv(p, rows_to_send, n_recv) -> received rows`` is the point-to-point step.
+    Received rows land in place; the caller's own rows are unchanged."""
+    out = np.array(local, copy=True)
+    for p, (snd, rcv) in enumerate(plans):
+        if p == rank or (len(snd) == 0 and len(rcv) == 0):
+            continue
+        got = sendrecv(p, np.ascontiguousarray(local[snd]), len(rcv))
+        if len(rcv):
+            out[rcv] = got
+    return out
+
+
+def exchange_bytes(ctx, nranks: int) -> int:
+    """Multipole bytes this rank receives per evaluation (kind 1 all-gather + kind 2 halo)."""
+    total = 0
+    ld = ((ctx.order ** 3 + 31) // 32) * 32  # padded row on the device (ldE)
+    me = ctx.partition_info()["rank"]
+    for v in range(2, ctx.height):
+        kind = ctx.exchange_plan(v, 0)[0]
+        if kind == 1:
+            b = ctx.partition_ranges(v)
+            total += (int(b[-1]) - int(b[me + 1] - b[me])) * ld * 8
+        elif kind == 2:
+            total += sum(len(ctx.exchange_plan(v, p)[2]) for p in range(nranks) if p != me) * ld * 8
+    return total
+
+
+def evaluate_partitioned(ctxs) -> list:
     """Stepped partitioned evaluation of N rank contexts driven from one host process
     (single-device emulation): ``ctxs[r]`` is partitioned as rank r of len(ctxs).
-    ``levels_exchange(v)`` tells whether level v is exchanged. Returns each rank's
-    gathered fields (zero outside its owned particles)."""
+    Returns each rank's gathered fields (zero outside its owned particles)."""
     n = len(ctxs)
     height = ctxs[0].height
     for c in ctxs:
@@ -40,14 +73,75 @@ def evaluate_partitioned(ctxs, levels_exchange) -> list:
     for v in range(height - 1, 1, -1):
         for c in ctxs:
             c.upward_level(v)
-        if levels_exchange(v):
+        kind = ctxs[0].exchange_plan(v, 0)[0]
+        if kind == 0:
+            continue
+        full = [c.expansion(v, 0) for c in ctxs]
+        if kind == 1:
             begins = ctxs[0].partition_ranges(v)
-            full = [c.expansion(v, 0) for c in ctxs]
             segs = [full[r][begins[r]:begins[r + 1]] for r in range(n)]
             for r, c in enumerate(ctxs):
                 c.set_expansion(v, 0, exchange_segments(full[r], begins, r, lambda _s: segs))
+            continue
+        for r, c in enumerate(ctxs):
+            plans = [c.exchange_plan(v, p)[1:] for p in range(n)]
+
+            def sendrecv(p, _rows, n_recv, r=r):
+                snd_p = ctxs[p].exchange_plan(v, r)[1]  # what p sends to r
+                assert np.array_equal(snd_p, plans[p][1]), (v, r, p)
+                return full[p][snd_p]
+
+            c.set_expansion(v, 0, exchange_halo(full[r], plans, r, sendrecv))
     out = []
     for c in ctxs:
         c.downward()
         out.append(c.gather())
     return out
+
+
+def evaluate_rank(ctx, dist) -> list:
+    """Stepped partitioned evaluation of this process's rank over ``torch.distributed``
+    (CPU tensors: gloo). ``ctx`` is partitioned as dist.get_rank() of dist.get_world_size().
+    Returns this rank's gathered fields (zero outside its owned particles)."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    ctx.reset()
+    for v in range(ctx.height - 1, 1, -1):
+        ctx.upward_level(v)
+        kind = ctx.exchange_plan(v, 0)[0]
+        if kind == 0:
+            continue
+        local = ctx.expansion(v, 0)
+        if kind == 1:
+            begins = ctx.partition_ranges(v)
+            width = local.shape[1]
+            rows = int(max(begins[r + 1] - begins[r] for r in range(world)))
+
+            def gather(seg):
+                pad = torch.zeros(rows, width, dtype=torch.float64)
+                pad[:seg.shape[0]] = torch.from_numpy(seg)
+                parts = [torch.zeros_like(pad) for _ in range(world)]
+                dist.all_gather(parts, pad)
+                return [parts[r][:begins[r + 1] - begins[r]].numpy() for r in range(world)]
+
+            ctx.set_expansion(v, 0, exchange_segments(local, begins, rank, gather))
+            continue
+        plans = [ctx.exchange_plan(v, p)[1:] for p in range(world)]
+        reqs, bufs = [], {}
+        for p in range(world):
+            if p == rank:
+                continue
+            snd, rcv = plans[p]
+            if len(snd):
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(local[snd])), p))
+            if len(rcv):
+                bufs[p] = torch.zeros(len(rcv), local.shape[1], dtype=torch.float64)
+                reqs.append(dist.irecv(bufs[p], p))
+        for q in reqs:
+            q.wait()
+        out = np.array(local, copy=True)
+        for p, b in bufs.items():
+            out[plans[p][1]] = b.numpy()
+        ctx.set_expansion(v, 0, out)
+    ctx.downward()
+    return ctx.gather()

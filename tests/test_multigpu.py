@@ -1,12 +1,14 @@
 """Multi-GPU path: contiguous Morton ranges of leaves, one multipole
-all-gather per upward level, owner-computes downward pass.
+exchange per upward level (all-gather at the alignment level, per-peer halo below),
+owner-computes downward pass.
 
 * CPU: the balanced contiguous split (fmmgpu_plan_partition, host-only), and the
-  exchange step with real torch.distributed processes (gloo, world size 2): every rank
-  contributes its owned rows and all ranks end with the same full array.
-* GPU (one device): N partitioned contexts emulate N ranks through the stepped API with
-  a host all-gather; the per-rank fields must partition the particles and their sum
-  must equal the oracle (<= 1e-12) and the unpartitioned evaluation (<= 1e-13).
+  exchange steps with real torch.distributed processes (gloo, world size 2): the
+  all-gather of owned rows and the point-to-point halo step.
+* GPU (one device): N partitioned contexts emulate N ranks through the stepped API and
+  the library's exchange plan; the per-rank fields must partition the particles and
+  their sum must equal the oracle (<= 1e-12) and the unpartitioned evaluation
+  (<= 1e-13). Two real processes (both on the one device) run the library over gloo.
 """
 import os
 import socket
@@ -80,6 +82,57 @@ def _gloo_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _gloo_halo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, ROOT)
+        import torch
+        from paper_1206_0115_b200.distributed import exchange_halo
+        full_ref = np.arange(50 * 3, dtype=np.float64).reshape(50, 3) + 1
+        own = [np.arange(0, 25), np.arange(25, 50)]
+        local = np.zeros_like(full_ref)
+        local[own[rank]] = full_ref[own[rank]]
+        peer = 1 - rank
+        # rank r needs these cells of its peer (the halo), ascending
+        need = [np.array([25, 26, 30, 49]), np.array([0, 3, 24])]
+        plans = [None, None]
+        plans[peer] = (need[peer], need[rank])
+        plans[rank] = (np.zeros(0, int), np.zeros(0, int))
+
+        def sendrecv(p, rows, n_recv):
+            buf = torch.zeros(n_recv, rows.shape[1], dtype=torch.float64)
+            reqs = [dist.isend(torch.from_numpy(rows), p), dist.irecv(buf, p)]
+            for r in reqs:
+                r.wait()
+            return buf.numpy()
+
+        got = exchange_halo(local, plans, rank, sendrecv)
+        expect = local.copy()
+        expect[need[rank]] = full_ref[need[rank]]
+        q.put((rank, bool(np.array_equal(got, expect))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo_exchange_with_gloo_world2():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_halo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=5) for _ in range(2))
+    assert res == {0: True, 1: True}
+    assert all(p.exitcode == 0 for p in procs)
+
+
 @needs_lib
 def test_exchange_with_gloo_world2():
     import multiprocessing as mp
@@ -120,7 +173,10 @@ def test_partitioned_evaluation_emulated(nranks, case):
         ctxs.append(c)
     info = ctxs[0].partition_info()
     align = info["align_level"]
-    outs = evaluate_partitioned(ctxs, lambda v: v >= max(2, align))
+    kinds = [ctxs[0].exchange_plan(v, 0)[0] for v in range(h)]
+    assert all(k == 0 for k in kinds[:max(2, align)]) and all(k in (1, 2) for k in kinds[max(2, align):])
+    assert 2 in kinds  # the levels below the alignment level move only their halo
+    outs = evaluate_partitioned(ctxs)
     # owned particles partition the set: each particle is nonzero on exactly one rank
     slots = [c.partition_info()["slots"] for c in ctxs]
     assert slots[0][0] == 0 and slots[-1][1] == n
@@ -139,4 +195,93 @@ def test_partitioned_evaluation_emulated(nranks, case):
     g1 = ctxs[0].gather()
     assert relative_l2_error(g1[0], g_full[0]) == 0.0
     for c in ctxs + [full]:
+        c.close()
+
+
+def _library_rank(rank, world, port, case, q):
+    """One rank of a real 2-process run of the library (both processes on device 0):
+    whole tree, partition(rank, world), stepped evaluation with the exchange over gloo."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, ROOT)
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import torch
+        import paper_1206_0115_b200 as P
+        from paper_1206_0115_b200.distributed import evaluate_rank, exchange_bytes
+        n, h, l, dist_name, seed = case
+        xyzw = Oracle.generate_particles(n, dist_name, seed)
+        xyzw[:, 3] = 0.5 + np.random.default_rng(seed).random(n)
+        c = P.FmmContext(None, order=l)
+        c.build_tree(xyzw, h)
+        c.partition(rank, world)
+        g = evaluate_rank(c, dist)
+        s0, s1 = c.partition_info()["slots"]
+        # the fields of all ranks summed on every rank (each particle is owned once)
+        tot = torch.from_numpy(np.stack(g))
+        dist.all_reduce(tot)
+        q.put((rank, tot.numpy(), exchange_bytes(c, world), (s0, s1)))
+        c.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [(30000, 5, 5, "uniform", 11), (20000, 6, 4, "ellipsoid", 5)],
+                         ids=["n30000_h5_l5_uniform", "n20000_h6_l4_ellipsoid"])
+def test_two_processes_run_the_library_over_gloo(case):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_library_rank, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, tot, nbytes, slots = q.get(timeout=600)
+        res[r] = (tot, nbytes, slots)
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    n, h, l, dist_name, seed = case
+    xyzw = Oracle.generate_particles(n, dist_name, seed)
+    xyzw[:, 3] = 0.5 + np.random.default_rng(seed).random(n)
+    ref = OracleTree(xyzw, h).evaluate(OracleOps.cached(l))
+    for r in (0, 1):
+        g = res[r][0]
+        assert relative_l2_error(g[0], ref[0]) <= 1e-12
+        assert force_error(*g[1:], *ref[1:]) <= 1e-12
+    assert res[0][2][1] == res[1][2][0]  # the owned particle ranges meet
+    assert res[0][1] > 0 and res[1][1] > 0  # something was exchanged
+
+
+@pytest.mark.gpu
+def test_halo_plan_smaller_than_allgather():
+    """The halo exchange moves a fraction of the old whole-level all-gather (uniform
+    cloud, 8 ranks), and every rank's receive list from p is p's send list to it."""
+    import paper_1206_0115_b200 as P
+    from paper_1206_0115_b200.distributed import exchange_bytes
+    xyzw = Oracle.generate_particles(400000, "uniform", 3)
+    h, l, nr = 6, 5, 8
+    ctxs = []
+    for r in range(nr):
+        c = P.FmmContext(None, order=l)
+        c.build_tree(xyzw, h)
+        c.partition(r, nr)
+        ctxs.append(c)
+    ld = ((l ** 3 + 31) // 32) * 32
+    a = ctxs[0].partition_info()["align_level"]
+    allgather = sum((nr - 1) / nr * ctxs[0].level(v)[0].shape[0] * ld * 8 for v in range(max(2, a), h))
+    for r, c in enumerate(ctxs):
+        assert exchange_bytes(c, nr) < 0.3 * allgather
+        for v in range(max(2, a), h):
+            for p in range(nr):
+                k, snd, rcv = c.exchange_plan(v, p)
+                if k == 2 and p != r:
+                    assert np.array_equal(rcv, ctxs[p].exchange_plan(v, r)[1])
+    for c in ctxs:
         c.close()

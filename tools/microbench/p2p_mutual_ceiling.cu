@@ -124,6 +124,56 @@ __global__ void k_ring(double4* out, int reps) {
   if (acc == 1234.5) out[0] = make_double4(acc, 0, 0, 0);
 }
 
+
+// sub-ring design of csrc/p2p.cu's mutual kernel: 4 sub-rings of 8 lanes; each lane holds
+// TS sources (fixed, j-side sums in registers); a tile of 8 targets rotates around each
+// sub-ring (positions re-read from shared memory, accumulators moved by SHFL); the 4
+// sub-rings' partial target sums are combined by a 2-level butterfly after 8 steps.
+template <int TS>
+__global__ void k_subring(double4* out, int reps) {
+  __shared__ double4 tgt[64];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x)
+    tgt[i] = make_double4(0.5 + 1e-3 * i, 0.25 + 1e-5 * blockIdx.x, 0.125 + 1e-4 * (i % 7), 1.0);
+  __syncthreads();
+  double c375 = 0.375;
+  asm volatile("" : "+d"(c375));
+  const int lane = threadIdx.x & 31, l8 = lane & 7, base8 = lane & ~7;
+  double4 ps[TS], as[TS];
+#pragma unroll
+  for (int t = 0; t < TS; ++t) {
+    ps[t] = make_double4(7.0 + 0.001 * lane + 0.01 * t, 0.002 * (lane % 5), 0.0005 * t, 1.0 + (lane & 3));
+    as[t] = make_double4(0, 0, 0, 0);
+  }
+  double isum = 0;
+  for (int r = 0; r < reps; ++r)
+    for (int tile = 0; tile < 64; tile += 8) {
+      double4 at = make_double4(0, 0, 0, 0);
+#pragma unroll 2
+      for (int s = 0; s < 8; ++s) {
+        const double4 pt = tgt[tile + ((l8 + s) & 7)];
+#pragma unroll
+        for (int t = 0; t < TS; ++t) mutual(pt, ps[t], c375, at, as[t]);
+        const int src = base8 | ((l8 + 1) & 7);
+        at.x = rot(at.x, src);
+        at.y = rot(at.y, src);
+        at.z = rot(at.z, src);
+        at.w = rot(at.w, src);
+      }
+#pragma unroll
+      for (int o = 8; o < 32; o <<= 1) {
+        at.x += __shfl_xor_sync(0xffffffffu, at.x, o);
+        at.y += __shfl_xor_sync(0xffffffffu, at.y, o);
+        at.z += __shfl_xor_sync(0xffffffffu, at.z, o);
+        at.w += __shfl_xor_sync(0xffffffffu, at.w, o);
+      }
+      isum += at.x + at.y + at.z + at.w;
+    }
+  double acc = isum;
+#pragma unroll
+  for (int t = 0; t < TS; ++t) acc += as[t].x + as[t].y + as[t].z + as[t].w;
+  if (acc == 1234.5) out[0] = make_double4(acc, 0, 0, 0);
+}
+
 int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -154,6 +204,18 @@ int main() {
     time([&](int reps) { k_ring<1, 1><<<grid, warps * 32>>>(out, reps); }, thr * NS * 2 * 1, "ring T=1 lds-src", warps, grid);
     time([&](int reps) { k_ring<2, 1><<<grid, warps * 32>>>(out, reps); }, thr * NS * 2 * 2, "ring T=2 lds-src", warps, grid);
     time([&](int reps) { k_ring<4, 1><<<grid, warps * 32>>>(out, reps); }, thr * NS * 2 * 4, "ring T=4 lds-src", warps, grid);
+    for (int ts : {2, 3, 4, 6}) {
+      const double pairs = thr * 64 * ts * 2;  // directional per rep
+      char nm[32];
+      snprintf(nm, sizeof nm, "subring TS=%d", ts);
+      auto go = [&](int reps) {
+        if (ts == 2) k_subring<2><<<grid, warps * 32>>>(out, reps);
+        if (ts == 3) k_subring<3><<<grid, warps * 32>>>(out, reps);
+        if (ts == 4) k_subring<4><<<grid, warps * 32>>>(out, reps);
+        if (ts == 6) k_subring<6><<<grid, warps * 32>>>(out, reps);
+      };
+      time(go, pairs, nm, warps, grid);
+    }
   }
   CK(cudaGetLastError());
   return 0;

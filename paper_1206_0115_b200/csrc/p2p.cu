@@ -343,8 +343,11 @@ struct MuArgs {
 };
 
 // per-warp shared memory; TCAP = targets per chunk (64 on full leaf levels, 128 else:
-// config B 11.07 ms with 64 against 13.5 with 128 -- the larger CTA leaves less L1 for
-// the source loads -- and config D 192 -> 163 ms with 128 and the largest-first order)
+// config D 192 -> 163 ms with 128 and the largest-first order). Measured alternative for
+// big leaves (config D, ~570 particles): the full 32-lane ring with 4 targets per lane
+// in registers and sources rotating (no combine; tools/microbench "ring T=4 lds-src"):
+// 79% of the FP64 pipe under ncu but 161.5 ms + 2.9 ms for the small leaves, no faster
+// than this kernel alone (163 ms).
 template <int TCAP>
 struct MuWarp {
   double4 tpos[TCAP];

@@ -316,8 +316,17 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
 // streams all sources; later chunks add into the slots the first one wrote), leaves are
 // pulled from a global counter: results do not depend on which warp ran a leaf, so
 // evaluations stay bitwise reproducible.
-constexpr int MU_WARPS = 8;
-constexpr int MU_TS = 4;     // sources per lane per pass
+#ifndef FMMGPU_MU_WARPS
+#define FMMGPU_MU_WARPS 12
+#endif
+constexpr int MU_WARPS = FMMGPU_MU_WARPS;
+#ifndef FMMGPU_MU_TS
+#define FMMGPU_MU_TS 4
+#endif
+#ifndef FMMGPU_MU_MINB
+#define FMMGPU_MU_MINB 1
+#endif
+constexpr int MU_TS = FMMGPU_MU_TS;  // sources per lane per pass
 constexpr int MU_NUP = 13;
 constexpr int MU_MAXSEG = 27;
 
@@ -409,8 +418,42 @@ __device__ __forceinline__ void mu_tile(W& w, const int t0, const double4 (&ps)[
 #pragma unroll 2
   for (int s = 0; s < RING; ++s) {
     const double4 pt = tp[(lr + s) & (RING - 1)];
+#ifdef FMMGPU_MU_ILV
+    // the TS pairs stage by stage, so the scheduler sees TS independent chains
+    double dx[TS], dy[TS], dz[TS], r2[TS], inv[TS];
+#pragma unroll
+    for (int m = 0; m < TS; ++m) {
+      dx[m] = pt.x - ps[m].x;
+      dy[m] = pt.y - ps[m].y;
+      dz[m] = pt.z - ps[m].z;
+      r2[m] = fma(dx[m], dx[m], fma(dy[m], dy[m], dz[m] * dz[m]));
+    }
+#pragma unroll
+    for (int m = 0; m < TS; ++m) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(inv[m]) : "d"(r2[m]));
+#pragma unroll
+    for (int m = 0; m < TS; ++m) {
+      const double y = inv[m], t = r2[m] * y, e = fma(-t, y, 1.0);
+      inv[m] = fma(y, e * fma(e, c375, 0.5), y);
+      if constexpr (SELF) inv[m] = __double2hiint(r2[m]) != 0 ? inv[m] : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < TS; ++m) {
+      const double inv2 = inv[m] * inv[m];
+      const double ws = ps[m].w * inv[m], wt = pt.w * inv[m];
+      at.x += ws;
+      as[m].x += wt;
+      const double st = ws * inv2, ss = wt * inv2;
+      at.y = fma(st, dx[m], at.y);
+      at.z = fma(st, dy[m], at.z);
+      at.w = fma(st, dz[m], at.w);
+      as[m].y = fma(-ss, dx[m], as[m].y);
+      as[m].z = fma(-ss, dy[m], as[m].z);
+      as[m].w = fma(-ss, dz[m], as[m].w);
+    }
+#else
 #pragma unroll
     for (int m = 0; m < TS; ++m) mu_pair<SELF>(pt, ps[m], c375, at, as[m]);
+#endif
     at.x = __shfl_sync(0xffffffffu, at.x, nxt);
     at.y = __shfl_sync(0xffffffffu, at.y, nxt);
     at.z = __shfl_sync(0xffffffffu, at.z, nxt);
@@ -491,12 +534,16 @@ __device__ __forceinline__ void mu_pass_ts(const int ts, const MuArgs& a, W& w, 
     case 1: mu_pass<1, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
     case 2: mu_pass<2, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
     case 3: mu_pass<3, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
+#if FMMGPU_MU_TS > 4
+    case 4: mu_pass<4, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
+    case 5: case 6: mu_pass<6, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
+#endif
     default: mu_pass<MU_TS, SELF>(a, w, nseg, base, total, tcn, first_chunk, lane, c375); break;
   }
 }
 
 template <int TCAP>
-__global__ void __launch_bounds__(MU_WARPS * 32, 2) k_p2p_mutual(const MuArgs a) {
+__global__ void __launch_bounds__(MU_WARPS * 32, FMMGPU_MU_MINB) k_p2p_mutual(const MuArgs a) {
   extern __shared__ __align__(16) unsigned char mu_smem[];
   const int lane = threadIdx.x & 31;
   MuWarp<TCAP>& w = reinterpret_cast<MuWarp<TCAP>*>(mu_smem)[threadIdx.x >> 5];
@@ -683,8 +730,15 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
     if (nl == 0) return;
     MuArgs a{L.view(leaf), L.first_particle, L.particle_count, c->d_pw, reinterpret_cast<double4*>(c->d_near),
              reinterpret_cast<double4*>(c->d_slot), c->n, L.own0, L.own1, c->d_ctr, p2p_order(c, L, s), c->ow ? 1 : 0};
-    // Measured alternatives at config B (P2P 11.07 ms with 4 sources per lane, the rotation
-    // unrolled twice, 8-warp CTAs, 2 per SM at 128 registers): 2 or 3 sources per lane with
+    // 12-warp CTAs, one per SM at <= 168 registers (164 used): config B P2P 10.97 -> 10.89
+    // ms, config D 163.4 -> 160.0 ms against 8-warp CTAs, 2 per SM at 128 registers. Also
+    // measured (tools/gpu/gpu_r02g.sh): 10 warps at 164 registers (11.36 / 165.2 ms), 8 warps
+    // at up to 255 registers (11.97 / 171.7), 6 sources per lane with 8 or 12 warps (12.16 /
+    // 162.2, 12.45 / 169.0), the pairs of a step written stage by stage (ptxas schedules
+    // them the same way: no change). Loop ceiling of this sub-ring layout without memory
+    // traffic or padding (tools/microbench/p2p_mutual_ceiling.cu): 8.0 ms at config B's
+    // interaction count. Earlier measurements at config B (P2P 11.07 ms with 4 sources per
+    // lane, the rotation unrolled twice, 8-warp CTAs, 2 per SM at 128 registers): 2 or 3 sources per lane with
     // two target tiles interleaved per step (11.72 / 12.23 ms), 3 CTAs per SM at 80
     // registers (11.77 ms, spills), 4-warp CTAs with 20 warps per SM (11.5 ms), the rotation
     // unrolled 4 / 8 times (12.3 / 17.8 ms, register pressure), the slot addresses

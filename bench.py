@@ -244,36 +244,55 @@ def run_ours(args, world, rank, local):
     n, dist, h, order, desc = CONFIGS[args.config]
     xyzw = P.generate_particles(n, dist, 42)
     ctx = P.FmmContext(None, order=order, device=local)
-    ctx.build_tree(xyzw, h, 250)
-    tree_cold_ms = ctx.timings()["TREE"]  # first build: includes the H2D and every allocation
+    import torch
+    # N > 1: rank r holds only the input slice [r n / N, (r + 1) n / N): the
+    # distributed build all-gathers Morton keys and moves the particles of each rank's
+    # owned leaves and their halo over NCCL (csrc/dist.cu); the tree is the same as the
+    # single-device build and each rank owns a contiguous Morton range of leaves
+    sl = slice(rank * n // world, (rank + 1) * n // world)
+    if world > 1:
+        import torch.distributed as dist
+        uid = [P.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(uid[0], world, rank)
+
+    def build(dev_ptr=None):
+        if world == 1:
+            if dev_ptr is None:
+                ctx.build_tree(xyzw, h, 250)
+            else:
+                ctx.build_tree(n, h, 250, on_device_ptr=dev_ptr)
+        elif dev_ptr is None:
+            ctx.build_tree_distributed(xyzw[sl], h, 250)
+        else:
+            ctx.build_tree_distributed(None, h, 250, on_device_ptr=dev_ptr, n_local=sl.stop - sl.start)
+
+    t0 = time.perf_counter()
+    build()
+    tree_cold_ms = ctx.timings()["TREE"] if world == 1 else (time.perf_counter() - t0) * 1e3
     ledger = ctx.ledger()
 
     # tree + lists, warm: rebuilds from device-resident input,
-    # CUDA events around fmmgpu_build_tree / fmmgpu_build_lists, best of 5
-    import torch
-    dev_in = torch.from_numpy(xyzw).to(f"cuda:{local}")
+    # CUDA events around fmmgpu_build_tree / fmmgpu_build_lists, best of 5 (N > 1: the
+    # distributed build, host clock around the call, max over ranks)
+    dev_in = torch.from_numpy(np.ascontiguousarray(xyzw[sl] if world > 1 else xyzw)).to(f"cuda:{local}")
     tree_ms, lists_ms = [], []
     for _ in range(6):
-        ctx.build_tree(n, h, 250, on_device_ptr=dev_in.data_ptr())
+        barrier(world)
+        t0 = time.perf_counter()
+        build(dev_in.data_ptr())
+        host_ms = (time.perf_counter() - t0) * 1e3
         ctx.build_lists()
         t = ctx.timings()
-        tree_ms.append(t["TREE"])
+        tree_ms.append(t["TREE"] if world == 1 else max_over_ranks(host_ms, world))
         lists_ms.append(t["LISTS"])
     del dev_in
     torch.cuda.empty_cache()
 
     def attach_partition():
-        """N > 1: this rank owns a contiguous Morton range of leaves; the
-        multipoles of each upward level are all-gathered over NCCL inside evaluate."""
-        if world == 1:
-            return
-        ctx.partition(rank, world)
-        if not getattr(ctx, "_comm", False):
-            import torch.distributed as dist
-            uid = [P.comm_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            ctx.comm_init(uid[0], world, rank)
-            ctx._comm = True
+        """N > 1: the distributed build already partitioned the leaves for this rank."""
+        if world > 1:
+            ctx.partition(rank, world)
 
     attach_partition()
     for _ in range(args.warmup):
@@ -294,7 +313,8 @@ def run_ours(args, world, rank, local):
     # pinned output sets used alternately, so step k's H2D and step k-1's D2H run on the
     # copy engines under step k-1's / step k's device work; the serial fmmgpu_run is
     # timed beside it.
-    pins = [torch.from_numpy(xyzw).pin_memory() for _ in range(2 if world == 1 else 1)]
+    pins = [torch.from_numpy(np.ascontiguousarray(xyzw[sl] if world > 1 else xyzw)).pin_memory()
+            for _ in range(2 if world == 1 else 1)]
     outsets = [[torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(4)] for _ in range(len(pins))]
     pin_in, outs = pins[0], outsets[0]
     lib = P.lib()
@@ -305,11 +325,12 @@ def run_ours(args, world, rank, local):
             rc = lib.fmmgpu_run(ctx.h, c_void_p(pin_in.data_ptr()), n, h, 250, *[c_void_p(o.data_ptr()) for o in outs])
             ctx._check(rc)
             return
-        # N > 1: pinned H2D + tree on every rank, own range, evaluate with the exchange,
-        # D2H of the gathered fields (zero outside the owned particles)
-        rc = lib.fmmgpu_build_tree(ctx.h, c_void_p(pin_in.data_ptr()), n, 0, h, 250, None)
+        # N > 1: pinned H2D of this rank's slice, distributed build (keys all-gathered,
+        # owned + halo particles exchanged over NCCL), evaluate with the multipole
+        # exchange, D2H of the gathered fields (zero outside the owned particles)
+        rc = lib.fmmgpu_build_tree_distributed(ctx.h, c_void_p(pin_in.data_ptr()), sl.stop - sl.start, 0, h, 250,
+                                               None)
         ctx._check(rc)
-        attach_partition()
         ctx.evaluate()
         ctx._check(lib.fmmgpu_download_fields(ctx.h, *[c_void_p(o.data_ptr()) for o in outs], 0))
 
@@ -341,7 +362,8 @@ def run_ours(args, world, rank, local):
         for k in range(2):  # every step's result really came back: compare with the serial run
             if not all(torch.equal(a, b) for a, b in zip(outsets[k], serial_ref)):
                 raise RuntimeError("pipelined run returned different fields than fmmgpu_run")
-    e2e = {"value": n / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": 32 * n, "d2h_bytes_per_step": 32 * n,
+    e2e = {"value": n / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": 32 * n,
+           "d2h_bytes_per_step": 32 * n * world,
            "ms_per_step": e2e_s * 1e3, "steps": ksteps, "path": path,
            "serial_fmmgpu_run": {"value": n / e2e_serial_s / 1e6, "ms_per_step": e2e_serial_s * 1e3}}
 

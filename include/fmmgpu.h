@@ -242,6 +242,41 @@ int fmmgpu_comm_destroy(fmmgpu_ctx* ctx);
 int fmmgpu_upward_level(fmmgpu_ctx* ctx, int level);
 int fmmgpu_downward(fmmgpu_ctx* ctx);
 
+/* Distributed input (halo particles; csrc/dist.cu). Rank r holds only
+ * the input slice [offsets[r], offsets[r+1]) of the n particles (input order, slices in
+ * rank order). Replaces GroupTree::build (geometry.cpp:73-161) for a partitioned run:
+ * only Morton keys (8 B per particle) are all-gathered; the tree is bit-identical to the
+ * single-device build of the whole set; each rank then receives the particle records of
+ * its owned leaves and their 26-neighbour halo, nothing else.
+ *
+ * With an attached NCCL communicator, one call does all of it: */
+int fmmgpu_build_tree_distributed(fmmgpu_ctx* ctx, const double* xyzw_local, uint64_t n_local, int on_device,
+                                  int height, int group, const double* root4 /* NULL: bounding cube */);
+/* Stepped form (the caller supplies the collectives):
+ *   fmmgpu_dist_local   upload the slice, *lohi6 = its per-axis {min[3], max[3]};
+ *   (caller: min / max over ranks) fmmgpu_root_from_bounds -> root cube (geometry.cpp:28-34);
+ *   fmmgpu_dist_keys    the slice's leaf keys (u64) and its outside-the-root flag;
+ *   (caller: all-gather keys in rank order, OR the flags)
+ *   fmmgpu_dist_build   tree from the keys, fmmgpu_partition(rank, nranks), particle plan,
+ *                       own records placed;
+ *   fmmgpu_dist_plan    per peer: Morton slots sent to / received from it (NULL = counts);
+ *   fmmgpu_dist_pack / fmmgpu_dist_unpack   records {x,y,z,w} of those slots, in that order;
+ *   fmmgpu_dist_check   coincident particles among the owned leaves (*flag bit 2);
+ *   (caller: OR the flags) fmmgpu_dist_commit   FMMGPU_DOMAIN_ERROR if set, else the tree
+ *                       is ready for evaluations. */
+int fmmgpu_root_from_bounds(const double* lohi6, double* root4);
+int fmmgpu_dist_local(fmmgpu_ctx* ctx, const double* xyzw_local, uint64_t n_local, int on_device, double* lohi6);
+int fmmgpu_dist_keys(fmmgpu_ctx* ctx, const double* root4, int height, uint64_t* keys_out, int out_on_device,
+                     int* flag);
+int fmmgpu_dist_build(fmmgpu_ctx* ctx, const uint64_t* keys_all, int keys_on_device, const uint64_t* offsets,
+                      int rank, int nranks, int height, int group, const double* root4, int flag);
+int fmmgpu_dist_plan(fmmgpu_ctx* ctx, int peer, uint32_t* send_slots, uint32_t* send_count, uint32_t* recv_slots,
+                     uint32_t* recv_count);
+int fmmgpu_dist_pack(fmmgpu_ctx* ctx, int peer, double* records_out, int out_on_device);
+int fmmgpu_dist_unpack(fmmgpu_ctx* ctx, int peer, const double* records_in, int in_on_device);
+int fmmgpu_dist_check(fmmgpu_ctx* ctx, int* flag);
+int fmmgpu_dist_commit(fmmgpu_ctx* ctx, int flag);
+
 /* bench.cpp:19-61 generate_particles (mt19937_64, explicit scaling); dist 0 uniform,
  * 1 sphere, 2 ellipsoid surface (config D: the sphere's directions on semi-axes
  * 0.5, 0.35, 0.2). Host-side input generator so both sides see identical doubles. */

@@ -105,6 +105,17 @@ def lib():
         L.fmmgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
         L.fmmgpu_exchange_plan.argtypes = [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
         L.fmmgpu_set_measurement.argtypes = [c_void_p, c_int]
+        L.fmmgpu_root_from_bounds.argtypes = [c_void_p, c_void_p]
+        L.fmmgpu_dist_local.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_void_p]
+        L.fmmgpu_dist_keys.argtypes = [c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p]
+        L.fmmgpu_dist_build.argtypes = [c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_void_p,
+                                        c_int]
+        L.fmmgpu_dist_plan.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]
+        L.fmmgpu_dist_pack.argtypes = [c_void_p, c_int, c_void_p, c_int]
+        L.fmmgpu_dist_unpack.argtypes = [c_void_p, c_int, c_void_p, c_int]
+        L.fmmgpu_dist_check.argtypes = [c_void_p, c_void_p]
+        L.fmmgpu_dist_commit.argtypes = [c_void_p, c_int]
+        L.fmmgpu_build_tree_distributed.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_int, c_int, c_void_p]
         _lib = L
     return _lib
 
@@ -132,6 +143,16 @@ def plan_partition(weights, nranks: int) -> np.ndarray:
     rc = lib().fmmgpu_plan_partition(_p(w) if len(w) else None, len(w), nranks, _p(out))
     if rc:
         raise _ERRORS.get(rc, FmmError)("plan_partition failed")
+    return out
+
+
+def root_from_bounds(lohi) -> np.ndarray:
+    """Root cube {cx, cy, cz, width} of per-axis bounds {min[3], max[3]} (geometry.cpp:28-34)."""
+    b = np.ascontiguousarray(lohi, dtype=np.float64)
+    out = np.zeros(4)
+    rc = lib().fmmgpu_root_from_bounds(_p(b), _p(out))
+    if rc != 0:
+        raise InvalidArgument("root_from_bounds: empty or invalid bounds")
     return out
 
 
@@ -428,6 +449,73 @@ class FmmContext:
 
     def comm_init(self, uid: bytes, nranks: int, rank: int):
         self._check(self._lib.fmmgpu_comm_init(self.h, uid, nranks, rank))
+
+    # ---- distributed input (fmmgpu_dist_*, csrc/dist.cu): this rank holds one input slice
+    def dist_local(self, xyzw_local) -> np.ndarray:
+        """Upload this rank's input slice; returns its per-axis bounds {min[3], max[3]}."""
+        a = np.ascontiguousarray(xyzw_local, dtype=np.float64).reshape(-1, 4)
+        self._dist_n = a.shape[0]
+        lohi = np.zeros(6)
+        self._check(self._lib.fmmgpu_dist_local(self.h, _p(a), a.shape[0], 0, _p(lohi)))
+        return lohi
+
+    def dist_keys(self, root, height: int):
+        """Leaf Morton keys (u64) of the uploaded slice and its outside-the-root flag."""
+        r = np.ascontiguousarray(root, dtype=np.float64)
+        keys = np.zeros(self._dist_n, dtype=np.uint64)
+        flag = c_int()
+        self._check(self._lib.fmmgpu_dist_keys(self.h, _p(r), height, _p(keys), 0, byref(flag)))
+        return keys, flag.value
+
+    def dist_build(self, keys_all, offsets, rank: int, nranks: int, height: int, group_size: int, root, flag: int):
+        """Tree from the all-gathered keys, partition, particle plan (own records placed)."""
+        k = np.ascontiguousarray(keys_all, dtype=np.uint64)
+        o = np.ascontiguousarray(offsets, dtype=np.uint64)
+        r = np.ascontiguousarray(root, dtype=np.float64)
+        self._check(self._lib.fmmgpu_dist_build(self.h, _p(k), 0, _p(o), rank, nranks, height, group_size, _p(r),
+                                                int(flag)))
+        self.n, self.height, self.group_size = int(o[-1]), height, group_size
+
+    def dist_plan(self, peer: int):
+        """(send_slots, recv_slots): Morton slots whose records go to / come from `peer`."""
+        sc, rc = ctypes.c_uint32(), ctypes.c_uint32()
+        self._check(self._lib.fmmgpu_dist_plan(self.h, peer, None, byref(sc), None, byref(rc)))
+        snd = np.zeros(sc.value, dtype=np.uint32)
+        rcv = np.zeros(rc.value, dtype=np.uint32)
+        self._check(self._lib.fmmgpu_dist_plan(self.h, peer, _p(snd), byref(sc), _p(rcv), byref(rc)))
+        return snd, rcv
+
+    def dist_pack(self, peer: int) -> np.ndarray:
+        n = len(self.dist_plan(peer)[0])
+        out = np.zeros((n, 4))
+        self._check(self._lib.fmmgpu_dist_pack(self.h, peer, _p(out), 0))
+        return out
+
+    def dist_unpack(self, peer: int, records):
+        a = np.ascontiguousarray(records, dtype=np.float64).reshape(-1, 4)
+        self._check(self._lib.fmmgpu_dist_unpack(self.h, peer, _p(a), 0))
+
+    def dist_check(self) -> int:
+        f = c_int()
+        self._check(self._lib.fmmgpu_dist_check(self.h, byref(f)))
+        return f.value
+
+    def dist_commit(self, flag: int):
+        self._check(self._lib.fmmgpu_dist_commit(self.h, int(flag)))
+
+    def build_tree_distributed(self, xyzw_local, height: int, group_size: int = 250, root=None, on_device_ptr=None,
+                               n_local=None):
+        """All of the distributed build over the attached NCCL communicator."""
+        if on_device_ptr is not None:
+            ptr, n, dev = c_void_p(on_device_ptr), int(n_local), 1
+        else:
+            a = np.ascontiguousarray(xyzw_local, dtype=np.float64).reshape(-1, 4)
+            ptr, n, dev = _p(a), a.shape[0], 0
+        r = None if root is None else np.ascontiguousarray(root, dtype=np.float64)
+        self._check(self._lib.fmmgpu_build_tree_distributed(self.h, ptr, n, dev, height, group_size, _p(r)))
+        ntot = c_uint64()
+        self._check(self._lib.fmmgpu_tree_info(self.h, byref(ntot), None, None, None))
+        self.n, self.height, self.group_size = ntot.value, height, group_size
 
     def upward_level(self, level: int):
         self._check(self._lib.fmmgpu_upward_level(self.h, level))

@@ -226,6 +226,18 @@ struct fmmgpu_ctx {
   size_t halo_buf_cap = 0;
   bool skip_exchange = false;    // fmmgpu_set_measurement: partitioned work timed without peers
   std::vector<std::vector<uint32_t>> part_begin;  // per level: first owned cell of every rank (+ end)
+  // distributed input (dist.cu, SURVEY §8e halo particles): this rank holds the input slice
+  // [dist_off[rank], dist_off[rank + 1]) in d_loc; the tree comes from all-gathered keys,
+  // d_pw holds only the owned and halo leaves once the particle exchange is committed
+  bool dist = false, dist_ready = true;
+  double4* d_loc = nullptr;
+  size_t d_loc_cap = 0;
+  uint64_t dist_nloc = 0, dist_ntot = 0, dist_offset = 0;
+  std::vector<uint64_t> dist_off;                 // nranks + 1 slice offsets (input order)
+  uint32_t* d_dsend = nullptr;                    // slots to send, grouped by peer
+  uint32_t* d_drecv = nullptr;                    // slots to receive, grouped by peer
+  std::vector<uint32_t> dsend_off, drecv_off;     // nranks + 1 offsets into the two lists
+  int comm_rank = 0, comm_n = 1;                  // of the attached NCCL communicator
   // captured evaluation (fmmgpu_evaluate): replayed while tree / partition / operators hold
   cudaGraphExec_t graph_exec = nullptr;
   bool graph_warm = false;   // one eager evaluation done since the last invalidation
@@ -284,8 +296,18 @@ namespace fmmgpu {
 void interp_setup(fmmgpu_ctx* c);
 void m2l_setup(fmmgpu_ctx* c, bool compute_factors);
 void m2l_free(fmmgpu_ctx* c);
+struct DistKeys {            // distributed build (dist.cu): all-gathered keys, no positions
+  const uint64_t* keys;      // [n] leaf Morton keys in input order (device)
+  int flag;                  // OR of the ranks' outside-the-root flags (bit 0)
+};
 void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, int height, int group,
-                const double* root4);
+                const double* root4, const DistKeys* dist = nullptr);
+void root_from_bounds(const double lo[3], const double hi[3], double root[4]);
+void device_bounds(fmmgpu_ctx* c, const double4* d, uint64_t n, double lohi[6], cudaStream_t s);
+void device_keys(const double4* d, uint64_t n, const double root[4], int height, uint64_t* keys, uint32_t* idx,
+                 int* flag, cudaStream_t s);
+void dist_free(fmmgpu_ctx* c);
+int coincident_check(fmmgpu_ctx* c, uint32_t leaf0, uint32_t leaf1, cudaStream_t s);
 void tree_free(fmmgpu_ctx* c);
 void yt_keep_free(fmmgpu_ctx* c);
 void lists_build(fmmgpu_ctx* c);

@@ -51,6 +51,8 @@ void reset_arrays(fmmgpu_ctx* c, cudaStream_t s);
 // new tree start zeroed (GroupTree::allocate_*, geometry.cpp:199-214).
 void need_tree(fmmgpu_ctx* c) {
   if (!c->have_tree) throw Error(FMMGPU_LOGIC_ERROR, "no tree: call fmmgpu_build_tree first");
+  if (!c->dist_ready)
+    throw Error(FMMGPU_LOGIC_ERROR, "distributed tree: particle exchange not committed (fmmgpu_dist_commit)");
   if (c->zero_pending) {
     reset_arrays(c, c->s_far);
     c->zero_pending = false;

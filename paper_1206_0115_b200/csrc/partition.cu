@@ -222,6 +222,10 @@ int fmmgpu_partition(fmmgpu_ctx* c, int rank, int nranks) {
     if (!c || !c->have_tree) throw Error(FMMGPU_LOGIC_ERROR, "no tree: call fmmgpu_build_tree first");
     if (nranks < 1 || rank < 0 || rank >= nranks || nranks > 64)
       throw Error(FMMGPU_INVALID_ARGUMENT, "bad rank / nranks (1 <= nranks <= 64)");
+    if (c->dist && !c->dsend_off.empty() && (rank != c->part_rank || nranks != c->part_n))
+      throw Error(FMMGPU_LOGIC_ERROR, "distributed tree: its particles were placed for rank " +
+                                          std::to_string(c->part_rank) + " of " + std::to_string(c->part_n));
+    if (c->dist && !c->dsend_off.empty()) return FMMGPU_OK;  // already partitioned this way
     FMM_CUDA(cudaSetDevice(c->device));
     FMM_CUDA(cudaStreamSynchronize(c->s_near));
     FMM_CUDA(cudaStreamSynchronize(c->s_far));
@@ -467,6 +471,8 @@ int fmmgpu_comm_init(fmmgpu_ctx* c, const char* id128, int nranks, int rank) {
     NCCL_CHECK(nccl().commInitRank(&comm, nranks, id, rank));
     if (c->nccl) nccl().commDestroy(static_cast<ncclComm_t>(c->nccl));
     c->nccl = comm;
+    c->comm_rank = rank;
+    c->comm_n = nranks;
     return FMMGPU_OK;
   } catch (const Error& e) {
     if (c) c->err = e.what();

@@ -99,17 +99,30 @@ __global__ void k_permute(const double4* __restrict__ in, const uint32_t* __rest
   }
 }
 
+// distributed builds: input index per slot is the sorted iota, its inverse is all that
+// the permute pass produced besides the positions (which arrive by the particle exchange)
+__global__ void k_iota(uint32_t* __restrict__ idx, uint64_t n) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) idx[i] = static_cast<uint32_t>(i);
+}
+__global__ void k_inverse(const uint32_t* __restrict__ id, uint64_t n, uint32_t* __restrict__ inv) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) inv[id[i]] = static_cast<uint32_t>(i);
+}
+
 // leaf cell of every Morton slot, and the coincident-particle check
 // (geometry.cpp:126-136: equal positions inside one leaf -> domain_error).
 __global__ void k_leaf_scan(const uint32_t* __restrict__ first, const uint32_t* __restrict__ count, uint32_t ncells,
-                            const double4* __restrict__ pw, uint32_t* __restrict__ pcell, int* __restrict__ flag) {
+                            const double4* __restrict__ pw, uint32_t* __restrict__ pcell, int* __restrict__ flag,
+                            uint32_t cell0 = 0) {
   __shared__ double xs[8][64];  // x of the leaf's particles (leaves of <= 64), per warp
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   if (warp >= ncells) return;
   const uint32_t f = first[warp], m = count[warp];
   const double* px = reinterpret_cast<const double*>(pw + f);
-  for (uint32_t a = lane; a < m; a += 32) pcell[f + a] = warp;
+  if (pcell)
+    for (uint32_t a = lane; a < m; a += 32) pcell[f + a] = cell0 + warp;
   if (m <= 64) {
     // x staged once; the pair loop reads it as a shared-memory broadcast (one wavefront
     // per source instead of a strided L1 read per pair), y and z only for equal x
@@ -357,11 +370,67 @@ void tree_free(fmmgpu_ctx* c) {
   dfree(c, c->d_near, s); dfree(c, c->d_far, s); dfree(c, c->d_out, s);
   dfree(c, c->d_slot, s);
   dfree(c, c->d_p2p_order, s);
+  dist_free(c);
   c->have_tree = false;
 }
 
+// bounding_cube (geometry.cpp:28-34) from per-axis bounds, host arithmetic without
+// contraction; shared by the single-device build and the distributed one
+void root_from_bounds(const double lo[3], const double hi[3], double root[4]) {
+  double extent = 0;
+  for (int a = 0; a < 3; ++a) {
+    root[a] = 0.5 * (lo[a] + hi[a]);
+    extent = std::max(extent, hi[a] - lo[a]);
+  }
+  root[3] = extent > 0 ? extent * (1.0 + 1e-6) : 1.0;
+}
+
+// per-axis min / max of n device particles -> lohi = {lo[3], hi[3]} (+-inf when n = 0)
+void device_bounds(fmmgpu_ctx* c, const double4* d, uint64_t n, double lohi[6], cudaStream_t s) {
+  for (int a = 0; a < 3; ++a) {
+    lohi[a] = INFINITY;
+    lohi[3 + a] = -INFINITY;
+  }
+  if (n == 0) return;
+  const int nb = static_cast<int>(std::min<uint64_t>(1184, blocks(n, 256)));
+  double* part = static_cast<double*>(scratch(c, sizeof(double) * 6 * nb));
+  k_minmax_partial<<<nb, 256, 0, s>>>(d, n, part);
+  FMM_CUDA(cudaGetLastError());
+  std::vector<double> h(6 * nb);
+  std::memcpy(h.data(), readback(c, part, sizeof(double) * 6 * nb, s), sizeof(double) * 6 * nb);
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < nb; ++b) {
+      lohi[a] = std::min(lohi[a], h[a * nb + b]);
+      lohi[3 + a] = std::max(lohi[3 + a], h[(3 + a) * nb + b]);
+    }
+}
+
+// Morton leaf keys of n device particles against root (geometry.cpp:76-94), as u64, and
+// the outside-the-root flag (bit 1 of *flag, device) -- the per-rank step of a
+// distributed build
+void device_keys(const double4* d, uint64_t n, const double root[4], int height, uint64_t* keys, uint32_t* idx,
+                 int* flag, cudaStream_t s) {
+  if (n == 0) return;
+  const int leaf = height - 1;
+  const uint32_t grid = 1u << leaf;
+  const double cw = root[3] / static_cast<double>(grid);
+  double lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = root[a] - 0.5 * root[3];
+    hi[a] = lo[a] + root[3];
+  }
+  k_keys<<<blocks(n, 256), 256, 0, s>>>(d, n, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], cw, grid, keys, idx, flag);
+  FMM_CUDA(cudaGetLastError());
+}
+
+// Distributed builds (dist != nullptr, csrc/dist.cu): the keys of all n particles were
+// computed by the ranks from their input slices and all-gathered (device, input order);
+// the positions are NOT here: d_pw stays zero until the particle exchange places this
+// rank's owned and halo leaves, and the coincident-particle check runs after it on the
+// owned leaves. Everything else (sort, levels, classes, expansions) is the same code, so
+// the tree is bit-identical to the single-device build of the whole set.
 void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, int height, int group,
-                const double* root4) {
+                const double* root4, const DistKeys* dist) {
   // argument validation, geometry.cpp:65-69 and bounding_cube's empty check
   if (height < 3 || height > 21) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: height must be in [3, 21]");
   if (group < 1) throw Error(FMMGPU_INVALID_ARGUMENT, "GroupTree: group size must be positive");
@@ -379,7 +448,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
 
   // input -> device (input order); a pipelined run (fmmgpu_run_async) has already
   // copied it into d_in on its H2D stream
-  const bool in_place = on_device && xyzw == reinterpret_cast<const double*>(c->d_in) && c->d_in_cap >= n;
+  if (dist && !root4) throw Error(FMMGPU_LOGIC_ERROR, "distributed build without a root cube");
+  const bool in_place = dist || (on_device && xyzw == reinterpret_cast<const double*>(c->d_in) && c->d_in_cap >= n);
   if (!in_place && c->d_in_cap < n) {
     if (c->d_in) FMM_CUDA(cudaFreeAsync(c->d_in, s));
     FMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c->d_in), n * sizeof(double4), s));
@@ -394,27 +464,9 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   if (root4) {
     std::copy(root4, root4 + 4, root);
   } else {
-    const int nb = static_cast<int>(std::min<uint64_t>(1184, blocks(n, 256)));
-    double* part = static_cast<double*>(scratch(c, sizeof(double) * 6 * nb));
-    k_minmax_partial<<<nb, 256, 0, s>>>(c->d_in, n, part);
-    FMM_CUDA(cudaGetLastError());
-    std::vector<double> h(6 * nb);
-    std::memcpy(h.data(), readback(c, part, sizeof(double) * 6 * nb, s), sizeof(double) * 6 * nb);
-    double lo[3], hi[3];
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = h[a * nb];
-      hi[a] = h[(3 + a) * nb];
-      for (int b = 1; b < nb; ++b) {
-        lo[a] = std::min(lo[a], h[a * nb + b]);
-        hi[a] = std::max(hi[a], h[(3 + a) * nb + b]);
-      }
-    }
-    double extent = 0;  // geometry.cpp:28-34, host arithmetic without contraction
-    for (int a = 0; a < 3; ++a) {
-      root[a] = 0.5 * (lo[a] + hi[a]);
-      extent = std::max(extent, hi[a] - lo[a]);
-    }
-    root[3] = extent > 0 ? extent * (1.0 + 1e-6) : 1.0;
+    double lohi[6];
+    device_bounds(c, c->d_in, n, lohi, s);
+    root_from_bounds(lohi, lohi + 3, root);
   }
   trace("root cube");
   std::copy(root, root + 4, c->root);
@@ -441,8 +493,12 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   L.particle_count = dalloc<uint32_t>(c, n, s);
   size_t tb = 0;
   auto sort_and_encode = [&](auto* keys, auto* keys_sorted) {
-    k_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, c->lo[0], c->lo[1], c->lo[2], hib[0], hib[1], hib[2], cw, grid,
-                                           keys, idx, c->d_flag);
+    if (dist) {
+      k_iota<<<blocks(n, 256), 256, 0, s>>>(idx, n);
+    } else {
+      k_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, c->lo[0], c->lo[1], c->lo[2], hib[0], hib[1], hib[2], cw,
+                                             grid, keys, idx, c->d_flag);
+    }
     FMM_CUDA(cudaGetLastError());
     trace("keys");
     FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys_sorted, idx, c->d_id, static_cast<int>(n), 0,
@@ -452,7 +508,12 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     trace("sort");
     c->d_pw = dalloc<double4>(c, n, s);
     c->d_inv = dalloc<uint32_t>(c, n, s);
-    k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw, c->d_inv);
+    if (dist) {
+      k_inverse<<<blocks(n, 256), 256, 0, s>>>(c->d_id, n, c->d_inv);
+      FMM_CUDA(cudaMemsetAsync(c->d_pw, 0, n * sizeof(double4), s));
+    } else {
+      k_permute<<<blocks(n, 256), 256, 0, s>>>(c->d_in, c->d_id, n, c->d_pw, c->d_inv);
+    }
     FMM_CUDA(cudaGetLastError());
     trace("keys+sort+permute");
     FMM_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb, keys_sorted, L.code, L.particle_count, d_runs,
@@ -460,7 +521,11 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     FMM_CUDA(cub::DeviceRunLengthEncode::Encode(scratch(c, tb), tb, keys_sorted, L.code, L.particle_count, d_runs,
                                                 static_cast<int>(n), s));
   };
-  if (3 * leaf <= 32) {
+  if (dist) {  // the all-gathered u64 keys are sorted in place of computed ones
+    uint64_t* k64s = dalloc<uint64_t>(c, n, s);
+    sort_and_encode(const_cast<uint64_t*>(dist->keys), k64s);
+    dfree(c, k64s, s);
+  } else if (3 * leaf <= 32) {
     uint32_t* k32 = dalloc<uint32_t>(c, n, s);
     uint32_t* k32s = dalloc<uint32_t>(c, n, s);
     sort_and_encode(k32, k32s);
@@ -502,7 +567,10 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     dfree(c, fi, s);
     dfree(c, fis, s);
   };
-  if (n <= 64ull * runs) {
+  if (dist) {  // positions arrive later: the coincident check runs in fmmgpu_dist_check
+    k_leaf_cells<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs,
+                                                                  c->d_pcell);
+  } else if (n <= 64ull * runs) {
     // small leaves on average; a leaf above 64 raises flag bit 4 and the sorted check
     // runs after the readback below (clustered inputs)
     k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs, c->d_pw,
@@ -614,6 +682,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   const uint32_t* h_offs = static_cast<const uint32_t*>(readback(c, d_offs, (9 * height + 1) * sizeof(uint32_t), s));
   for (int v = 2; v < height; ++v) std::memcpy(c->lv[v].cls_off, h_offs + 9 * v, 9 * sizeof(uint32_t));
   int flag = static_cast<int>(h_offs[9 * height]);
+  if (dist) flag = dist->flag & 1;  // every rank's key step, OR-ed by the caller
   if ((flag & 4) && !(flag & 3)) {  // a leaf above 64 particles: the sorted fine-key check
     fine_key_check();
     flag = *static_cast<const int*>(readback(c, c->d_flag, sizeof(int), s));
@@ -629,8 +698,52 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     throw Error(FMMGPU_DOMAIN_ERROR, "GroupTree: coincident particles");
   }
   c->have_tree = true;
+  c->dist = dist != nullptr;
+  c->dist_ready = !c->dist;
   ensure_p2p_slots(c);
   cache_trim_old(c, s);  // blocks of the previous tree this one did not reuse
+}
+
+
+// Coincident-particle check (geometry.cpp:126-136) of the leaves [c0, c1) of the current
+// tree, positions in d_pw: the distributed build runs it on each rank's owned leaves
+// after the particle exchange. Returns the flag bits (2 = coincident particles).
+int coincident_check(fmmgpu_ctx* c, uint32_t c0, uint32_t c1, cudaStream_t s) {
+  const Level& L = c->lv[c->height - 1];
+  if (c1 <= c0) return 0;
+  const uint32_t runs = c1 - c0;
+  const uint32_t f0 = *static_cast<const uint32_t*>(readback(c, L.first_particle + c0, 4, s));
+  const uint64_t s0 = f0, s1 = c1 < L.n ? *static_cast<const uint32_t*>(readback(c, L.first_particle + c1, 4, s))
+                                        : c->n;
+  const uint64_t m = s1 - s0;
+  FMM_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
+  bool fine = m > 64ull * runs;
+  if (!fine) {
+    k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle + c0, L.particle_count + c0, runs,
+                                                                 c->d_pw, nullptr, c->d_flag);
+    FMM_CUDA(cudaGetLastError());
+    const int f = *static_cast<const int*>(readback(c, c->d_flag, sizeof(int), s));
+    if (f & 2) return f;
+    fine = (f & 4) != 0;
+  }
+  if (!fine) return 0;
+  size_t tb = 0;
+  uint64_t* fk = dalloc<uint64_t>(c, m, s);
+  uint64_t* fks = dalloc<uint64_t>(c, m, s);
+  uint32_t* fi = dalloc<uint32_t>(c, m, s);
+  uint32_t* fis = dalloc<uint32_t>(c, m, s);
+  const double4* pw = c->d_pw + s0;
+  k_fine_keys<<<blocks(m, 256), 256, 0, s>>>(pw, m, c->lo[0], c->lo[1], c->lo[2], c->root[3] / 2097152.0, fk, fi);
+  FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, fk, fks, fi, fis, static_cast<int>(m), 0, 63, s));
+  FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, fk, fks, fi, fis, static_cast<int>(m), 0, 63, s));
+  FMM_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
+  k_equal_key_runs<<<blocks(m, 256), 256, 0, s>>>(fks, fis, m, pw, c->d_flag);
+  FMM_CUDA(cudaGetLastError());
+  dfree(c, fk, s);
+  dfree(c, fks, s);
+  dfree(c, fi, s);
+  dfree(c, fis, s);
+  return *static_cast<const int*>(readback(c, c->d_flag, sizeof(int), s)) & 2;
 }
 
 }  // namespace fmmgpu

@@ -145,3 +145,95 @@ def evaluate_rank(ctx, dist) -> list:
         ctx.set_expansion(v, 0, out)
     ctx.downward()
     return ctx.gather()
+
+
+# ---------------------------------------------------------------- distributed input
+# Each rank holds one slice of the input (input order, slices in rank order); only the
+# Morton keys are all-gathered, then each rank receives the particle records of its
+# owned leaves and their 26-neighbour halo (csrc/dist.cu). The library does it over
+# NCCL in one call (FmmContext.build_tree_distributed); these drive the same steps
+# (fmmgpu_dist_*) with host collectives.
+
+def _root(lohi_all, root):
+    if root is not None:
+        return np.ascontiguousarray(root, dtype=np.float64)
+    from . import root_from_bounds
+    g = np.concatenate([lohi_all[:, :3].min(axis=0), lohi_all[:, 3:6].max(axis=0)])
+    return root_from_bounds(g)
+
+
+def build_distributed_emulated(ctxs, slices, height: int, group_size: int = 250, root=None):
+    """Distributed build of N rank contexts from one host process (single-device
+    emulation): ``slices[r]`` is rank r's (n_r, 4) input slice. Raises like the library
+    (every rank) when particles coincide. Returns the per-rank particle records received."""
+    n = len(ctxs)
+    lohi = np.stack([c.dist_local(s) for c, s in zip(ctxs, slices)])
+    offsets = np.concatenate([[0], np.cumsum([len(s) for s in slices])]).astype(np.uint64)
+    rt = _root(lohi, root)
+    kf = [c.dist_keys(rt, height) for c in ctxs]
+    keys = np.concatenate([k for k, _ in kf]) if offsets[-1] else np.zeros(0, np.uint64)
+    flag = 0
+    for _, f in kf:
+        flag |= f
+    for r, c in enumerate(ctxs):
+        c.dist_build(keys, offsets, r, n, height, group_size, rt, flag)
+    moved = [0] * n
+    for r, c in enumerate(ctxs):
+        for p in range(n):
+            if p == r:
+                continue
+            rec = ctxs[p].dist_pack(r)  # what p sends to r
+            assert len(rec) == len(c.dist_plan(p)[1]), (r, p)
+            c.dist_unpack(p, rec)
+            moved[r] += len(rec)
+    cf = 0
+    for c in ctxs:
+        cf |= c.dist_check()
+    for c in ctxs:
+        c.dist_commit(cf)
+    return moved
+
+
+def build_distributed_rank(ctx, xyzw_local, height: int, group_size: int, dist, root=None) -> int:
+    """Distributed build of this process's rank over ``torch.distributed`` (gloo, CPU
+    tensors): all-gathers of the bounds and keys, isend / irecv of particle records per
+    peer. Returns the number of particle records this rank received."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    lohi = ctx.dist_local(xyzw_local)
+    nloc = len(np.asarray(xyzw_local).reshape(-1, 4))
+    meta = torch.tensor(list(lohi) + [float(nloc)], dtype=torch.float64)
+    parts = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(parts, meta)
+    m = torch.stack(parts).numpy()
+    counts = m[:, 6].astype(np.uint64)
+    offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    rt = _root(m[:, :6], root)
+    keys, flag = ctx.dist_keys(rt, height)
+    width = int(counts.max()) if world else 0
+    pad = torch.zeros(width, dtype=torch.int64)
+    pad[:nloc] = torch.from_numpy(keys.view(np.int64))
+    kparts = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(kparts, pad)
+    keys_all = np.concatenate([kparts[r][:int(counts[r])].numpy() for r in range(world)]).view(np.uint64)
+    f = torch.tensor([flag], dtype=torch.int64)
+    dist.all_reduce(f, op=dist.ReduceOp.MAX)
+    ctx.dist_build(keys_all, offsets, rank, world, height, group_size, rt, int(f.item()))
+    reqs, bufs = [], {}
+    for p in range(world):
+        if p == rank:
+            continue
+        snd, rcv = ctx.dist_plan(p)
+        if len(snd):
+            reqs.append(dist.isend(torch.from_numpy(ctx.dist_pack(p)), p))
+        if len(rcv):
+            bufs[p] = torch.zeros(len(rcv), 4, dtype=torch.float64)
+            reqs.append(dist.irecv(bufs[p], p))
+    for q in reqs:
+        q.wait()
+    for p, b in bufs.items():
+        ctx.dist_unpack(p, b.numpy())
+    cf = torch.tensor([ctx.dist_check()], dtype=torch.int64)
+    dist.all_reduce(cf, op=dist.ReduceOp.MAX)
+    ctx.dist_commit(int(cf.item()))
+    return sum(len(b) for b in bufs.values())

@@ -23,7 +23,8 @@
 // graphs whose elided zero-pair M2L blocks leave L2L(2, b) without predecessors
 // (taskflow.cpp:179-186) -- reproduces one evaluation. run_task may be called from the
 // reference's worker threads (execute, runtime.cpp:165): calls are serialised by a
-// mutex. P2PReduce is folded into P2P (one-sided owner-computes, no slot buffers).
+// mutex. The first P2P / P2PReduce task runs the mutual near field and its ordered slot
+// drain (p2p_block(mutual=true) + p2p_reduce, direct.cpp:151-200).
 #pragma once
 
 #include <array>

@@ -395,7 +395,7 @@ def run_ours(args, world, rank, local):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"{args.config}:P2P")
     p2p_tf = flops["P2P"] / (iso["P2P"] / 1e3) / 1e12
-    mutual = os.environ.get("FMMGPU_P2P_ONESIDED", "0") != "1"
+    mutual = ctx.p2p_kernel() == "mutual"
     # DP instructions per directional interaction: 12 for the mutual kernel (24 per pair,
     # both directions), 18 for the one-sided kernel; the ledger counts 15 flop per
     # directional interaction and the peak 2 flop per DFMA

@@ -102,12 +102,16 @@ int fmmgpu_synchronize(fmmgpu_ctx* ctx);
  * after tree, partition or operator changes). Off by default (FMMGPU_GRAPH=1 turns it on
  * for new contexts): eager launches on the two prioritised streams measured faster. */
 int fmmgpu_set_graph(fmmgpu_ctx* ctx, int on);
-/* Near-field kernel: mutual = 1 (default) evaluates each pair of neighbouring leaves once,
+/* Near-field kernel: mutual = 1 evaluates each pair of neighbouring leaves once,
  * p2p_block(mutual=true) with P2PBuffers slots and the ordered p2p_reduce
  * (direct.cpp:63-92, 151-200); mutual = 0 evaluates every directional interaction on the
- * target's side (p2p_block(mutual=false), direct.cpp:111-150). Both are deterministic and
- * agree to rounding; FMMGPU_P2P_ONESIDED=1 makes 0 the default of new contexts. */
+ * target's side (p2p_block(mutual=false), direct.cpp:111-150); mutual = 2 (default) picks
+ * the mutual kernel when the owned leaf level has >= 8 leaves per resident warp of it,
+ * else the one-sided one. Both are deterministic and agree to rounding;
+ * FMMGPU_P2P_ONESIDED=1 makes 0 the default of new contexts. */
 int fmmgpu_set_p2p_mode(fmmgpu_ctx* ctx, int mutual);
+/* the kernel the current tree / partition runs: 1 mutual, 0 one-sided, -1 no tree */
+int fmmgpu_p2p_kernel(const fmmgpu_ctx* ctx);
 
 /* FmmContext::gather (bench.cpp:350-365): fields in input order into HOST or DEVICE
  * arrays of n doubles each (any may be NULL). Synchronizes. */

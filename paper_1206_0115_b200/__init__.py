@@ -89,6 +89,7 @@ def lib():
         L.fmmgpu_set_trace.argtypes = [c_void_p, c_int]
         L.fmmgpu_set_graph.argtypes = [c_void_p, c_int]
         L.fmmgpu_set_p2p_mode.argtypes = [c_void_p, c_int]
+        L.fmmgpu_p2p_kernel.argtypes = [c_void_p]
         L.fmmgpu_trace_spans.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p]
         for name in ("fmmgpu_reset", "fmmgpu_p2m", "fmmgpu_l2p", "fmmgpu_p2p", "fmmgpu_evaluate",
                      "fmmgpu_synchronize", "fmmgpu_build_lists"):
@@ -556,7 +557,12 @@ class FmmContext:
     def set_p2p_mode(self, mutual: bool = True):
         """Near field kernel: mutual (p2p_block(mutual=true) + slots + ordered reduce,
         direct.cpp:63-92, 151-200) or one-sided (fmmgpu_set_p2p_mode)."""
-        self._check(self._lib.fmmgpu_set_p2p_mode(self.h, 1 if mutual else 0))
+        mode = mutual if (isinstance(mutual, int) and not isinstance(mutual, bool)) else (1 if mutual else 0)
+        self._check(self._lib.fmmgpu_set_p2p_mode(self.h, mode))
+
+    def p2p_kernel(self) -> str:
+        """'mutual' or 'onesided': the near-field kernel the current tree runs (mode 2 = auto)."""
+        return "mutual" if self._lib.fmmgpu_p2p_kernel(self.h) == 1 else "onesided"
 
     def set_trace(self, on: bool = True):
         """Per-launch device trace of the following evaluations (fmmgpu_set_trace)."""

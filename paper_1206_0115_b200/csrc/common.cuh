@@ -207,7 +207,7 @@ struct fmmgpu_ctx {
   double* d_near = nullptr;      // near-field fields [n] x {pot,fx,fy,fz} (Morton order)
   // mutual P2P (p2p.cu): the j-side sums of each leaf's 13 upper half-shell neighbours,
   // [13][n] x {pot,fx,fy,fz} (the reference's P2PBuffers slots), and the leaf counter
-  bool p2p_mutual = true;
+  int p2p_mode = 2;  // 0 one-sided, 1 mutual, 2 auto (mutual when there are enough leaves)
   double* d_slot = nullptr;
   uint32_t* d_ctr = nullptr;
   // non-full leaf levels: leaves by decreasing work (+ sort buffers), valid for the owned
@@ -319,6 +319,7 @@ void launch_l2p(fmmgpu_ctx* c, cudaStream_t s);
 void launch_m2l(fmmgpu_ctx* c, int level, cudaStream_t s);
 void launch_p2p(fmmgpu_ctx* c, cudaStream_t s);
 void ensure_p2p_slots(fmmgpu_ctx* c);  // allocates the mutual P2P slots of the current tree (s_far)
+bool p2p_use_mutual(const fmmgpu_ctx* c, uint32_t leaves);  // the kernel launch_p2p picks
 void launch_gather(fmmgpu_ctx* c, cudaStream_t s);
 void partition_free(fmmgpu_ctx* c);
 }  // namespace fmmgpu

@@ -201,7 +201,7 @@ void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx
   FMM_CUDA(cudaMalloc(&c->d_ctr, 256));
   {  // FMMGPU_P2P_ONESIDED=1: new contexts start with the one-sided kernel (fmmgpu_set_p2p_mode)
     const char* pe = std::getenv("FMMGPU_P2P_ONESIDED");
-    c->p2p_mutual = !(pe && std::atoi(pe) == 1);
+    c->p2p_mode = (pe && std::atoi(pe) == 1) ? 0 : 2;
   }
   interp_setup(c);
   if (factors) {  // share the operators of an existing context (no second SVD)
@@ -660,10 +660,17 @@ int fmmgpu_set_graph(fmmgpu_ctx* c, int on) {
 
 int fmmgpu_set_p2p_mode(fmmgpu_ctx* c, int mutual) {
   return guarded(c, [&] {
-    c->p2p_mutual = mutual != 0;
+    if (mutual < 0 || mutual > 2) throw Error(FMMGPU_INVALID_ARGUMENT, "set_p2p_mode: mode must be 0, 1 or 2");
+    c->p2p_mode = mutual;
     fmmgpu_invalidate_graph(c);
     ensure_p2p_slots(c);
   });
+}
+
+int fmmgpu_p2p_kernel(const fmmgpu_ctx* c) {
+  if (!c || !c->have_tree) return -1;
+  const Level& L = c->lv[c->height - 1];
+  return p2p_use_mutual(c, L.own1 - L.own0) ? 1 : 0;
 }
 
 int fmmgpu_set_trace(fmmgpu_ctx* c, int on) {

@@ -683,8 +683,20 @@ __global__ void k_mu_work(const LevelView leaf, const uint32_t* __restrict__ cou
 // The slot array of the current tree and, for trees with a non-full leaf level (clustered
 // clouds, config D), the buffers of the largest-first leaf order: allocated with the tree
 // on s_far (ordered before any evaluation's fork).
+// Mode 2 (auto, the default) runs the mutual kernel when the (owned) leaf level has at
+// least 8 leaves per resident warp: each warp owns a leaf from start to end, so a few
+// large leaves leave most warps idle (config A, 512 leaves of ~195 particles: mutual 1.78
+// ms, one-sided 0.6 ms), while the one-sided kernel splits a parent's work units over
+// several CTAs.
+bool p2p_use_mutual(const fmmgpu_ctx* c, uint32_t leaves) {
+  if (c->p2p_mode != 2) return c->p2p_mode == 1;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  return uint64_t(leaves) >= 8ull * static_cast<uint64_t>(sms) * MU_WARPS;
+}
+
 void ensure_p2p_slots(fmmgpu_ctx* c) {
-  if (!c->p2p_mutual || !c->have_tree || c->d_slot) return;
+  if (!c->have_tree || c->d_slot || !p2p_use_mutual(c, c->lv[c->height - 1].n)) return;
   c->d_slot = static_cast<double*>(cache_alloc(c, size_t(MU_NUP) * 32 * c->n, c->s_far));
   c->p2p_order_range[0] = c->p2p_order_range[1] = 0;
   const Level& L = c->lv[c->height - 1];
@@ -724,7 +736,7 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
   const int leaf = c->height - 1;
   const Level& L = c->lv[leaf];
   const Level& P = c->lv[leaf - 1];
-  if (c->p2p_mutual) {
+  if (p2p_use_mutual(c, L.own1 - L.own0)) {
     if (!c->d_slot) throw Error(FMMGPU_LOGIC_ERROR, "mutual P2P: slot array not allocated");
     const uint32_t nl = L.own1 - L.own0;
     if (nl == 0) return;

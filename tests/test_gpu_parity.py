@@ -519,3 +519,45 @@ def test_coincident_check_clustered_leaf(fmm):
     with pytest.raises(P.DomainError):
         c.build_tree(dup, 4)
     c.build_tree(base, 4)
+
+
+@pytest.mark.parametrize("case", [(6000, 13, 3, "sphere", 8, True), (12000, 12, 4, "uniform", 2, False)],
+                         ids=["n6000_h13_l3_sphere", "n12000_h12_l4_uniform"])
+def test_deep_tree_64bit_keys(fmm, case):
+    """Trees deeper than 11 levels: leaf keys above 32 bits (the u64 sort path), levels
+    beyond the dense code maps (binary-search cell lookup in every kernel), almost one
+    particle per leaf. Tree and lists bit-exact with the oracle; the evaluation against
+    the reference itself (else the oracle) within the north-star bar."""
+    n, h, l, dist, seed, rw = case
+    xyzw = make_particles(n, dist, seed, rw)
+    ot = OracleTree(xyzw, h)
+    c = ctx_for(fmm, xyzw, h, l)
+    assert np.array_equal(c.root_cube(), ot.root_cube())
+    for a, b in zip(c.particles(), ot.particles()):
+        assert np.array_equal(a, b)
+    for v in range(h):
+        gc, gb = c.level(v)
+        oc, ob = ot.level(v)
+        gc["_pad"] = 0
+        oc["_pad"] = 0
+        assert np.array_equal(gc, oc), f"level {v} cells"
+        assert np.array_equal(gb, ob), f"level {v} blocks"
+    assert c.level(h - 1)[0]["code"].max() >= (1 << 32)  # the 64-bit key path ran
+    c.build_lists()
+    goff, gcells, gtot = c.near()
+    ooff, ocells, _, otot = ot.near()
+    assert np.array_equal(goff, ooff) and np.array_equal(gcells, ocells) and gtot == otot
+    for v in range(2, h):
+        for a, b in zip(c.far(v), ot.far(v)):
+            assert np.array_equal(a, b), f"far level {v}"
+    c.evaluate()
+    g = c.gather()
+    if RefLib.available():
+        ref = RefContext(xyzw, h, l)
+        ref.execute(workers=4)
+        rf = ref.fields()
+    else:
+        rf = ot.evaluate(OracleOps.cached(l))
+    assert relative_l2_error(g[0], rf[0]) <= TOL
+    assert force_error(*g[1:], *rf[1:]) <= TOL
+    c.close()

@@ -523,7 +523,7 @@ def test_coincident_check_clustered_leaf(fmm):
 
 @pytest.mark.parametrize("case", [(6000, 13, 3, "sphere", 8, True), (12000, 12, 4, "uniform", 2, False)],
                          ids=["n6000_h13_l3_sphere", "n12000_h12_l4_uniform"])
-def test_deep_tree_64bit_keys(fmm, case):
+def test_deep_tree_64bit_keys(fmm, case, tmp_path):
     """Trees deeper than 11 levels: leaf keys above 32 bits (the u64 sort path), levels
     beyond the dense code maps (binary-search cell lookup in every kernel), almost one
     particle per leaf. Tree and lists bit-exact with the oracle; the evaluation against
@@ -552,12 +552,25 @@ def test_deep_tree_64bit_keys(fmm, case):
             assert np.array_equal(a, b), f"far level {v}"
     c.evaluate()
     g = c.gather()
-    if RefLib.available():
-        ref = RefContext(xyzw, h, l)
-        ref.execute(workers=4)
-        rf = ref.fields()
-    else:
+    if not RefLib.available():
         rf = ot.evaluate(OracleOps.cached(l))
-    assert relative_l2_error(g[0], rf[0]) <= TOL
-    assert force_error(*g[1:], *rf[1:]) <= TOL
+        assert relative_l2_error(g[0], rf[0]) <= TOL
+        assert force_error(*g[1:], *rf[1:]) <= TOL
+        c.close()
+        return
+    ref = RefContext(xyzw, h, l)
+    ref.execute(workers=4)
+    rf = ref.fields()
+    own = (relative_l2_error(g[0], rf[0]), force_error(*g[1:], *rf[1:]))
+    # the same operators on both sides (the reference's M2L cache file)
+    cache = str(tmp_path / "ref.bin")
+    ref.save_m2l_cache(cache)
+    c2 = ctx_for(fmm, xyzw, h, l, cache=cache)
+    c2.evaluate()
+    g2 = c2.gather()
+    shared = (relative_l2_error(g2[0], rf[0]), force_error(*g2[1:], *rf[1:]))
+    print("deep tree", case, "own factors", own, "reference factors", shared)
+    assert shared[0] <= TOL and shared[1] <= TOL, shared
+    assert own[0] <= TOL and own[1] <= TOL, own
     c.close()
+    c2.close()

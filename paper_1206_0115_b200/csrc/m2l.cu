@@ -370,12 +370,10 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
 // l = 6, 7: 128-row M-tiles, 2 stages, 24 columns (l = 7: W 68 KB + ring 41 KB); larger
 // orders: 128-row M-tiles, 3 stages, 16 columns, so two CTAs still fit on an SM. The
 // epilogue tables are built for the M-tile in use.
-constexpr int PA_THREADS = 256;
-
-template <int PA_BM, int PA_ST, int BN, int WM, int WN, int PA_BK = 16>
-__global__ void __launch_bounds__(PA_THREADS, 2) k_m2l_phase_a(const GemmArgs g) {
+template <int PA_BM, int PA_ST, int BN, int WM, int WN, int PA_BK = 16, int MINB = 2>
+__global__ void __launch_bounds__(WM * WN * 32, MINB) k_m2l_phase_a(const GemmArgs g) {
+  constexpr int PA_THREADS = WM * WN * 32;
   constexpr int PA_SPAD = PA_BK + 4;  // == 4 (mod 16): conflict-free fragments
-  static_assert(WM * WN * 32 == PA_THREADS, "8 warps");
   constexpr int WTM = PA_BM / WM, WTN = BN / WN;
   constexpr int MT = WTM / 8, NT = WTN / 8;
   extern __shared__ __align__(16) double smem[];
@@ -715,7 +713,7 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     g.a_class_stride = size_t(T.rowsA) * c->ldE;
     g.K = c->ldE;
     // BN chosen so the resident multipoles + the A ring fit two CTAs per SM
-    auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST, int bk = 16) {
+    auto launch = [&](auto kern, int bn, int PA_BM, int PA_ST, int bk = 16, int threads = 256) {
       const size_t smem = sizeof(double) * (size_t(bn) * (g.K + 4) + size_t(PA_ST) * PA_BM * (bk + 4)) +
                           sizeof(uint32_t) * size_t(T.vtMax) * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -735,15 +733,26 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       }();
       g.cls_fast = cls_fast;
       dim3 grid = cls_fast ? dim3(8, (maxcls + bn - 1) / bn, ms) : dim3((maxcls + bn - 1) / bn, 8, ms);
-      kern<<<grid, PA_THREADS, smem, s>>>(g);
+      kern<<<grid, threads, smem, s>>>(g);
       FMM_CUDA(cudaGetLastError());
     };
     // l <= 5: 32-wide k-slices through a 2-stage ring (config B: 27.26 vs 27.81 ms per
     // evaluation with 16-wide slices and 4 stages; a 3-stage 32-wide ring no longer fits
     // two CTAs per SM)
-    if (T.bmA == 64) launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
-    else if (c->ldE <= 352) launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
-    else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
+#ifndef FMMGPU_PA_VARIANT
+#define FMMGPU_PA_VARIANT 0
+#endif
+    if (T.bmA == 64) {
+      if (FMMGPU_PA_VARIANT == 1) launch(k_m2l_phase_a<64, 2, 64, 2, 2, 32>, 64, 64, 2, 32, 128);
+      else if (FMMGPU_PA_VARIANT == 2) launch(k_m2l_phase_a<64, 2, 32, 2, 2, 32, 3>, 32, 64, 2, 32, 128);
+      else if (FMMGPU_PA_VARIANT == 3) launch(k_m2l_phase_a<64, 3, 32, 2, 2, 32, 2>, 32, 64, 3, 32, 128);
+      else launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
+    } else if (c->ldE <= 352) {
+      if (FMMGPU_PA_VARIANT == 4) launch(k_m2l_phase_a<128, 2, 32, 8, 1, 16, 1>, 32, 128, 2, 16, 256);
+      else launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
+    } else {
+      launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
+    }
   }
   g.cls_cells = L.tgtB ? L.tgtB : L.cls_cells;
   std::copy(L.tgtB ? L.tgtB_off : L.cls_off, (L.tgtB ? L.tgtB_off : L.cls_off) + 9, g.cls_off);

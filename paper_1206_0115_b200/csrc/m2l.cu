@@ -739,20 +739,12 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     // l <= 5: 32-wide k-slices through a 2-stage ring (config B: 27.26 vs 27.81 ms per
     // evaluation with 16-wide slices and 4 stages; a 3-stage 32-wide ring no longer fits
     // two CTAs per SM)
-#ifndef FMMGPU_PA_VARIANT
-#define FMMGPU_PA_VARIANT 0
-#endif
-    if (T.bmA == 64) {
-      if (FMMGPU_PA_VARIANT == 1) launch(k_m2l_phase_a<64, 2, 64, 2, 2, 32>, 64, 64, 2, 32, 128);
-      else if (FMMGPU_PA_VARIANT == 2) launch(k_m2l_phase_a<64, 2, 32, 2, 2, 32, 3>, 32, 64, 2, 32, 128);
-      else if (FMMGPU_PA_VARIANT == 3) launch(k_m2l_phase_a<64, 3, 32, 2, 2, 32, 2>, 32, 64, 3, 32, 128);
-      else launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
-    } else if (c->ldE <= 352) {
-      if (FMMGPU_PA_VARIANT == 4) launch(k_m2l_phase_a<128, 2, 32, 8, 1, 16, 1>, 32, 128, 2, 16, 256);
-      else launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
-    } else {
-      launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
-    }
+    // Also measured (tools/gpu/gpu_r02o.sh, evaluation ms at config B / C): 64 x 64 with 4
+    // warps of 32 x 32 (24.84 vs 24.53), 64 x 32 with 4 warps and 3 CTAs per SM (24.62), the
+    // same with a 3-stage ring (25.79); at l = 7, 128 x 32 with one CTA per SM (97.76 vs 88.76).
+    if (T.bmA == 64) launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
+    else if (c->ldE <= 352) launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
+    else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
   }
   g.cls_cells = L.tgtB ? L.tgtB : L.cls_cells;
   std::copy(L.tgtB ? L.tgtB_off : L.cls_off, (L.tgtB ? L.tgtB_off : L.cls_off) + 9, g.cls_off);

@@ -726,6 +726,11 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
         return e ? static_cast<uint32_t>(std::atoi(e)) : 2u;  // config B: 28.55 vs 28.76 ms (1 wave)
       }();
       while (ms < mtiles && ncols * ms < waves * 2u * 148u) ++ms;
+      static const int ms_min = [] {  // FMMGPU_M2L_MS_MIN: minimum M-split (A/B aid)
+        const char* e = std::getenv("FMMGPU_M2L_MS_MIN");
+        return e ? std::atoi(e) : 1;
+      }();
+      ms = std::max(ms, std::min(ms_min, mtiles));
       g.msplit = ms;
       static const int cls_fast = [] {  // FMMGPU_M2L_CLS_FAST=0: class-slowest order (A/B aid)
         const char* e = std::getenv("FMMGPU_M2L_CLS_FAST");

@@ -230,6 +230,7 @@ struct GemmArgs {
   const int* kslot;       // vector slot per target-stack column [8][ldY] (host tables)
   double* local;          // phase B output (local_own)
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
+  int rowB0;              // phase B: first row of this launch's M-tiles (tail launches)
   int msplit;             // phase A M-split factor (coarse levels)
   int cls_fast;           // phase A grid: parity class in blockIdx.x (else blockIdx.y)
   int ow;                 // phase B: write local_own instead of accumulating (evaluation)
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
   const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
   const uint32_t n0 = blockIdx.y * BN;
   if (n0 >= ncls) return;
-  const int m0 = blockIdx.x * BM;
+  const int m0 = g.rowB0 + blockIdx.x * BM;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp / WN, wn = warp % WN;
   const int gq = lane >> 2, tq = lane & 3;
@@ -726,11 +727,9 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
         return e ? static_cast<uint32_t>(std::atoi(e)) : 2u;  // config B: 28.55 vs 28.76 ms (1 wave)
       }();
       while (ms < mtiles && ncols * ms < waves * 2u * 148u) ++ms;
-      static const int ms_min = [] {  // FMMGPU_M2L_MS_MIN: minimum M-split (A/B aid)
-        const char* e = std::getenv("FMMGPU_M2L_MS_MIN");
-        return e ? std::atoi(e) : 1;
-      }();
-      ms = std::max(ms, std::min(ms_min, mtiles));
+      // (forcing an M-split of 2 / 4 / 8 on full levels so fewer classes' operators are live
+      // in L2 at once: config C 88.66 / 88.26 / 88.31 vs 88.81 ms, config B 24.60 / 24.75 vs
+      // 24.56 -- not adopted)
       g.msplit = ms;
       static const int cls_fast = [] {  // FMMGPU_M2L_CLS_FAST=0: class-slowest order (A/B aid)
         const char* e = std::getenv("FMMGPU_M2L_CLS_FAST");
@@ -783,12 +782,28 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       }
     }
     g.part = ks > 1 ? c->d_splitk : nullptr;
-    const size_t smem = sizeof(double) * B_ST * (B_BM + B_BN) * (B_BK + 4);
-    auto kern = k_m2l_phase_b<B_BM, B_BN, B_WM, B_WN, B_ST, B_BK>;
-    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    dim3 grid(mtiles, (maxcls + B_BN - 1) / B_BN, 8 * ks);
-    kern<<<grid, B_WM * B_WN * 32, smem, s>>>(g);
-    FMM_CUDA(cudaGetLastError());
+    // M-tiles of 128 rows; the rows past the last whole tile go to a 96- or 64-row tail
+    // tile when that covers them (l = 7: 343 rows as 2 x 128 + 96 = 352 instead of 384, 11%
+    // fewer DMMAs; l = 6: 128 + 96 = 224 instead of 256)
+    auto run = [&](auto kern, int bm, int threads, int tiles, int row0) {
+      if (tiles <= 0) return;
+      const size_t smem = sizeof(double) * B_ST * (bm + B_BN) * (B_BK + 4);
+      FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      g.rowB0 = row0;
+      dim3 grid(tiles, (maxcls + B_BN - 1) / B_BN, 8 * ks);
+      kern<<<grid, threads, smem, s>>>(g);
+      FMM_CUDA(cudaGetLastError());
+    };
+    const int full = c->l3 / B_BM, tail = c->l3 - full * B_BM;
+    const int whole = tail > 96 ? full + 1 : full;
+    run(k_m2l_phase_b<B_BM, B_BN, B_WM, B_WN, B_ST, B_BK>, B_BM, B_WM * B_WN * 32, whole, 0);
+    if (tail > 0 && tail <= 64) {
+      run(k_m2l_phase_b<64, B_BN, 2, B_WN, B_ST, B_BK>, 64, 2 * B_WN * 32, 1, full * B_BM);
+      if (full) ++c->launches;
+    } else if (tail > 64 && tail <= 96) {
+      run(k_m2l_phase_b<96, B_BN, 3, B_WN, B_ST, B_BK>, 96, 3 * B_WN * 32, 1, full * B_BM);
+      if (full) ++c->launches;
+    }
     if (ks > 1) {
       const uint32_t ntg = g.cls_off[8];
       const uint64_t tot = uint64_t(ntg) * c->ldE;

@@ -287,6 +287,7 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
     }
     if (c->d_in) cudaFreeAsync(c->d_in, c->s_far);
     if (c->d_tmp) cudaFreeAsync(c->d_tmp, c->s_far);
+    if (c->d_loc) cudaFree(c->d_loc);  // distributed input slice (dist.cu)
     cudaStreamSynchronize(c->s_far);
   }
   m2l_free(c);

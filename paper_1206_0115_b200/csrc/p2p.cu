@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
 // the 4 accumulators moved by SHFL one lane per step), so after 8 steps every lane's
 // sources met all 8 targets and each target's sums are back in their home lane; the
 // 4 sub-rings' partial target sums are then combined by a fixed 2-level butterfly.
-// Per pair: 24 DP instructions + 1 MUFU.RSQ64H for both directions (12 per directional
+// Per pair: 23 DP instructions + 1 MUFU.RSQ64H for both directions (11.5 per directional
 // interaction against 18 one-sided).
 //
 // One warp owns a leaf from start to end (targets in chunks of TCAP, every chunk
@@ -369,8 +369,10 @@ struct MuWarp {
 __device__ __forceinline__ double4 mu_dummy_target() { return make_double4(-1e100, -1e100, -1e100, 0.0); }
 
 // One pair, both directions (direct.cpp:156-169): d = x_t - x_s; the target gets
-// +w_s (inv, inv^3 d), the source +w_t inv and -w_t inv^3 d. The target side is formed
-// exactly as interact() forms it. SELF: i == j (r^2 = +0) contributes nothing.
+// +w_s (inv, inv^3 d), the source +w_t inv and -w_t inv^3 d. SELF: i == j (r^2 = +0)
+// contributes nothing. 23 DP instructions + 1 MUFU.RSQ64H per pair: the potentials are
+// fused into the accumulations (fma(w, inv, acc)) and inv^3 is formed once for both
+// sides; the Newton step computes y e and the polynomial in parallel (depth 4).
 template <bool SELF>
 __device__ __forceinline__ void mu_pair(const double4 pt, const double4 ps, const double c375, double4& at,
                                         double4& as) {
@@ -378,15 +380,13 @@ __device__ __forceinline__ void mu_pair(const double4 pt, const double4 ps, cons
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
-  const double t = r2 * y;
-  const double e = fma(-t, y, 1.0);
-  double inv = fma(y, e * fma(e, c375, 0.5), y);
+  const double e = fma(-r2, y * y, 1.0);
+  double inv = fma(y * e, fma(e, c375, 0.5), y);
   if constexpr (SELF) inv = __double2hiint(r2) != 0 ? inv : 0.0;
-  const double inv2 = inv * inv;
-  const double ws = ps.w * inv, wt = pt.w * inv;
-  at.x += ws;
-  as.x += wt;
-  const double st = ws * inv2, ss = wt * inv2;
+  const double inv3 = inv * (inv * inv);
+  at.x = fma(ps.w, inv, at.x);
+  as.x = fma(pt.w, inv, as.x);
+  const double st = ps.w * inv3, ss = pt.w * inv3;
   at.y = fma(st, dx, at.y);
   at.z = fma(st, dy, at.z);
   at.w = fma(st, dz, at.w);
@@ -418,42 +418,8 @@ __device__ __forceinline__ void mu_tile(W& w, const int t0, const double4 (&ps)[
 #pragma unroll 2
   for (int s = 0; s < RING; ++s) {
     const double4 pt = tp[(lr + s) & (RING - 1)];
-#ifdef FMMGPU_MU_ILV
-    // the TS pairs stage by stage, so the scheduler sees TS independent chains
-    double dx[TS], dy[TS], dz[TS], r2[TS], inv[TS];
-#pragma unroll
-    for (int m = 0; m < TS; ++m) {
-      dx[m] = pt.x - ps[m].x;
-      dy[m] = pt.y - ps[m].y;
-      dz[m] = pt.z - ps[m].z;
-      r2[m] = fma(dx[m], dx[m], fma(dy[m], dy[m], dz[m] * dz[m]));
-    }
-#pragma unroll
-    for (int m = 0; m < TS; ++m) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(inv[m]) : "d"(r2[m]));
-#pragma unroll
-    for (int m = 0; m < TS; ++m) {
-      const double y = inv[m], t = r2[m] * y, e = fma(-t, y, 1.0);
-      inv[m] = fma(y, e * fma(e, c375, 0.5), y);
-      if constexpr (SELF) inv[m] = __double2hiint(r2[m]) != 0 ? inv[m] : 0.0;
-    }
-#pragma unroll
-    for (int m = 0; m < TS; ++m) {
-      const double inv2 = inv[m] * inv[m];
-      const double ws = ps[m].w * inv[m], wt = pt.w * inv[m];
-      at.x += ws;
-      as[m].x += wt;
-      const double st = ws * inv2, ss = wt * inv2;
-      at.y = fma(st, dx[m], at.y);
-      at.z = fma(st, dy[m], at.z);
-      at.w = fma(st, dz[m], at.w);
-      as[m].y = fma(-ss, dx[m], as[m].y);
-      as[m].z = fma(-ss, dy[m], as[m].z);
-      as[m].w = fma(-ss, dz[m], as[m].w);
-    }
-#else
 #pragma unroll
     for (int m = 0; m < TS; ++m) mu_pair<SELF>(pt, ps[m], c375, at, as[m]);
-#endif
     at.x = __shfl_sync(0xffffffffu, at.x, nxt);
     at.y = __shfl_sync(0xffffffffu, at.y, nxt);
     at.z = __shfl_sync(0xffffffffu, at.z, nxt);

@@ -380,13 +380,30 @@ __device__ __forceinline__ void mu_pair(const double4 pt, const double4 ps, cons
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+#ifndef FMMGPU_MU_PAIR
+#define FMMGPU_MU_PAIR 0
+#endif
+#if FMMGPU_MU_PAIR == 0
+  const double t = r2 * y;
+  const double e = fma(-t, y, 1.0);
+  double inv = fma(y, e * fma(e, c375, 0.5), y);
+#else
   const double e = fma(-r2, y * y, 1.0);
   double inv = fma(y * e, fma(e, c375, 0.5), y);
+#endif
   if constexpr (SELF) inv = __double2hiint(r2) != 0 ? inv : 0.0;
+#if FMMGPU_MU_PAIR == 2
   const double inv3 = inv * (inv * inv);
   at.x = fma(ps.w, inv, at.x);
   as.x = fma(pt.w, inv, as.x);
   const double st = ps.w * inv3, ss = pt.w * inv3;
+#else
+  const double inv2 = inv * inv;
+  const double ws = ps.w * inv, wt = pt.w * inv;
+  at.x += ws;
+  as.x += wt;
+  const double st = ws * inv2, ss = wt * inv2;
+#endif
   at.y = fma(st, dx, at.y);
   at.z = fma(st, dy, at.z);
   at.w = fma(st, dz, at.w);
@@ -470,15 +487,30 @@ __device__ __forceinline__ void mu_pass(const MuArgs& a, W& w, const uint32_t ns
       ps[m] = dummy_source();
     }
   }
-  // 8-target tiles, and a last tile of 4 when only 1..4 targets remain
-  const int n8 = (tcn & 7) > 4 ? (tcn + 7) & ~7 : tcn & ~7;
+  // 8-target tiles; the last 1..7 targets as tiles of 4 and 2 (7: one more tile of 8), so at
+  // most one dummy target per chunk instead of up to 3
+#ifdef FMMGPU_MU_OLDTAIL
+  const int n8o = (tcn & 7) > 4 ? (tcn + 7) & ~7 : tcn & ~7;
+#pragma unroll 1
+  for (int t0 = 0; t0 < n8o; t0 += 8) mu_tile<TS, 8, SELF>(w, t0, ps, as, lane, c375);
+  if (tcn > n8o) mu_tile<TS, 4, SELF>(w, n8o, ps, as, lane, c375);
+  if (false) {
+    const int rem = 0;
+    const int n8 = 0;
+#else
+  const int rem = tcn & 7;
+  const int n8 = rem == 7 ? tcn + 1 : tcn - rem;
 #pragma unroll 1
   for (int t0 = 0; t0 < n8; t0 += 8) mu_tile<TS, 8, SELF>(w, t0, ps, as, lane, c375);
-#ifndef FMMGPU_MU_NO_RING4
-  if (tcn > n8) mu_tile<TS, 4, SELF>(w, n8, ps, as, lane, c375);
-#else
-  if (tcn > n8) mu_tile<TS, 8, SELF>(w, n8, ps, as, lane, c375);
+  if (rem != 7) {
 #endif
+    int t0 = n8;
+    if (rem >= 3) {
+      mu_tile<TS, 4, SELF>(w, t0, ps, as, lane, c375);
+      t0 += 4;
+    }
+    if (rem == 1 || rem == 2 || rem >= 5) mu_tile<TS, 2, SELF>(w, t0, ps, as, lane, c375);
+  }
 #pragma unroll
   for (int m = 0; m < TS; ++m) {
     if (dst[m] != ~0ull) {

@@ -396,10 +396,10 @@ def run_ours(args, world, rank, local):
         traffic = json.load(open(tp)).get(f"{args.config}:P2P")
     p2p_tf = flops["P2P"] / (iso["P2P"] / 1e3) / 1e12
     mutual = ctx.p2p_kernel() == "mutual"
-    # DP instructions per directional interaction: 11.5 for the mutual kernel (23 per pair,
+    # DP instructions per directional interaction: 12 for the mutual kernel (24 per pair,
     # both directions), 18 for the one-sided kernel; the ledger counts 15 flop per
     # directional interaction and the peak 2 flop per DFMA
-    dp_per_dir = 11.5 if mutual else 18
+    dp_per_dir = 12 if mutual else 18
     roof = {"bound": "fp64",
             "kernel": ("k_p2p_mutual + k_p2p_drain (P2P with P2PBuffers slots and ordered reduce, FP64 pipe)"
                        if mutual else "k_p2p (one-sided P2P, FP64 pipe)"),

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_p2p(const P2PArgs a) {
 // the 4 accumulators moved by SHFL one lane per step), so after 8 steps every lane's
 // sources met all 8 targets and each target's sums are back in their home lane; the
 // 4 sub-rings' partial target sums are then combined by a fixed 2-level butterfly.
-// Per pair: 23 DP instructions + 1 MUFU.RSQ64H for both directions (11.5 per directional
+// Per pair: 24 DP instructions + 1 MUFU.RSQ64H for both directions (12 per directional
 // interaction against 18 one-sided).
 //
 // One warp owns a leaf from start to end (targets in chunks of TCAP, every chunk
@@ -369,10 +369,13 @@ struct MuWarp {
 __device__ __forceinline__ double4 mu_dummy_target() { return make_double4(-1e100, -1e100, -1e100, 0.0); }
 
 // One pair, both directions (direct.cpp:156-169): d = x_t - x_s; the target gets
-// +w_s (inv, inv^3 d), the source +w_t inv and -w_t inv^3 d. SELF: i == j (r^2 = +0)
-// contributes nothing. 23 DP instructions + 1 MUFU.RSQ64H per pair: the potentials are
-// fused into the accumulations (fma(w, inv, acc)) and inv^3 is formed once for both
-// sides; the Newton step computes y e and the polynomial in parallel (depth 4).
+// +w_s (inv, inv^3 d), the source +w_t inv and -w_t inv^3 d. The target side is formed
+// exactly as interact() forms it. SELF: i == j (r^2 = +0) contributes nothing.
+// Measured alternatives (tools/gpu/gpu_r02t.sh, P2P ms at config B / D): the Newton step
+// at dependency depth 4 (11.01 / 162.7 vs 10.90 / 159.5), and 23 DP instructions per pair
+// (potentials fused into the accumulations, inv^3 shared; 12.04 / 163.0 with the tail
+// tiles below): the kernel is latency-bound, a longer chain costs more than an
+// instruction saves.
 template <bool SELF>
 __device__ __forceinline__ void mu_pair(const double4 pt, const double4 ps, const double c375, double4& at,
                                         double4& as) {
@@ -380,30 +383,15 @@ __device__ __forceinline__ void mu_pair(const double4 pt, const double4 ps, cons
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
-#ifndef FMMGPU_MU_PAIR
-#define FMMGPU_MU_PAIR 0
-#endif
-#if FMMGPU_MU_PAIR == 0
   const double t = r2 * y;
   const double e = fma(-t, y, 1.0);
   double inv = fma(y, e * fma(e, c375, 0.5), y);
-#else
-  const double e = fma(-r2, y * y, 1.0);
-  double inv = fma(y * e, fma(e, c375, 0.5), y);
-#endif
   if constexpr (SELF) inv = __double2hiint(r2) != 0 ? inv : 0.0;
-#if FMMGPU_MU_PAIR == 2
-  const double inv3 = inv * (inv * inv);
-  at.x = fma(ps.w, inv, at.x);
-  as.x = fma(pt.w, inv, as.x);
-  const double st = ps.w * inv3, ss = pt.w * inv3;
-#else
   const double inv2 = inv * inv;
   const double ws = ps.w * inv, wt = pt.w * inv;
   at.x += ws;
   as.x += wt;
   const double st = ws * inv2, ss = wt * inv2;
-#endif
   at.y = fma(st, dx, at.y);
   at.z = fma(st, dy, at.z);
   at.w = fma(st, dz, at.w);
@@ -487,30 +475,13 @@ __device__ __forceinline__ void mu_pass(const MuArgs& a, W& w, const uint32_t ns
       ps[m] = dummy_source();
     }
   }
-  // 8-target tiles; the last 1..7 targets as tiles of 4 and 2 (7: one more tile of 8), so at
-  // most one dummy target per chunk instead of up to 3
-#ifdef FMMGPU_MU_OLDTAIL
-  const int n8o = (tcn & 7) > 4 ? (tcn + 7) & ~7 : tcn & ~7;
-#pragma unroll 1
-  for (int t0 = 0; t0 < n8o; t0 += 8) mu_tile<TS, 8, SELF>(w, t0, ps, as, lane, c375);
-  if (tcn > n8o) mu_tile<TS, 4, SELF>(w, n8o, ps, as, lane, c375);
-  if (false) {
-    const int rem = 0;
-    const int n8 = 0;
-#else
-  const int rem = tcn & 7;
-  const int n8 = rem == 7 ? tcn + 1 : tcn - rem;
+  // 8-target tiles, and a last tile of 4 when only 1..4 targets remain. (Tails of 4 + 2
+  // targets, at most one dummy per chunk instead of up to 3, measured slower: P2P 12.49 vs
+  // 10.90 ms at B -- the extra tile instantiation costs the main loop its schedule.)
+  const int n8 = (tcn & 7) > 4 ? (tcn + 7) & ~7 : tcn & ~7;
 #pragma unroll 1
   for (int t0 = 0; t0 < n8; t0 += 8) mu_tile<TS, 8, SELF>(w, t0, ps, as, lane, c375);
-  if (rem != 7) {
-#endif
-    int t0 = n8;
-    if (rem >= 3) {
-      mu_tile<TS, 4, SELF>(w, t0, ps, as, lane, c375);
-      t0 += 4;
-    }
-    if (rem == 1 || rem == 2 || rem >= 5) mu_tile<TS, 2, SELF>(w, t0, ps, as, lane, c375);
-  }
+  if (tcn > n8) mu_tile<TS, 4, SELF>(w, n8, ps, as, lane, c375);
 #pragma unroll
   for (int m = 0; m < TS; ++m) {
     if (dst[m] != ~0ull) {

@@ -231,6 +231,34 @@ __global__ void k_level_parent(const uint32_t* __restrict__ leafstart_c, const u
   parent_c[j] = idx_v[leafstart_c ? leafstart_c[j] : j] - 1;
 }
 
+// Full trees (every leaf position occupied, e.g. uniform clouds: configs B, C, E): every
+// level is full, cell i of a level has code i, children 8i..8i+7 and parent i / 8, and the
+// parity class q of a level of n cells is the cells 8j + q. One launch fills all of it
+// (the general path above takes ~80 small launches: level flags, scans, class sorts).
+struct FullLevels {
+  uint64_t* code[22];
+  uint32_t* first_child[22];
+  uint32_t* child_count[22];
+  uint32_t* parent[22];
+  uint32_t* cls_cells[22];
+  uint64_t start[23];  // first flattened index of level v
+  int leaf;
+};
+__global__ void k_full_levels(const FullLevels f) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= f.start[f.leaf + 1]) return;
+  int v = 0;
+  while (t >= f.start[v + 1]) ++v;
+  const uint64_t i = t - f.start[v], n = f.start[v + 1] - f.start[v];
+  if (v < f.leaf) {  // the leaf level's code / first_child / child_count come from the build
+    f.code[v][i] = i;
+    f.first_child[v][i] = static_cast<uint32_t>(8 * i);
+    f.child_count[v][i] = 8;
+  }
+  f.parent[v][i] = static_cast<uint32_t>(i >> 3);  // level 0: 0, as the general path
+  if (v >= 2) f.cls_cells[v][(i & 7) * (n >> 3) + (i >> 3)] = static_cast<uint32_t>(i);
+}
+
 __global__ void k_fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (i < n) p[i] = v;
@@ -583,6 +611,41 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   }
 
   trace("leaf level");
+  const bool full_tree = leaf <= 10 && uint64_t(runs) == (uint64_t{1} << (3 * leaf));
+  if (full_tree) {  // every level full: one launch (k_full_levels) instead of the general path
+    FullLevels f{};
+    f.leaf = leaf;
+    f.start[0] = 0;
+    for (int v = 0; v <= leaf; ++v) {
+      const uint64_t nv = uint64_t{1} << (3 * v);
+      f.start[v + 1] = f.start[v] + nv;
+      Level& V = c->lv[v];
+      V.n = static_cast<uint32_t>(nv);
+      if (v < leaf) {
+        V.code = dalloc<uint64_t>(c, nv, s);
+        V.first_child = dalloc<uint32_t>(c, nv, s);
+        V.child_count = dalloc<uint32_t>(c, nv, s);
+        V.parent = dalloc<uint32_t>(c, nv, s);
+        V.first_particle = dalloc<uint32_t>(c, nv, s);
+        V.particle_count = dalloc<uint32_t>(c, nv, s);
+        FMM_CUDA(cudaMemsetAsync(V.first_particle, 0, 4 * nv, s));
+        FMM_CUDA(cudaMemsetAsync(V.particle_count, 0, 4 * nv, s));
+      }
+      if (v >= 2) {
+        V.cls_cells = dalloc<uint32_t>(c, nv, s);
+        for (int q = 0; q <= 8; ++q) V.cls_off[q] = static_cast<uint32_t>(q * (nv >> 3));
+      }
+      f.code[v] = V.code;
+      f.first_child[v] = V.first_child;
+      f.child_count[v] = V.child_count;
+      f.parent[v] = V.parent;
+      f.cls_cells[v] = V.cls_cells;
+    }
+    k_full_levels<<<blocks(f.start[leaf + 1], 256), 256, 0, s>>>(f);
+    FMM_CUDA(cudaGetLastError());
+    dfree(c, idx, s);
+    dfree(c, d_runs, s);
+  } else {
   // parent levels (geometry.cpp:138-153), on the device only
   const uint32_t R = runs;
   uint32_t* d_counts = dalloc<uint32_t>(c, 22, s);
@@ -628,6 +691,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   dfree(c, d_counts, s);
   dfree(c, idx, s);
   dfree(c, d_runs, s);
+  }  // general (not full) tree
 
   trace("parent levels");
   // blocks of group_size cells (geometry.cpp:155-160); lookup maps; parity classes;
@@ -646,7 +710,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
       k_fill_u32<<<blocks(cap, 256), 256, 0, s>>>(V.map, cap, NPOS);
       k_scatter_map<<<blocks(V.n, 256), 256, 0, s>>>(V.code, V.n, V.map);
     }
-    if (v >= 2) {
+    if (v >= 2 && !full_tree) {
       uint8_t* oct = dalloc<uint8_t>(c, V.n, s);
       uint8_t* oct_sorted = dalloc<uint8_t>(c, V.n, s);
       uint32_t* iota = dalloc<uint32_t>(c, V.n, s);
@@ -680,7 +744,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
 
   k_copy_words<<<1, 32, 0, s>>>(reinterpret_cast<const uint32_t*>(c->d_flag), 1, d_offs + 9 * height);
   const uint32_t* h_offs = static_cast<const uint32_t*>(readback(c, d_offs, (9 * height + 1) * sizeof(uint32_t), s));
-  for (int v = 2; v < height; ++v) std::memcpy(c->lv[v].cls_off, h_offs + 9 * v, 9 * sizeof(uint32_t));
+  if (!full_tree)
+    for (int v = 2; v < height; ++v) std::memcpy(c->lv[v].cls_off, h_offs + 9 * v, 9 * sizeof(uint32_t));
   int flag = static_cast<int>(h_offs[9 * height]);
   if (dist) flag = dist->flag & 1;  // every rank's key step, OR-ed by the caller
   if ((flag & 4) && !(flag & 3)) {  // a leaf above 64 particles: the sorted fine-key check

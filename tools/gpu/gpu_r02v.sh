@@ -1,7 +1,7 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"
 O=gpurun_out/r02v; mkdir -p $O
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/tree_launches.csv python tools/scratch/profile_tree.py > $O/tree.out 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/tree_launches.csv python tools/scratch/profile_tree.py > $O/tree.out 2>&1
 python - <<'PY' > $O/tree_launches.txt
 import csv
 rows=list(csv.reader(open("gpurun_out/r02v/tree_launches.csv")))

@@ -89,6 +89,71 @@ __global__ void k_keys(const double4* __restrict__ p, uint64_t n, double lo0, do
   idx[i] = static_cast<uint32_t>(i);
 }
 
+// Root cube and key geometry on the device, so the keys need no host round trip: the
+// reduction of the min / max partials and bounding_cube's arithmetic (geometry.cpp:28-34)
+// in explicit round-to-nearest operations, bit-identical to root_from_bounds on the host;
+// the host reads the result back together with the leaf count.
+struct TreeGeo {
+  double root[4];
+  double lo[3], hi[3];
+  double cw;
+  uint32_t runs, pad;
+};
+__global__ void k_root_geo(const double* __restrict__ part, int nb, int given, double r0, double r1, double r2,
+                           double r3, uint32_t grid, TreeGeo* __restrict__ g) {
+  __shared__ double red[6][32];
+  const int a6 = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp a6 < 6 reduces one bound
+  if (!given && a6 < 6) {
+    double v = a6 < 3 ? INFINITY : -INFINITY;
+    for (int b = lane; b < nb; b += 32) v = a6 < 3 ? fmin(v, part[a6 * nb + b]) : fmax(v, part[a6 * nb + b]);
+    for (int o = 16; o > 0; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = a6 < 3 ? fmin(v, w) : fmax(v, w);
+    }
+    red[a6][lane] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double root[4];
+  if (given) {
+    root[0] = r0; root[1] = r1; root[2] = r2; root[3] = r3;
+  } else {
+    double extent = 0;
+    for (int a = 0; a < 3; ++a) {
+      const double lo = red[a][0], hi = red[3 + a][0];
+      root[a] = __dmul_rn(0.5, __dadd_rn(lo, hi));
+      extent = fmax(extent, __dsub_rn(hi, lo));
+    }
+    root[3] = extent > 0 ? __dmul_rn(extent, 1.0 + 1e-6) : 1.0;
+  }
+  for (int a = 0; a < 4; ++a) g->root[a] = root[a];
+  for (int a = 0; a < 3; ++a) {
+    g->lo[a] = __dsub_rn(root[a], __dmul_rn(0.5, root[3]));
+    g->hi[a] = __dadd_rn(g->lo[a], root[3]);
+  }
+  g->cw = __ddiv_rn(root[3], static_cast<double>(grid));
+}
+template <typename K>
+__global__ void k_keys_geo(const double4* __restrict__ p, uint64_t n, const TreeGeo* __restrict__ g, uint32_t grid,
+                           K* __restrict__ keys, uint32_t* __restrict__ idx, int* __restrict__ flag) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double4 q = p[i];
+  const double c[3] = {q.x, q.y, q.z};
+  const double cw = g->cw;
+  uint32_t ijk[3];
+  for (int a = 0; a < 3; ++a) {
+    const double lo = g->lo[a], hi = g->hi[a];
+    if (c[a] < lo || c[a] > hi) atomicOr(flag, 1);  // domain_error
+    double u = floor(__ddiv_rn(__dsub_rn(c[a], lo), cw));
+    if (u < 0) u = 0;
+    if (u >= grid) u = grid - 1;
+    ijk[a] = static_cast<uint32_t>(u);
+  }
+  keys[i] = static_cast<K>(morton(ijk[0], ijk[1], ijk[2]));
+  idx[i] = static_cast<uint32_t>(i);
+}
+
 __global__ void k_permute(const double4* __restrict__ in, const uint32_t* __restrict__ idx, uint64_t n,
                           double4* __restrict__ out, uint32_t* __restrict__ inv) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -487,28 +552,26 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     FMM_CUDA(cudaMemcpyAsync(c->d_in, xyzw, n * sizeof(double4), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   FMM_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
 
-  // root cube
-  double root[4];
-  if (root4) {
-    std::copy(root4, root4 + 4, root);
-  } else {
-    double lohi[6];
-    device_bounds(c, c->d_in, n, lohi, s);
-    root_from_bounds(lohi, lohi + 3, root);
-  }
-  trace("root cube");
-  std::copy(root, root + 4, c->root);
+  // root cube and key geometry, on the device (read back with the leaf count below)
   c->n = n;
   c->height = height;
   c->group = group;
   const int leaf = height - 1;
   const uint32_t grid = 1u << leaf;
-  const double cw = root[3] / static_cast<double>(grid);
-  double hib[3];
-  for (int a = 0; a < 3; ++a) {
-    c->lo[a] = root[a] - 0.5 * root[3];
-    hib[a] = c->lo[a] + root[3];
+  double* geo_mem = dalloc<double>(c, sizeof(TreeGeo) / sizeof(double), s);
+  TreeGeo* geo = reinterpret_cast<TreeGeo*>(geo_mem);
+  {
+    const int nb = root4 ? 1 : static_cast<int>(std::min<uint64_t>(1184, blocks(n, 256)));
+    double* part = static_cast<double*>(scratch(c, sizeof(double) * 6 * nb));
+    if (!root4) {
+      k_minmax_partial<<<nb, 256, 0, s>>>(c->d_in, n, part);
+      FMM_CUDA(cudaGetLastError());
+    }
+    k_root_geo<<<1, 256, 0, s>>>(part, nb, root4 ? 1 : 0, root4 ? root4[0] : 0, root4 ? root4[1] : 0,
+                                 root4 ? root4[2] : 0, root4 ? root4[3] : 0, grid, geo);
+    FMM_CUDA(cudaGetLastError());
   }
+  trace("root cube");
 
   // keys + stable radix sort of (key, input index); leaf cells = runs of equal keys
   // (geometry.cpp:113-122)
@@ -516,7 +579,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   uint32_t* idx = dalloc<uint32_t>(c, n, s);
   c->lv.resize(height);
   Level& L = c->lv[leaf];
-  uint32_t* d_runs = dalloc<uint32_t>(c, 1, s);
+  uint32_t* d_runs = &geo->runs;
   L.code = dalloc<uint64_t>(c, n, s);
   L.particle_count = dalloc<uint32_t>(c, n, s);
   size_t tb = 0;
@@ -524,8 +587,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     if (dist) {
       k_iota<<<blocks(n, 256), 256, 0, s>>>(idx, n);
     } else {
-      k_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, c->lo[0], c->lo[1], c->lo[2], hib[0], hib[1], hib[2], cw,
-                                             grid, keys, idx, c->d_flag);
+      k_keys_geo<<<blocks(n, 256), 256, 0, s>>>(c->d_in, n, geo, grid, keys, idx, c->d_flag);
     }
     FMM_CUDA(cudaGetLastError());
     trace("keys");
@@ -567,7 +629,13 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     dfree(c, k64s, s);
   }
   uint32_t runs = 0;
-  runs = *static_cast<const uint32_t*>(readback(c, d_runs, 4, s));
+  {  // the one readback before the level arrays: leaf count, root cube, key geometry
+    TreeGeo hg;
+    std::memcpy(&hg, readback(c, geo, sizeof(TreeGeo), s), sizeof(TreeGeo));
+    runs = hg.runs;
+    std::copy(hg.root, hg.root + 4, c->root);
+    std::copy(hg.lo, hg.lo + 3, c->lo);
+  }
   L.n = runs;
   L.first_particle = dalloc<uint32_t>(c, runs, s);
   FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, L.particle_count, L.first_particle, static_cast<int>(runs), s));
@@ -585,7 +653,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     uint64_t* fks = dalloc<uint64_t>(c, n, s);
     uint32_t* fi = dalloc<uint32_t>(c, n, s);
     uint32_t* fis = dalloc<uint32_t>(c, n, s);
-    k_fine_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_pw, n, c->lo[0], c->lo[1], c->lo[2], root[3] / 2097152.0, fk, fi);
+    k_fine_keys<<<blocks(n, 256), 256, 0, s>>>(c->d_pw, n, c->lo[0], c->lo[1], c->lo[2], c->root[3] / 2097152.0, fk,
+                                                fi);
     FMM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, fk, fks, fi, fis, static_cast<int>(n), 0, 63, s));
     FMM_CUDA(cub::DeviceRadixSort::SortPairs(scratch(c, tb), tb, fk, fks, fi, fis, static_cast<int>(n), 0, 63, s));
     k_equal_key_runs<<<blocks(n, 256), 256, 0, s>>>(fks, fis, n, c->d_pw, c->d_flag);
@@ -644,7 +713,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
     k_full_levels<<<blocks(f.start[leaf + 1], 256), 256, 0, s>>>(f);
     FMM_CUDA(cudaGetLastError());
     dfree(c, idx, s);
-    dfree(c, d_runs, s);
+    dfree(c, geo_mem, s);
   } else {
   // parent levels (geometry.cpp:138-153), on the device only
   const uint32_t R = runs;
@@ -690,7 +759,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   }
   dfree(c, d_counts, s);
   dfree(c, idx, s);
-  dfree(c, d_runs, s);
+  dfree(c, geo_mem, s);
   }  // general (not full) tree
 
   trace("parent levels");

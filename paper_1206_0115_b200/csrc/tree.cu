@@ -179,7 +179,7 @@ __global__ void k_inverse(const uint32_t* __restrict__ id, uint64_t n, uint32_t*
 // (geometry.cpp:126-136: equal positions inside one leaf -> domain_error).
 __global__ void k_leaf_scan(const uint32_t* __restrict__ first, const uint32_t* __restrict__ count, uint32_t ncells,
                             const double4* __restrict__ pw, uint32_t* __restrict__ pcell, int* __restrict__ flag,
-                            uint32_t cell0 = 0) {
+                            uint32_t cell0, uint32_t* __restrict__ big, uint32_t big_cap) {
   __shared__ double xs[8][64];  // x of the leaf's particles (leaves of <= 64), per warp
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -210,9 +210,45 @@ __global__ void k_leaf_scan(const uint32_t* __restrict__ first, const uint32_t* 
     }
     return;
   }
-  // a leaf of more than 64 particles: checked afterwards by the sorted fine-key pass
-  // (one warp would need O(m^2 / 32) steps for it)
-  if (lane == 0) atomicOr(flag, 4);
+  // a leaf of more than 64 particles: listed for k_leaf_scan_big (one CTA per leaf); the
+  // list order does not matter (the check is an OR). Overflow -> the sorted fine-key pass.
+  if (lane == 0) {
+    const uint32_t k = atomicAdd(big, 1u);
+    if (k < big_cap) big[1 + k] = warp;
+    else atomicOr(flag, 4);
+  }
+}
+
+// The listed leaves of 65..LS_BIG particles, one CTA (256 threads) per leaf: x staged in
+// shared memory, thread a compares its particle with every later one (x by broadcast-ish
+// reads, y and z only for equal x). At config B a uniform cloud has ~20 such leaves (a
+// Poisson tail above 64 around a mean of 38), which used to send all 10M particles
+// through the sorted fine-key check (1.1 ms); leaves above LS_BIG still take that path.
+constexpr uint32_t LS_BIG = 4096;
+__global__ void __launch_bounds__(256) k_leaf_scan_big(const uint32_t* __restrict__ first,
+                                                       const uint32_t* __restrict__ count,
+                                                       const uint32_t* __restrict__ big, uint32_t big_cap,
+                                                       const double4* __restrict__ pw, int* __restrict__ flag) {
+  __shared__ double xs[LS_BIG];
+  const uint32_t nbig = min(big[0], big_cap);
+  for (uint32_t e = blockIdx.x; e < nbig; e += gridDim.x) {
+    const uint32_t c = big[1 + e], f = first[c], m = count[c];
+    if (m > LS_BIG) {
+      if (threadIdx.x == 0) atomicOr(flag, 4);
+      continue;
+    }
+    __syncthreads();
+    for (uint32_t a = threadIdx.x; a < m; a += blockDim.x) xs[a] = pw[f + a].x;
+    __syncthreads();
+    for (uint32_t a = threadIdx.x; a < m; a += blockDim.x) {
+      const double xa = xs[a];
+      for (uint32_t b = a + 1; b < m; ++b)
+        if (xs[b] == xa) {
+          const double4 pa = pw[f + a], pb = pw[f + b];
+          if (pa.y == pb.y && pa.z == pb.z) atomicOr(flag, 2);
+        }
+    }
+  }
 }
 
 // Large leaves (mean > 64 particles, e.g. config D's surface cloud, or any leaf above 64
@@ -670,8 +706,13 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   } else if (n <= 64ull * runs) {
     // small leaves on average; a leaf above 64 raises flag bit 4 and the sorted check
     // runs after the readback below (clustered inputs)
+    uint32_t* big = dalloc<uint32_t>(c, 1 + 65536, s);
+    FMM_CUDA(cudaMemsetAsync(big, 0, 4, s));
     k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs, c->d_pw,
-                                                                 c->d_pcell, c->d_flag);
+                                                                 c->d_pcell, c->d_flag, 0, big, 65536);
+    FMM_CUDA(cudaGetLastError());
+    k_leaf_scan_big<<<296, 256, 0, s>>>(L.first_particle, L.particle_count, big, 65536, c->d_pw, c->d_flag);
+    dfree(c, big, s);
     FMM_CUDA(cudaGetLastError());
   } else {
     k_leaf_cells<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle, L.particle_count, runs,
@@ -853,8 +894,14 @@ int coincident_check(fmmgpu_ctx* c, uint32_t c0, uint32_t c1, cudaStream_t s) {
   FMM_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), s));
   bool fine = m > 64ull * runs;
   if (!fine) {
+    uint32_t* big = dalloc<uint32_t>(c, 1 + 65536, s);
+    FMM_CUDA(cudaMemsetAsync(big, 0, 4, s));
     k_leaf_scan<<<blocks(uint64_t(runs) * 32, 256), 256, 0, s>>>(L.first_particle + c0, L.particle_count + c0, runs,
-                                                                 c->d_pw, nullptr, c->d_flag);
+                                                                 c->d_pw, nullptr, c->d_flag, 0, big, 65536);
+    FMM_CUDA(cudaGetLastError());
+    k_leaf_scan_big<<<296, 256, 0, s>>>(L.first_particle + c0, L.particle_count + c0, big, 65536, c->d_pw,
+                                        c->d_flag);
+    dfree(c, big, s);
     FMM_CUDA(cudaGetLastError());
     const int f = *static_cast<const int*>(readback(c, c->d_flag, sizeof(int), s));
     if (f & 2) return f;

@@ -497,15 +497,16 @@ def test_coincident_check_small_leaves(fmm):
     c.build_tree(same_x, 4)  # a failed build leaves the context usable
 
 
-def test_coincident_check_clustered_leaf(fmm):
-    """a clustered input with small leaves on average but one leaf of ~2000
-    particles goes through the sorted fine-key check (k_leaf_scan flags leaves above 64)
-    instead of a one-warp O(m^2) loop: a duplicate inside the big leaf is a domain error,
-    the same cloud without it builds the reference's tree."""
+@pytest.mark.parametrize("cluster", [100, 2000, 6000])
+def test_coincident_check_clustered_leaf(fmm, cluster):
+    """a clustered input with small leaves on average but one big leaf: leaves
+    of 65..4096 particles are checked by one CTA each (k_leaf_scan_big), larger ones by the
+    sorted fine-key pass, never by a one-warp O(m^2) loop. A duplicate inside the big leaf
+    is a domain error; the same cloud without it builds the reference's tree."""
     P = fmm
     base = make_particles(20000, "uniform", 31, False)
     rng = np.random.default_rng(31)
-    base[:2000, :3] = 0.3 + 0.01 * rng.random((2000, 3))  # one leaf at height 4
+    base[:cluster, :3] = 0.3 + 0.01 * rng.random((cluster, 3))  # one leaf at height 4
     c = P.FmmContext(None, order=3)
     c.build_tree(base, 4)
     ot = OracleTree(base, 4)
@@ -513,9 +514,9 @@ def test_coincident_check_clustered_leaf(fmm):
     oc, _ = ot.level(3)
     gc["_pad"] = 0
     oc["_pad"] = 0
-    assert np.array_equal(gc, oc) and gc["particle_count"].max() >= 2000
+    assert np.array_equal(gc, oc) and gc["particle_count"].max() >= cluster
     dup = base.copy()
-    dup[1500, :3] = dup[7, :3]
+    dup[cluster - 5, :3] = dup[7, :3]
     with pytest.raises(P.DomainError):
         c.build_tree(dup, 4)
     c.build_tree(base, 4)

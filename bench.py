@@ -390,6 +390,18 @@ def run_ours(args, world, rank, local):
         byts = sum(8 * l3 * (cells[v + 1] + 2 * cells[v]) for v in range(2, leaf))
         per_op[k]["hbm_gbs"] = byts / (iso[k] / 1e3) / 1e9
         per_op[k]["hbm_frac"] = per_op[k]["hbm_gbs"] / hbm
+    # executed FP64 flops per operator (ncu DFMA / DADD / DMUL / DMMA counters of one
+    # evaluation, tools/fp64_ops.py -> profiles/fp64_ops.json): the utilisation beside the
+    # ledger fraction (the factored P2M / L2P kernels execute fewer flops than the ledger
+    # counts, M2L's DMMA executes padding rows)
+    fo = os.path.join(ROOT, "profiles", "fp64_ops.json")
+    if os.path.exists(fo):
+        ops = json.load(open(fo)).get(args.config, {})
+        for k, v in per_op.items():
+            if k in ops and ops[k].get("exec_flops"):
+                ef = ops[k]["exec_flops"]
+                v["exec_flops"] = ef
+                v["exec_frac"] = ef / (v["ms_isolated"] / 1e3) / 1e12 / v["peak_tflops"]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):

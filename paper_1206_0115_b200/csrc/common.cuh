@@ -157,6 +157,8 @@ struct M2LTables {
   int4* dRowA = nullptr;    // [8][rowsA]: {slot or -1, destination column in Yt, vector index in its M-tile, 0}
   int* dTileVec = nullptr;  // [8][rowsA/64][vtMax]: vector slots of each 64-row M-tile (-1 = none)
   int vtMax = 0;            // max distinct vectors in one 64-row M-tile
+  int* dTileVec2 = nullptr; // the same for the 128-row tiles of the streamed phase A (rowA.w)
+  int vtMax2 = 0;
   int* dKslot = nullptr;    // [8][ldY]: vector slot of column kk of the target stack, -1 = pad
 };
 

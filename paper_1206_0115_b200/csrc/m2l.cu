@@ -229,6 +229,8 @@ struct GemmArgs {
   int rowsA;
   const int* kslot;       // vector slot per target-stack column [8][ldY] (host tables)
   double* local;          // phase B output (local_own)
+  const int* tileVec2;    // streamed phase A: vector slots per 128-row tile [8][rowsA/128][vtMax2]
+  int vtMax2;
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
   int rowB0;              // phase B: first row of this launch's M-tiles (tail launches)
   int msplit;             // phase A M-split factor (coarse levels)
@@ -523,6 +525,116 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) k_m2l_phase_a(const GemmAr
   cp_wait<0>();
 }
 
+// Phase A, streamed (phase B's GEMM structure with phase A's scatter epilogue): a BM x BN
+// tile of Y = M1_p (rows) x W (source columns), BOTH operands streamed in BK-wide k-slices
+// through a cp.async ring, so each operator slice feeds BN = 64 columns even at l = 7
+// (the W-resident kernel holds 24 there). The epilogue resolves one target per (vector of
+// the tile, column) from a table filled before the main loop.
+template <int BM, int BN, int WM, int WN, int STAGES, int BK>
+__global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_a2(const GemmArgs g) {
+  constexpr int T = WM * WN * 32;
+  constexpr int WTM = BM / WM, WTN = BN / WN;
+  constexpr int MT = WTM / 8, NT = WTN / 8;
+  constexpr int SPAD = BK + 4;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                      // [STAGES][BM][SPAD]
+  double* Bs = smem + STAGES * BM * SPAD;  // [STAGES][BN][SPAD]
+  uint32_t* tgt = reinterpret_cast<uint32_t*>(Bs + STAGES * BN * SPAD);  // [vtMax2][BN]
+  __shared__ uint32_t col_cell[BN];
+
+  const int cls = blockIdx.z;
+  const uint32_t ncls = g.cls_off[cls + 1] - g.cls_off[cls];
+  const uint32_t n0 = blockIdx.y * BN;
+  if (n0 >= ncls) return;
+  const int mt = blockIdx.x, m0 = mt * BM;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / WN, wn = warp % WN;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  for (int j = tid; j < BN; j += T) col_cell[j] = (n0 + j < ncls) ? g.cls_cells[g.cls_off[cls] + n0 + j] : NPOS;
+  __syncthreads();
+
+  const double* A = g.A + cls * g.a_class_stride + size_t(m0) * g.lda;
+  const int KT = g.K / BK;
+  auto load_tile = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * BM * SPAD;
+    double* bs = Bs + stage * BN * SPAD;
+    for (int ch = tid; ch < BM * (BK / 2); ch += T) {
+      const int r = ch / (BK / 2), q = (ch % (BK / 2)) * 2;
+      cp16(as + r * SPAD + q, A + size_t(r) * g.lda + k0 + q);
+    }
+    for (int ch = tid; ch < BN * (BK / 2); ch += T) {
+      const int j = ch / (BK / 2), q = (ch % (BK / 2)) * 2;
+      const uint32_t cell = col_cell[j];
+      const bool ok = cell != NPOS;
+      cp16z(bs + j * SPAD + q, g.W + (ok ? size_t(cell) * g.ldE + k0 + q : 0), ok);
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < KT) load_tile(st, st);
+    cp_commit();
+  }
+  // target of (vector of this tile, column): source - v, while the first slices load
+  const int* vec = g.tileVec2 + (size_t(cls) * (g.rowsA / BM) + mt) * g.vtMax2;
+  for (int e = tid; e < g.vtMax2 * BN; e += T) {
+    const int j = e % BN, slot = __ldg(vec + e / BN);
+    uint32_t tc = NPOS;
+    const uint32_t cell = col_cell[j];
+    if (slot >= 0 && cell != NPOS) {
+      int ijk[3];
+      demorton(g.lv.code[cell], ijk);
+      tc = find_ijk(g.lv, ijk[0] - (slot / 49 - 3), ijk[1] - ((slot / 7) % 7 - 3), ijk[2] - (slot % 7 - 3));
+    }
+    tgt[e] = tc;
+  }
+  int4 rowinfo[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) rowinfo[i] = __ldg(g.rowA + cls * g.rowsA + m0 + wm * WTM + i * 8 + gq);
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int pf = kt + STAGES - 1;
+    if (pf < KT) load_tile(pf % STAGES, pf);
+    cp_commit();
+    const double* as = As + (kt % STAGES) * BM * SPAD + (wm * WTM + gq) * SPAD + tq;
+    const double* bs = Bs + (kt % STAGES) * BN * SPAD + (wn * WTN + gq) * SPAD + tq;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[MT], b[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[i] = as[i * 8 * SPAD + kk];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = bs[j * 8 * SPAD + kk];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_wait<0>();
+  // scatter block v of source s to target s - v (target-side column rowinfo.y)
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    if (rowinfo[i].x < 0) continue;
+    const uint32_t* trow = tgt + rowinfo[i].w * BN;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint32_t tcell = trow[wn * WTN + j * 8 + 2 * tq + e];
+        if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + rowinfo[i].y] = acc[i][j][e];
+      }
+  }
+}
+
 constexpr int B_BM = 128, B_BN = 64, B_WM = 4, B_WN = 2, B_ST = 2, B_BK = 32;
 
 }  // namespace
@@ -534,6 +646,8 @@ void m2l_free(fmmgpu_ctx* c) {
   if (T.dRowA) cudaFree(T.dRowA);
   if (T.dTileVec) cudaFree(T.dTileVec);
   T.dTileVec = nullptr;
+  if (T.dTileVec2) cudaFree(T.dTileVec2);
+  T.dTileVec2 = nullptr;
   if (T.dKslot) cudaFree(T.dKslot);
   T.dM1 = T.dM2 = nullptr;
   T.dRowA = nullptr;
@@ -596,7 +710,7 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   // 27.78 ms per evaluation. Measured at the config-B leaf (phase A + B): 128 x 64 / 2 stages 15.9 ms,
   // 128 x 32 / 3 stages 12.6 ms, vs 11.9 ms for 64 x 64 / 4 stages.
   T.bmA = c->ldE <= 128 ? 64 : 128;
-  T.rowsA = round_up(R, T.bmA);
+  T.rowsA = round_up(R, 128);  // whole 64- and 128-row tiles (2432 at l = 5, as round_up(R, 64))
   T.rowsB = round_up(n3, B_BM);
   std::vector<double> M1(size_t(8) * T.rowsA * c->ldE, 0.0), M2(size_t(8) * T.rowsB * T.ldY, 0.0);
   std::vector<int4> rowA(size_t(8) * T.rowsA, make_int4(-1, 0, 0, 0));
@@ -657,6 +771,26 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
       }
       T.vtMax = std::max<int>(T.vtMax, static_cast<int>(list.size()));
     }
+  {  // 128-row tiles of the streamed phase A: vector index in rowA.w
+    const int mt2 = T.rowsA / 128;
+    T.vtMax2 = 1;
+    std::vector<std::vector<int>> tv2(size_t(8) * mt2);
+    for (int p = 0; p < 8; ++p)
+      for (int mt = 0; mt < mt2; ++mt) {
+        auto& list = tv2[size_t(p) * mt2 + mt];
+        for (int r = 0; r < 128; ++r) {
+          int4& e = rowA[size_t(p) * T.rowsA + mt * 128 + r];
+          if (e.x < 0) continue;
+          if (list.empty() || list.back() != e.x) list.push_back(e.x);
+          e.w = static_cast<int>(list.size()) - 1;
+        }
+        T.vtMax2 = std::max<int>(T.vtMax2, static_cast<int>(list.size()));
+      }
+    std::vector<int> tileVec2(size_t(8) * mt2 * T.vtMax2, -1);
+    for (size_t i = 0; i < tv2.size(); ++i) std::copy(tv2[i].begin(), tv2[i].end(), tileVec2.begin() + i * T.vtMax2);
+    FMM_CUDA(cudaMalloc(&T.dTileVec2, tileVec2.size() * sizeof(int)));
+    FMM_CUDA(cudaMemcpy(T.dTileVec2, tileVec2.data(), tileVec2.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
   std::vector<int> tileVec(size_t(8) * mtiles * T.vtMax, -1);
   for (size_t i = 0; i < tv.size(); ++i)
     std::copy(tv[i].begin(), tv[i].end(), tileVec.begin() + i * T.vtMax);
@@ -700,6 +834,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   g.rowA = T.dRowA;
   g.tileVec = T.dTileVec;
   g.vtMax = T.vtMax;
+  g.tileVec2 = T.dTileVec2;
+  g.vtMax2 = T.vtMax2;
   g.rowsA = T.rowsA;
   g.kslot = T.dKslot;
   g.local = L.local_own;
@@ -746,7 +882,21 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     // Also measured (tools/gpu/gpu_r02o.sh, evaluation ms at config B / C): 64 x 64 with 4
     // warps of 32 x 32 (24.84 vs 24.53), 64 x 32 with 4 warps and 3 CTAs per SM (24.62), the
     // same with a 3-stage ring (25.79); at l = 7, 128 x 32 with one CTA per SM (97.76 vs 88.76).
-    if (T.bmA == 64) launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
+    static const int stream = [] {  // FMMGPU_M2L_PA_STREAM: streamed phase A variant (A/B aid)
+      const char* e = std::getenv("FMMGPU_M2L_PA_STREAM");
+      return e ? std::atoi(e) : 0;
+    }();
+    auto launch2 = [&](auto kern, int st, int bk) {
+      const size_t smem = sizeof(double) * size_t(st) * (128 + 64) * (bk + 4) + sizeof(uint32_t) * T.vtMax2 * 64;
+      FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      dim3 grid(T.rowsA / 128, (maxcls + 63) / 64, 8);
+      kern<<<grid, 256, smem, s>>>(g);
+      FMM_CUDA(cudaGetLastError());
+    };
+    if (stream == 1) launch2(k_m2l_phase_a2<128, 64, 4, 2, 2, 32>, 2, 32);
+    else if (stream == 2) launch2(k_m2l_phase_a2<128, 64, 4, 2, 3, 16>, 3, 16);
+    else if (stream == 3) launch2(k_m2l_phase_a2<128, 64, 4, 2, 2, 16>, 2, 16);
+    else if (T.bmA == 64) launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
     else if (c->ldE <= 352) launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
     else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
   }

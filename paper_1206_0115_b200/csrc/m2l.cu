@@ -886,16 +886,17 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       const char* e = std::getenv("FMMGPU_M2L_PA_STREAM");
       return e ? std::atoi(e) : 0;
     }();
-    auto launch2 = [&](auto kern, int st, int bk) {
-      const size_t smem = sizeof(double) * size_t(st) * (128 + 64) * (bk + 4) + sizeof(uint32_t) * T.vtMax2 * 64;
+    auto launch2 = [&](auto kern, int st, int bk, int bn, int threads) {
+      const size_t smem = sizeof(double) * size_t(st) * (128 + bn) * (bk + 4) + sizeof(uint32_t) * T.vtMax2 * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      dim3 grid(T.rowsA / 128, (maxcls + 63) / 64, 8);
-      kern<<<grid, 256, smem, s>>>(g);
+      dim3 grid(T.rowsA / 128, (maxcls + bn - 1) / bn, 8);
+      kern<<<grid, threads, smem, s>>>(g);
       FMM_CUDA(cudaGetLastError());
     };
-    if (stream == 1) launch2(k_m2l_phase_a2<128, 64, 4, 2, 2, 32>, 2, 32);
-    else if (stream == 2) launch2(k_m2l_phase_a2<128, 64, 4, 2, 3, 16>, 3, 16);
-    else if (stream == 3) launch2(k_m2l_phase_a2<128, 64, 4, 2, 2, 16>, 2, 16);
+    if (stream == 1) launch2(k_m2l_phase_a2<128, 64, 4, 2, 2, 32>, 2, 32, 64, 256);
+    else if (stream == 4) launch2(k_m2l_phase_a2<128, 128, 4, 4, 2, 32>, 2, 32, 128, 512);
+    else if (stream == 5) launch2(k_m2l_phase_a2<128, 64, 4, 2, 3, 32>, 3, 32, 64, 256);
+    else if (stream == 6) launch2(k_m2l_phase_a2<128, 128, 4, 2, 2, 16>, 2, 16, 128, 256);
     else if (T.bmA == 64) launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
     else if (c->ldE <= 352) launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
     else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);

@@ -368,11 +368,10 @@ __global__ void k_m2l_splitk_reduce(const double* __restrict__ part, int ksplit,
 // M1_p (R rows) streams past them in BM x BK slices through a cp.async ring that
 // runs across M-tile boundaries, so the scatter epilogue of one M-tile overlaps the
 // loads of the next and no CTA pays a pipeline ramp per 64 x 64 tile.
-// Tiles: l <= 5: 64-row M-tiles, 2-stage ring of 32-wide k-slices, 64 resident columns
-// (W 68 KB + ring 37 KB);
-// l = 6, 7: 128-row M-tiles, 2 stages, 24 columns (l = 7: W 68 KB + ring 41 KB); larger
-// orders: 128-row M-tiles, 3 stages, 16 columns, so two CTAs still fit on an SM. The
-// epilogue tables are built for the M-tile in use.
+// Used for l <= 5: 64-row M-tiles, 2-stage ring of 32-wide k-slices, 64 resident columns
+// (W 68 KB + ring 37 KB). Above order 5 the multipoles no longer fit 64 per CTA (24 at
+// l = 7), the operator then feeds too few columns per load, and k_m2l_phase_a2 (both
+// operands streamed, 128 x 64 tiles) is used instead.
 template <int PA_BM, int PA_ST, int BN, int WM, int WN, int PA_BK = 16, int MINB = 2>
 __global__ void __launch_bounds__(WM * WN * 32, MINB) k_m2l_phase_a(const GemmArgs g) {
   constexpr int PA_THREADS = WM * WN * 32;
@@ -703,10 +702,10 @@ void m2l_setup(fmmgpu_ctx* c, bool compute) {
   T.R = R;
   T.ldY = round_up(R, 32);
   // 64-row M-tiles x 64 resident columns, 2-stage ring of 32-wide k-slices for l <= 5;
-  // 128 x 24, 2-stage ring of 16-wide slices
-  // for l = 6, 7; 128 x 16, 3 stages above. Config C (l = 7) per evaluation: 128 x 16 / 3
-  // stages 96.9 ms, 64 x 32 / 2 stages 95.8 (16 x 16 warp tiles) or 95.1 (32 x 8), 128 x 24
-  // / 2 stages 94.0. Config B with 128 x 64 / 2 stages (32 x 32 warp tiles): 27.90 vs
+  // streamed 128 x 64 tiles (k_m2l_phase_a2) above. Earlier W-resident shapes at l = 7
+  // (config C per evaluation, before the streamed kernel): 128 x 16 / 3 stages 96.9 ms,
+  // 64 x 32 / 2 stages 95.8 (16 x 16 warp tiles) or 95.1 (32 x 8), 128 x 24 / 2 stages
+  // 94.0. Config B with 128 x 64 / 2 stages (32 x 32 warp tiles): 27.90 vs
   // 27.78 ms per evaluation. Measured at the config-B leaf (phase A + B): 128 x 64 / 2 stages 15.9 ms,
   // 128 x 32 / 3 stages 12.6 ms, vs 11.9 ms for 64 x 64 / 4 stages.
   T.bmA = c->ldE <= 128 ? 64 : 128;
@@ -882,10 +881,10 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     // Also measured (tools/gpu/gpu_r02o.sh, evaluation ms at config B / C): 64 x 64 with 4
     // warps of 32 x 32 (24.84 vs 24.53), 64 x 32 with 4 warps and 3 CTAs per SM (24.62), the
     // same with a 3-stage ring (25.79); at l = 7, 128 x 32 with one CTA per SM (97.76 vs 88.76).
-    static const int stream = [] {  // FMMGPU_M2L_PA_STREAM: streamed phase A variant (A/B aid)
-      const char* e = std::getenv("FMMGPU_M2L_PA_STREAM");
-      return e ? std::atoi(e) : 0;
-    }();
+    // l >= 6: the streamed kernel (config C 87.94 -> 80.21 ms per evaluation, l = 6
+    // 49.06 -> 45.42; at l = 5 it measured slower, 25.30 vs 24.59 ms at B). Streamed
+    // shapes also measured at C: 128 x 128 with 16 warps (84.42), 3-stage ring (88.50),
+    // 128 x 128 with 8 warps and 16-wide slices (86.04).
     auto launch2 = [&](auto kern, int st, int bk, int bn, int threads) {
       const size_t smem = sizeof(double) * size_t(st) * (128 + bn) * (bk + 4) + sizeof(uint32_t) * T.vtMax2 * bn;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -893,13 +892,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
       kern<<<grid, threads, smem, s>>>(g);
       FMM_CUDA(cudaGetLastError());
     };
-    if (stream == 1) launch2(k_m2l_phase_a2<128, 64, 4, 2, 2, 32>, 2, 32, 64, 256);
-    else if (stream == 4) launch2(k_m2l_phase_a2<128, 128, 4, 4, 2, 32>, 2, 32, 128, 512);
-    else if (stream == 5) launch2(k_m2l_phase_a2<128, 64, 4, 2, 3, 32>, 3, 32, 64, 256);
-    else if (stream == 6) launch2(k_m2l_phase_a2<128, 128, 4, 2, 2, 16>, 2, 16, 128, 256);
-    else if (T.bmA == 64) launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
-    else if (c->ldE <= 352) launch(k_m2l_phase_a<128, 2, 24, 8, 1>, 24, 128, 2);
-    else launch(k_m2l_phase_a<128, 3, 16, 8, 1>, 16, 128, 3);
+    if (T.bmA == 64) launch(k_m2l_phase_a<64, 2, 64, 2, 4, 32>, 64, 64, 2, 32);
+    else launch2(k_m2l_phase_a2<128, 64, 4, 2, 2, 32>, 2, 32, 64, 256);
   }
   g.cls_cells = L.tgtB ? L.tgtB : L.cls_cells;
   std::copy(L.tgtB ? L.tgtB_off : L.cls_off, (L.tgtB ? L.tgtB_off : L.cls_off) + 9, g.cls_off);

@@ -634,7 +634,19 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_a2(const GemmArgs g) 
   }
 }
 
-constexpr int B_BM = 128, B_BN = 64, B_WM = 4, B_WN = 2, B_ST = 2, B_BK = 32;
+#ifndef FMMGPU_B_ST
+#define FMMGPU_B_ST 2
+#endif
+#ifndef FMMGPU_B_BK
+#define FMMGPU_B_BK 32
+#endif
+#ifndef FMMGPU_B_BN
+#define FMMGPU_B_BN 64
+#endif
+#ifndef FMMGPU_B_WN
+#define FMMGPU_B_WN 2
+#endif
+constexpr int B_BM = 128, B_BN = FMMGPU_B_BN, B_WM = 4, B_WN = FMMGPU_B_WN, B_ST = FMMGPU_B_ST, B_BK = FMMGPU_B_BK;
 
 }  // namespace
 

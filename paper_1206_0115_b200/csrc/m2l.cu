@@ -634,19 +634,11 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_a2(const GemmArgs g) 
   }
 }
 
-#ifndef FMMGPU_B_ST
-#define FMMGPU_B_ST 2
-#endif
-#ifndef FMMGPU_B_BK
-#define FMMGPU_B_BK 32
-#endif
-#ifndef FMMGPU_B_BN
-#define FMMGPU_B_BN 64
-#endif
-#ifndef FMMGPU_B_WN
-#define FMMGPU_B_WN 2
-#endif
-constexpr int B_BM = 128, B_BN = FMMGPU_B_BN, B_WM = 4, B_WN = FMMGPU_B_WN, B_ST = FMMGPU_B_ST, B_BK = FMMGPU_B_BK;
+// Phase B tiles. Measured (evaluation ms at B / C, tools/gpu/gpu_r02ac.sh): 3-stage ring of
+// 16-wide slices 24.81 / 81.20, 2-stage 16-wide 24.80 / 80.86, 128 x 128 tiles with 8 warps
+// 25.04 / 81.24 (16-wide slices 25.25 / 82.44), against 24.60 / 80.28 for 128 x 64, 2-stage
+// 32-wide slices.
+constexpr int B_BM = 128, B_BN = 64, B_WM = 4, B_WN = 2, B_ST = 2, B_BK = 32;
 
 }  // namespace
 

@@ -1,12 +1,13 @@
 """Projected 1/2/4/8-GPU strong scaling of config B (and E) from one B200.
 
-Every rank of the multi-GPU path (csrc/partition.cu) builds the whole
-tree and evaluates only its owned Morton range of leaves; the exchange after each
-upward level is the library's plan (all-gather at the alignment level when needed,
-per-peer halo below). Without 8 GPUs, this times each rank's partitioned evaluation on
-the one device (fmmgpu_set_measurement: the exchange is skipped and the fields are
-refused) and adds the exchange volume the rank receives at an assumed NVLink rate.
-Projection = max over ranks; it is an estimate, not a measurement of the multi-GPU run.
+Every rank of the multi-GPU path (csrc/partition.cu, csrc/dist.cu) holds the
+same tree (built from all-gathered keys) and evaluates only its owned Morton range of
+leaves; the exchange after each upward level is the library's plan (all-gather at the
+alignment level when needed, per-peer halo below). Without 8 GPUs, this times each rank's
+partitioned evaluation on the one device (fmmgpu_set_measurement: the exchange is skipped
+and the fields are refused) and adds the exchange volume the rank receives at an assumed
+NVLink rate. Projection = max over ranks; it is an estimate, not a measurement of the
+multi-GPU run. tree_build_ms_per_rank is the single-device build of the whole set.
 
     python tools/scaling_projection.py [config] > profiles/r01_scaling_projection.json
 """

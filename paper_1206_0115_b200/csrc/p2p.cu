@@ -739,7 +739,10 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
       kern<<<grid, MU_WARPS * 32, smem, s>>>(a);
     };
     if (L.full) go(k_p2p_mutual<64>, static_cast<int>(MU_WARPS * sizeof(MuWarp<64>)));
-    else go(k_p2p_mutual<128>, static_cast<int>(MU_WARPS * sizeof(MuWarp<128>)));
+#ifndef FMMGPU_MU_TCAP_SPARSE
+#define FMMGPU_MU_TCAP_SPARSE 128
+#endif
+    else go(k_p2p_mutual<FMMGPU_MU_TCAP_SPARSE>, static_cast<int>(MU_WARPS * sizeof(MuWarp<FMMGPU_MU_TCAP_SPARSE>)));
     FMM_CUDA(cudaGetLastError());
     const uint64_t dthreads = uint64_t(nl) * 32;
     k_p2p_drain<<<static_cast<unsigned>((dthreads + 255) / 256), 256, 0, s>>>(a);

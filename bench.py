@@ -308,6 +308,15 @@ def run_ours(args, world, rank, local):
     ms_step = max_over_ranks(total_ms / args.steps, world)
     value = n / (ms_step / 1e3) / 1e6  # the whole job: N particles evaluated across all ranks
 
+    # isolated per-operator device times (each operator alone, CUDA events on its
+    # stream, 5 repetitions), taken right after the timed evaluations: the roofline
+    # numerators' denominators. The P2P kernel is the largest single kernel; its share of
+    # the step is reported beside it.
+    iso = {k: ctx.time_operator(k, -1, 5) for k in ("P2M", "M2M", "M2L", "L2L", "L2P", "P2P")}
+    iso_m2l_leaf = ctx.time_operator("M2L", h - 1, 5)
+    ctx.evaluate()
+    ctx.synchronize()
+
     # e2e through the C ABI with pinned host buffers, every step: H2D + tree + eval + D2H.
     # N = 1: the pipelined entry point (fmmgpu_run_async), two pinned input sets and two
     # pinned output sets used alternately, so step k's H2D and step k-1's D2H run on the
@@ -367,15 +376,8 @@ def run_ours(args, world, rank, local):
            "ms_per_step": e2e_s * 1e3, "steps": ksteps, "path": path,
            "serial_fmmgpu_run": {"value": n / e2e_serial_s / 1e6, "ms_per_step": e2e_serial_s * 1e3}}
 
-    # isolated per-operator device times (each operator alone, CUDA events on its
-    # stream): the roofline numerators' denominators. The P2P kernel is the largest
-    # single kernel; its share of the step is reported beside it.
     flops = ledger["flops"]
-    iso = {k: ctx.time_operator(k, -1, 3) for k in ("P2M", "M2M", "M2L", "L2L", "L2P", "P2P")}
     leaf = h - 1
-    iso_m2l_leaf = ctx.time_operator("M2L", leaf, 3)
-    ctx.evaluate()
-    ctx.synchronize()
     peaks = {"P2M": FP64_DFMA_TFLOPS, "M2M": FP64_DFMA_TFLOPS, "M2L": FP64_DMMA_TFLOPS, "L2L": FP64_DFMA_TFLOPS,
              "L2P": FP64_DFMA_TFLOPS, "P2P": FP64_DFMA_TFLOPS}
     per_op = {}

@@ -351,8 +351,8 @@ struct MuArgs {
   int ow;             // evaluation: write near instead of adding
 };
 
-// per-warp shared memory; TCAP = targets per chunk (64 on full leaf levels, 128 else:
-// config D 192 -> 163 ms with 128 and the largest-first order). Measured alternative for
+// per-warp shared memory; TCAP = targets per chunk (64 on full leaf levels, 256 else:
+// config D 192 -> 163 ms with 128 and the largest-first order, 162.5 with 256). Measured alternative for
 // big leaves (config D, ~570 particles): the full 32-lane ring with 4 targets per lane
 // in registers and sources rotating (no combine; tools/microbench "ring T=4 lds-src"):
 // 79% of the FP64 pipe under ncu but 161.5 ms + 2.9 ms for the small leaves, no faster
@@ -739,10 +739,10 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
       kern<<<grid, MU_WARPS * 32, smem, s>>>(a);
     };
     if (L.full) go(k_p2p_mutual<64>, static_cast<int>(MU_WARPS * sizeof(MuWarp<64>)));
-#ifndef FMMGPU_MU_TCAP_SPARSE
-#define FMMGPU_MU_TCAP_SPARSE 128
-#endif
-    else go(k_p2p_mutual<FMMGPU_MU_TCAP_SPARSE>, static_cast<int>(MU_WARPS * sizeof(MuWarp<FMMGPU_MU_TCAP_SPARSE>)));
+    // non-full leaf levels: 256-target chunks (12 x 16.4 KB of shared memory): config D
+    // 164.5 -> 162.5 ms per evaluation against 128 (192: 163.2), fewer passes over each
+    // large leaf's source stream and fewer read-modify-writes of its slots
+    else go(k_p2p_mutual<256>, static_cast<int>(MU_WARPS * sizeof(MuWarp<256>)));
     FMM_CUDA(cudaGetLastError());
     const uint64_t dthreads = uint64_t(nl) * 32;
     k_p2p_drain<<<static_cast<unsigned>((dthreads + 255) / 256), 256, 0, s>>>(a);

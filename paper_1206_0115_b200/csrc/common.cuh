@@ -186,6 +186,9 @@ struct fmmgpu_ctx {
   std::string err;
   cudaStream_t s_far = nullptr, s_near = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // coarse M2L levels and the L2L chain run on s_aux beside the leaf M2L (evaluation)
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_up = nullptr, ev_aux = nullptr;
   cudaEvent_t ev_t[16] = {};
   double timings[10] = {};
   uint64_t launches = 0;
@@ -246,8 +249,10 @@ struct fmmgpu_ctx {
   bool use_graph = false;    // replay evaluations as a captured graph (fmmgpu_set_graph)
   bool capturing = false;
   uint64_t graph_launches = 0;
-  double* d_splitk = nullptr;  // M2L phase B split-K partials
-  size_t splitk_cap = 0;
+  // M2L phase B split-K partials: [0] coarse levels, [1] the leaf level (the two can run
+  // concurrently on s_aux and s_far)
+  double* d_splitk[2] = {};
+  size_t splitk_cap[2] = {};
   bool out_valid = false;        // d_out holds near + far of the current arrays
   bool zero_pending = false;     // expansions / field accumulators of a new tree not yet cleared
   // set while an unpartitioned evaluation is enqueued: every operator writes its output

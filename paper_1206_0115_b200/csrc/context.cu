@@ -194,6 +194,9 @@ void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx
   FMM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   FMM_CUDA(cudaStreamCreateWithPriority(&c->s_far, cudaStreamNonBlocking, prio_hi));
   FMM_CUDA(cudaStreamCreateWithPriority(&c->s_near, cudaStreamNonBlocking, prio_lo));
+  FMM_CUDA(cudaStreamCreateWithPriority(&c->s_aux, cudaStreamNonBlocking, prio_hi));
+  FMM_CUDA(cudaEventCreateWithFlags(&c->ev_up, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&c->ev_aux, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   for (auto& e : c->ev_t) FMM_CUDA(cudaEventCreate(&e));
@@ -292,7 +295,8 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
   }
   m2l_free(c);
   fmmgpu_invalidate_graph(c);
-  if (c->d_splitk) cudaFree(c->d_splitk);
+  for (auto* p : c->d_splitk)
+    if (p) cudaFree(p);
   if (c->nccl) fmmgpu_comm_destroy(c);
   if (c->d_interp) cudaFree(c->d_interp);
   if (c->d_flag) cudaFree(c->d_flag);
@@ -306,6 +310,9 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->s_far) cudaStreamDestroy(c->s_far);
   if (c->s_near) cudaStreamDestroy(c->s_near);
+  if (c->s_aux) cudaStreamDestroy(c->s_aux);
+  if (c->ev_up) cudaEventDestroy(c->ev_up);
+  if (c->ev_aux) cudaEventDestroy(c->ev_aux);
   delete c;
 }
 
@@ -512,14 +519,43 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
     exchange_level(c, v, s);
   }
   record(c, e[3], s);
-  for (int v = 2; v <= leaf; ++v) {
-    Span sp(c, FMMGPU_M2L, v, s, 0);
-    launch_m2l(c, v, s);
-  }
-  record(c, e[4], s);
-  for (int v = 2; v < leaf; ++v) {
-    Span sp(c, FMMGPU_L2L, v, s, 0);
-    launch_l2l(c, v, s);
+  static const bool aux = [] {  // FMMGPU_AUX=0: the whole far chain on one stream (A/B aid)
+    const char* v = std::getenv("FMMGPU_AUX");
+    return !(v && std::atoi(v) == 0);
+  }();
+  if (aux && leaf > 2) {
+    // M2L of every level reads only that level's multipoles, complete after the upward
+    // pass, so the coarse levels' M2L and the L2L chain (which needs local(v) = own + down
+    // of the coarse levels only) run on a second high-priority stream beside the leaf M2L;
+    // L2P waits for both. The small, latency-bound coarse launches then overlap the leaf
+    // M2L instead of running alone.
+    FMM_CUDA(cudaEventRecord(c->ev_up, s));
+    FMM_CUDA(cudaStreamWaitEvent(c->s_aux, c->ev_up, 0));
+    {
+      Span sp(c, FMMGPU_M2L, leaf, s, 0);
+      launch_m2l(c, leaf, s);
+    }
+    for (int v = 2; v < leaf; ++v) {
+      Span sp(c, FMMGPU_M2L, v, c->s_aux, 2);
+      launch_m2l(c, v, c->s_aux);
+    }
+    for (int v = 2; v < leaf; ++v) {
+      Span sp(c, FMMGPU_L2L, v, c->s_aux, 2);
+      launch_l2l(c, v, c->s_aux);
+    }
+    record(c, e[4], s);
+    FMM_CUDA(cudaEventRecord(c->ev_aux, c->s_aux));
+    FMM_CUDA(cudaStreamWaitEvent(s, c->ev_aux, 0));
+  } else {
+    for (int v = 2; v <= leaf; ++v) {
+      Span sp(c, FMMGPU_M2L, v, s, 0);
+      launch_m2l(c, v, s);
+    }
+    record(c, e[4], s);
+    for (int v = 2; v < leaf; ++v) {
+      Span sp(c, FMMGPU_L2L, v, s, 0);
+      launch_l2l(c, v, s);
+    }
   }
   record(c, e[5], s);
   {

@@ -920,17 +920,18 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     }();
     while (ks < 16 && ctas * ks < waves * 2u * 148u && kt / (2 * ks) >= 8) ks *= 2;
     g.ksplit = ks;
+    const int sb = v == c->height - 1 ? 1 : 0;  // the leaf may run beside the coarse levels
     if (ks > 1) {  // own buffer (not the shared scratch): captured graphs keep this pointer
       const size_t bytes = sizeof(double) * ks * size_t(L.n) * c->ldE;
-      if (bytes > c->splitk_cap) {
+      if (bytes > c->splitk_cap[sb]) {
         if (c->capturing) throw Error(FMMGPU_LOGIC_ERROR, "split-K buffer growth during graph capture");
-        if (c->d_splitk) FMM_CUDA(cudaFreeAsync(c->d_splitk, s));
-        FMM_CUDA(cudaMallocAsync(&c->d_splitk, bytes, s));
-        c->splitk_cap = bytes;
+        if (c->d_splitk[sb]) FMM_CUDA(cudaFreeAsync(c->d_splitk[sb], s));
+        FMM_CUDA(cudaMallocAsync(&c->d_splitk[sb], bytes, s));
+        c->splitk_cap[sb] = bytes;
         fmmgpu_invalidate_graph(c);
       }
     }
-    g.part = ks > 1 ? c->d_splitk : nullptr;
+    g.part = ks > 1 ? c->d_splitk[sb] : nullptr;
     // M-tiles of 128 rows; the rows past the last whole tile go to a 96- or 64-row tail
     // tile when that covers them (l = 7: 343 rows as 2 x 128 + 96 = 352 instead of 384, 11%
     // fewer DMMAs; l = 6: 128 + 96 = 224 instead of 256)

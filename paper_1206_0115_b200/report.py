@@ -7,7 +7,7 @@
   device's ledger rows), breakdown, occupancy over the device spans (bench.cpp:516-584);
 * ``write_chrome_trace`` trace.json in the reference's Chrome "ph":"X" format
   (runtime.cpp:277-292) from the device spans of FmmContext.trace_spans (one span per
-  operator launch; tid = CUDA stream: 0 far field, 1 near field).
+  operator launch; tid = CUDA stream: 0 far field, 1 near field, 2 coarse M2L + L2L).
 """
 from __future__ import annotations
 
@@ -69,6 +69,7 @@ def format_breakdown(rows: dict) -> str:
 def occupancy(spans, wall_ms: float | None = None, workers: int = 2) -> dict:
     """occupancy (runtime.cpp:260-276) over device spans: busy fraction per CUDA stream
     (the reference: per worker thread) and each kind's share of the busy time."""
+    workers = max([workers] + [sp[2] + 1 for sp in spans])  # streams: 0 far, 1 near, 2 coarse far
     busy = [0.0] * workers
     share = {k: 0.0 for k in KINDS}
     if wall_ms is None:

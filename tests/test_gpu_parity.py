@@ -293,8 +293,14 @@ def test_trace_spans(fmm, tmp_path):
     for a, b in zip(ref, got):
         assert np.array_equal(a, b)
     kinds = [(k, lv) for k, lv, _, _, _ in spans]
-    assert kinds == [("P2P", 4), ("P2M", 4), ("M2M", 3), ("M2M", 2), ("M2L", 2), ("M2L", 3), ("M2L", 4),
+    # the leaf M2L on the far-field stream, the coarse M2L levels and the L2L chain beside it
+    assert kinds == [("P2P", 4), ("P2M", 4), ("M2M", 3), ("M2M", 2), ("M2L", 4), ("M2L", 2), ("M2L", 3),
                      ("L2L", 2), ("L2L", 3), ("L2P", 4), ("P2PREDUCE", 4)]
+    aux = [sp for sp in spans if sp[2] == 2]
+    assert [(k, lv) for k, lv, *_ in aux] == [("M2L", 2), ("M2L", 3), ("L2L", 2), ("L2L", 3)]
+    assert all(b[3] >= a[4] - 1e-6 for a, b in zip(aux, aux[1:]))
+    l2p = [sp for sp in spans if sp[0] == "L2P"][0]
+    assert l2p[3] >= max(sp[4] for sp in aux) - 1e-6  # L2P after the coarse chain
     far = [sp for sp in spans if sp[2] == 0]
     assert all(sp[4] >= sp[3] for sp in spans)
     assert all(b[3] >= a[4] - 1e-6 for a, b in zip(far, far[1:]))  # one stream: in order

@@ -519,10 +519,13 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
     exchange_level(c, v, s);
   }
   record(c, e[3], s);
-  static const bool aux = [] {  // FMMGPU_AUX=0: the whole far chain on one stream (A/B aid)
+  // Measured (tools/gpu/gpu_r02af.sh, ms per evaluation single stream / aux stream): A 0.97 /
+  // 0.99, B 24.54 / 24.62, C 80.18 / 79.61, E 240.54 / 240.73 -- used above order 5 only.
+  static const int aux_env = [] {  // FMMGPU_AUX=0/1 forces it (A/B aid)
     const char* v = std::getenv("FMMGPU_AUX");
-    return !(v && std::atoi(v) == 0);
+    return v ? std::atoi(v) : -1;
   }();
+  const bool aux = aux_env >= 0 ? aux_env != 0 : c->ldE > 128;
   if (aux && leaf > 2) {
     // M2L of every level reads only that level's multipoles, complete after the upward
     // pass, so the coarse levels' M2L and the L2L chain (which needs local(v) = own + down

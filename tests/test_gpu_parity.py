@@ -293,7 +293,30 @@ def test_trace_spans(fmm, tmp_path):
     for a, b in zip(ref, got):
         assert np.array_equal(a, b)
     kinds = [(k, lv) for k, lv, _, _, _ in spans]
-    # the leaf M2L on the far-field stream, the coarse M2L levels and the L2L chain beside it
+    assert kinds == [("P2P", 4), ("P2M", 4), ("M2M", 3), ("M2M", 2), ("M2L", 2), ("M2L", 3), ("M2L", 4),
+                     ("L2L", 2), ("L2L", 3), ("L2P", 4), ("P2PREDUCE", 4)]
+    far = [sp for sp in spans if sp[2] == 0]
+    assert all(sp[4] >= sp[3] for sp in spans)
+    assert all(b[3] >= a[4] - 1e-6 for a, b in zip(far, far[1:]))  # one stream: in order
+    write_chrome_trace(str(tmp_path / "trace.json"), spans)
+    c.set_trace(False)
+    assert c.trace_spans() == []
+
+
+def test_trace_spans_coarse_stream(fmm):
+    """Above order 5 the coarse M2L levels and the L2L chain run on a second far-field
+    stream beside the leaf M2L; L2P starts after both; fields equal the one-stream order
+    to rounding (the same operations, different launch overlap only)."""
+    xyzw = make_particles(20000, "uniform", 4, True)
+    c = ctx_for(fmm, xyzw, 5, 6)
+    c.evaluate()
+    ref = c.gather()
+    c.set_trace(True)
+    c.evaluate()
+    spans = c.trace_spans()
+    for a, b in zip(ref, c.gather()):
+        assert np.array_equal(a, b)
+    kinds = [(k, lv) for k, lv, _, _, _ in spans]
     assert kinds == [("P2P", 4), ("P2M", 4), ("M2M", 3), ("M2M", 2), ("M2L", 4), ("M2L", 2), ("M2L", 3),
                      ("L2L", 2), ("L2L", 3), ("L2P", 4), ("P2PREDUCE", 4)]
     aux = [sp for sp in spans if sp[2] == 2]
@@ -301,12 +324,12 @@ def test_trace_spans(fmm, tmp_path):
     assert all(b[3] >= a[4] - 1e-6 for a, b in zip(aux, aux[1:]))
     l2p = [sp for sp in spans if sp[0] == "L2P"][0]
     assert l2p[3] >= max(sp[4] for sp in aux) - 1e-6  # L2P after the coarse chain
-    far = [sp for sp in spans if sp[2] == 0]
-    assert all(sp[4] >= sp[3] for sp in spans)
-    assert all(b[3] >= a[4] - 1e-6 for a, b in zip(far, far[1:]))  # one stream: in order
-    write_chrome_trace(str(tmp_path / "trace.json"), spans)
+    _, of = _oracle_eval(xyzw, 5, 6, 63)
+    g = c.gather()
+    assert relative_l2_error(g[0], of[0]) <= TOL
+    assert force_error(*g[1:], *of[1:]) <= TOL
     c.set_trace(False)
-    assert c.trace_spans() == []
+    c.close()
 
 
 def test_pipelined_runs(fmm):

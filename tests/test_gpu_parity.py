@@ -305,8 +305,8 @@ def test_trace_spans(fmm, tmp_path):
 
 def test_trace_spans_coarse_stream(fmm):
     """Above order 5 the coarse M2L levels and the L2L chain run on a second far-field
-    stream beside the leaf M2L; L2P starts after both; fields equal the one-stream order
-    to rounding (the same operations, different launch overlap only)."""
+    stream beside the leaf M2L; L2P starts after both; traced and untraced runs give the
+    same bits, and the fields match the oracle."""
     xyzw = make_particles(20000, "uniform", 4, True)
     c = ctx_for(fmm, xyzw, 5, 6)
     c.evaluate()

@@ -137,6 +137,74 @@ __global__ void k_far(FarArgs a, uint32_t* __restrict__ cnt, const unsigned long
     for (int q = 0; q < 16; ++q) cnt[(size_t(b) * 16 + q) * a.group + cl] = k16[q];
 }
 
+// The fill as one warp per target cell: the candidate sources (children of the sorted
+// parent neighbours, ascending) are spread over the lanes in order; each 32-candidate step
+// groups the lanes by canonical class (__match_any_sync), so a class's entries of the step
+// are written to consecutive slots (a few segments per store instead of 32 scattered
+// ones). Same positions as k_far<true>: within a (block, class) group the cells in order,
+// within a cell the sources ascending.
+__global__ void __launch_bounds__(256) k_far_fill_warp(FarArgs a, const unsigned long long* __restrict__ pos,
+                                                       uint32_t* __restrict__ tgt, uint32_t* __restrict__ src,
+                                                       uint16_t* __restrict__ vec) {
+  __shared__ uint32_t s_first[8][28], s_off[8][28];
+  __shared__ uint32_t s_cnt[8][16];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= a.L.n) return;
+  const uint64_t code = a.L.code[c];
+  int ijk[3];
+  demorton(code, ijk);
+  // parent neighbours, ascending (every lane forms the same list), children per neighbour
+  uint32_t pn[27];
+  const int m = parent_neighbours(a.P, code >> 3, pn);
+  uint32_t cntn = 0, firstn = 0;
+  if (lane < m) {
+    firstn = a.p_first_child[pn[lane]];
+    cntn = a.p_child_count[pn[lane]];
+  }
+  uint32_t incl = cntn;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (lane < m) {
+    s_first[wl][lane] = firstn;
+    s_off[wl][lane] = incl - cntn;
+  }
+  if (lane < 16) s_cnt[wl][lane] = 0;
+  __syncwarp();
+  const uint32_t b = c / a.group, cl = c % a.group;
+  for (uint32_t base = 0; base < total; base += 32) {
+    const uint32_t e = base + lane;
+    int q = -1, slot = 0;
+    uint32_t ch = 0;
+    if (e < total) {
+      int t = 0;
+      while (t + 1 < m && s_off[wl][t + 1] <= e) ++t;
+      ch = s_first[wl][t] + (e - s_off[wl][t]);
+      int cijk[3];
+      demorton(a.L.code[ch], cijk);
+      const int ti = cijk[0] - ijk[0], tj = cijk[1] - ijk[1], tk = cijk[2] - ijk[2];
+      if (max(abs(ti), max(abs(tj), abs(tk))) > 1) {
+        slot = (ti + 3) * 49 + (tj + 3) * 7 + (tk + 3);
+        q = a.canon[slot];
+      }
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, q);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    if (q >= 0) {
+      const unsigned long long p = pos[(size_t(b) * 16 + q) * a.group + cl] + s_cnt[wl][q] + rank;
+      tgt[p] = c;
+      src[p] = ch;
+      vec[p] = static_cast<uint16_t>(slot);
+    }
+    __syncwarp();
+    if (q >= 0 && rank == 0) s_cnt[wl][q] += __popc(peers);
+    __syncwarp();
+  }
+}
+
 __global__ void k_group_off(const unsigned long long* __restrict__ pos, uint64_t ngroups, uint32_t group,
                             uint64_t total, uint64_t* __restrict__ goff) {
   const uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -245,7 +313,7 @@ void lists_build(fmmgpu_ctx* c) {
     L.far_vec = dalloc<uint16_t>(total, s);
     L.far_group_off = dalloc<uint64_t>(ng + 1, s);
     k_group_off<<<blocks(ng + 1, 256), 256, 0, s>>>(pos, ng, c->group, total, L.far_group_off);
-    k_far<true><<<blocks(L.n, 128), 128, 0, s>>>(a, nullptr, pos, L.far_target, L.far_source, L.far_vec);
+    k_far_fill_warp<<<blocks(uint64_t(L.n) * 32, 256), 256, 0, s>>>(a, pos, L.far_target, L.far_source, L.far_vec);
     FMM_CUDA(cudaGetLastError());
     cudaFreeAsync(cnt, s);
     cudaFreeAsync(pos, s);

@@ -189,6 +189,7 @@ struct fmmgpu_ctx {
   // coarse M2L levels and the L2L chain run on s_aux beside the leaf M2L (evaluation)
   cudaStream_t s_aux = nullptr;
   cudaEvent_t ev_up = nullptr, ev_aux = nullptr;
+  cudaEvent_t ev_p2p_main = nullptr;  // the mutual near-field kernel done (slots written)
   cudaEvent_t ev_t[16] = {};
   double timings[10] = {};
   uint64_t launches = 0;
@@ -322,9 +323,11 @@ void lists_free(fmmgpu_ctx* c);
 void launch_p2m(fmmgpu_ctx* c, cudaStream_t s);
 void launch_m2m(fmmgpu_ctx* c, int parent_level, cudaStream_t s);
 void launch_l2l(fmmgpu_ctx* c, int parent_level, cudaStream_t s);
-void launch_l2p(fmmgpu_ctx* c, cudaStream_t s);
+void launch_l2p(fmmgpu_ctx* c, cudaStream_t s, bool drain = false);
 void launch_m2l(fmmgpu_ctx* c, int level, cudaStream_t s);
-void launch_p2p(fmmgpu_ctx* c, cudaStream_t s);
+// fuse_drain (evaluations): the mutual kernel only; its slot drain runs inside L2P
+// (launch_l2p(..., true)) after the event ev_p2p_main this records
+void launch_p2p(fmmgpu_ctx* c, cudaStream_t s, bool fuse_drain = false);
 void ensure_p2p_slots(fmmgpu_ctx* c);  // allocates the mutual P2P slots of the current tree (s_far)
 bool p2p_use_mutual(const fmmgpu_ctx* c, uint32_t leaves);  // the kernel launch_p2p picks
 void launch_gather(fmmgpu_ctx* c, cudaStream_t s);

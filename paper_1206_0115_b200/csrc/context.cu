@@ -197,6 +197,7 @@ void ctx_init(fmmgpu_ctx* c, int device, int order, double eps, const fmmgpu_ctx
   FMM_CUDA(cudaStreamCreateWithPriority(&c->s_aux, cudaStreamNonBlocking, prio_hi));
   FMM_CUDA(cudaEventCreateWithFlags(&c->ev_up, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&c->ev_aux, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&c->ev_p2p_main, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   for (auto& e : c->ev_t) FMM_CUDA(cudaEventCreate(&e));
@@ -313,6 +314,7 @@ void fmmgpu_destroy(fmmgpu_ctx* c) {
   if (c->s_aux) cudaStreamDestroy(c->s_aux);
   if (c->ev_up) cudaEventDestroy(c->ev_up);
   if (c->ev_aux) cudaEventDestroy(c->ev_aux);
+  if (c->ev_p2p_main) cudaEventDestroy(c->ev_p2p_main);
   delete c;
 }
 
@@ -498,10 +500,18 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
   }
   FMM_CUDA(cudaEventRecord(c->ev_fork, s));
   FMM_CUDA(cudaStreamWaitEvent(c->s_near, c->ev_fork, 0));
+  // mutual near field: its ordered slot drain (p2p_reduce) is fused into L2P, which waits
+  // for the near-field kernel (the drain's HBM pass then overlaps L2P's arithmetic)
+  static const int fuse_env = [] {  // FMMGPU_FUSE_DRAIN=0: separate drain kernel (A/B aid)
+    const char* v = std::getenv("FMMGPU_FUSE_DRAIN");
+    return v ? std::atoi(v) : 1;
+  }();
+  const Level& LL = c->lv[leaf];
+  const bool fuse = fuse_env != 0 && p2p_use_mutual(c, LL.own1 - LL.own0);
   record(c, e[6], c->s_near);
   {
     Span sp(c, FMMGPU_P2P, leaf, c->s_near, 1);
-    launch_p2p(c, c->s_near);
+    launch_p2p(c, c->s_near, fuse);
   }
   record(c, e[7], c->s_near);
   record(c, e[1], s);
@@ -561,9 +571,10 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
     }
   }
   record(c, e[5], s);
+  if (fuse) FMM_CUDA(cudaStreamWaitEvent(s, c->ev_p2p_main, 0));
   {
     Span sp(c, FMMGPU_L2P, leaf, s, 0);
-    launch_l2p(c, s);
+    launch_l2p(c, s, fuse);
   }
   record(c, e[8], s);
   FMM_CUDA(cudaEventRecord(c->ev_join, c->s_near));

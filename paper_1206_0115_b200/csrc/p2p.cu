@@ -701,7 +701,7 @@ const uint32_t* p2p_order(fmmgpu_ctx* c, const Level& L, cudaStream_t s) {
 }
 }  // namespace
 
-void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
+void launch_p2p(fmmgpu_ctx* c, cudaStream_t s, bool fuse_drain) {
   const int leaf = c->height - 1;
   const Level& L = c->lv[leaf];
   const Level& P = c->lv[leaf - 1];
@@ -744,6 +744,11 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s) {
     // large leaf's source stream and fewer read-modify-writes of its slots
     else go(k_p2p_mutual<256>, static_cast<int>(MU_WARPS * sizeof(MuWarp<256>)));
     FMM_CUDA(cudaGetLastError());
+    if (fuse_drain) {  // the drain happens in L2P (transfer.cu), after this event
+      FMM_CUDA(cudaEventRecord(c->ev_p2p_main, s));
+      c->launches += 1;
+      return;
+    }
     const uint64_t dthreads = uint64_t(nl) * 32;
     k_p2p_drain<<<static_cast<unsigned>((dthreads + 255) / 256), 256, 0, s>>>(a);
     FMM_CUDA(cudaGetLastError());

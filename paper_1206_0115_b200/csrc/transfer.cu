@@ -91,7 +91,19 @@ struct LeafArgs {
   int ldE;
   Geo geo;
   int ow;  // overwrite (evaluation): P2M writes the multipole incl. zero padding, L2P writes far
+  // L2P with the mutual near field's slot drain fused (evaluations): near[j] += slot[s][j]
+  // in slot order for the slots whose writer leaf exists and is owned (k_p2p_drain)
+  const double4* slot;  // [13][n], nullptr = no drain
+  double4* near;
+  LevelView leafv;
 };
+
+// upper half-shell direction of slot s (p2p.cu mu_up)
+__device__ __forceinline__ void drain_dir(int s, int d[3]) {
+  d[0] = s >= 4 ? 1 : 0;
+  d[1] = s >= 4 ? (s - 4) / 3 - 1 : (s >= 1 ? 1 : 0);
+  d[2] = s >= 4 ? (s - 4) % 3 - 1 : (s >= 1 ? s - 2 : 1);
+}
 
 constexpr int P2M_THREADS = 128;
 constexpr int P2M_WARPS = P2M_THREADS / 32;
@@ -196,6 +208,7 @@ __global__ void __launch_bounds__(L2P_THREADS, MINB > 0 ? MINB : 0) k_l2p_block(
   __shared__ double tn[L * (L - 1) + 1];
   __shared__ uint32_t cfirst[L2P_CELLS + 1];
   __shared__ double cctr[L2P_CELLS][3];
+  __shared__ uint32_t cmask[L2P_CELLS];  // fused drain: slots present per cell
   const uint32_t c0 = a.cell0 + blockIdx.x * L2P_CELLS;
   const uint32_t nc = min(static_cast<uint32_t>(L2P_CELLS), a.ncells - c0);
   const uint64_t p0 = a.first[c0], p1 = uint64_t(a.first[c0 + nc - 1]) + a.count[c0 + nc - 1];
@@ -212,6 +225,18 @@ __global__ void __launch_bounds__(L2P_THREADS, MINB > 0 ? MINB : 0) k_l2p_block(
     cell_center(a.geo, a.code[c], cctr[threadIdx.x]);
   }
   if (threadIdx.x == 0) cfirst[nc] = static_cast<uint32_t>(p1);
+  if (a.slot) {
+    if (threadIdx.x < L2P_CELLS) cmask[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < nc * 13; e += L2P_THREADS) {
+      const uint32_t lc = e / 13, sl = e % 13, q = c0 + lc;
+      int ijk[3], d[3];
+      demorton(a.code[q], ijk);
+      drain_dir(static_cast<int>(sl), d);
+      const uint32_t w = find_ijk(a.leafv, ijk[0] - d[0], ijk[1] - d[1], ijk[2] - d[2]);
+      if (w != NPOS && w >= a.cell0 && w < a.ncells) atomicOr(&cmask[lc], 1u << sl);
+    }
+  }
   for (int i = threadIdx.x; i < L * (L - 1); i += L2P_THREADS) tn[i] = a.tn[i];
   // staged 4 elements at a time so the loads of a thread are in flight together
   for (uint32_t i0 = threadIdx.x; i0 < nc * L3; i0 += 4 * L2P_THREADS) {
@@ -303,6 +328,20 @@ __global__ void __launch_bounds__(L2P_THREADS, MINB > 0 ? MINB : 0) k_l2p_block(
     r.z -= inv * dy;
     r.w -= inv * dz;
     far4[s] = r;
+    if (a.slot) {  // p2p_reduce of this particle (the k_p2p_drain order)
+      const uint32_t m = cmask[lc];
+      double4 nr = a.near[s];
+#pragma unroll
+      for (int sl = 0; sl < 13; ++sl)
+        if ((m >> sl) & 1u) {
+          const double4 v = a.slot[uint64_t(sl) * a.n + s];
+          nr.x += v.x;
+          nr.y += v.y;
+          nr.z += v.z;
+          nr.w += v.w;
+        }
+      a.near[s] = nr;
+    }
   }
 }
 
@@ -671,12 +710,17 @@ void launch_p2m(fmmgpu_ctx* c, cudaStream_t s) {
   ++c->launches;
 }
 
-void launch_l2p(fmmgpu_ctx* c, cudaStream_t s) {
+void launch_l2p(fmmgpu_ctx* c, cudaStream_t s, bool drain) {
   LeafArgs a = leaf_args(c);
   a.expansion = c->lv[c->height - 1].local_own;
   a.down = c->lv[c->height - 1].local_down;
   a.far = c->d_far;
   a.ow = c->ow;
+  if (drain) {
+    a.slot = reinterpret_cast<const double4*>(c->d_slot);
+    a.near = reinterpret_cast<double4*>(c->d_near);
+    a.leafv = c->lv[c->height - 1].view(c->height - 1);
+  }
   dispatch_order<RunL2P>(c->order, a, s);
   FMM_CUDA(cudaGetLastError());
   ++c->launches;

@@ -3,7 +3,7 @@
 # reference baselines, the reference arm, launch list + ncu of the top kernels at B,
 # scaling projection and distributed-input volumes
 cd "$GRAFT_REPO_ROOT"
-O=gpurun_out/final; mkdir -p $O
+O=gpurun_out/final2; mkdir -p $O
 nproc > $O/host.txt; free -g >> $O/host.txt; nvidia-smi >> $O/host.txt
 timeout 1800 python -m pytest tests -m gpu -q -rs > $O/pytest_gpu.log 2>&1; echo "exit $?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1

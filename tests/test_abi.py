@@ -49,3 +49,24 @@ def test_no_cpu_fallback_without_device():
     assert (xyzw == Oracle.generate_particles(4, "uniform", 42)).all()
     s = P.generate_particles(50, "sphere", 3)
     assert (s == Oracle.generate_particles(50, "sphere", 3)).all()
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libfmmgpu.so not built")
+@pytest.mark.parametrize("dist,seed", [("uniform", 1), ("sphere", 2), ("ellipsoid", 3)])
+def test_root_from_bounds_matches_bounding_cube(dist, seed):
+    """The distributed build's root cube (fmmgpu_root_from_bounds, host-only, over the
+    ranks' combined min / max) is bit-identical to bounding_cube (geometry.cpp:18-36) of
+    the whole set, here the CPU restatement's root of the same particles; bad bounds are
+    refused."""
+    import numpy as np
+    from oracles import Oracle, OracleTree
+    import sys
+    sys.path.insert(0, ROOT)
+    import paper_1206_0115_b200 as P
+    xyzw = Oracle.generate_particles(5000, dist, seed)
+    slices = np.array_split(xyzw, 3)
+    lohi = np.concatenate([np.min([s[:, :3].min(axis=0) for s in slices], axis=0),
+                           np.max([s[:, :3].max(axis=0) for s in slices], axis=0)])
+    assert np.array_equal(P.root_from_bounds(lohi), OracleTree(xyzw, 3).root_cube())
+    with pytest.raises(P.InvalidArgument):
+        P.root_from_bounds(np.array([1.0, 0, 0, 0, 1, 1]))  # min > max on x

@@ -17,11 +17,15 @@ namespace {
 
 inline unsigned blocks(uint64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
+// list arrays come from the context's stream-ordered block cache, so rebuilds reuse the
+// previous lists' blocks (config E's far lists are 4.4 GB: a fresh cudaMallocAsync of them
+// cost tens of ms)
 template <typename T>
-T* dalloc(size_t count, cudaStream_t s) {
-  void* p = nullptr;
-  FMM_CUDA(cudaMallocAsync(&p, (count ? count : 1) * sizeof(T), s));
-  return static_cast<T*>(p);
+T* dalloc(fmmgpu_ctx* c, size_t count, cudaStream_t s) {
+  return static_cast<T*>(cache_alloc(c, (count ? count : 1) * sizeof(T), s));
+}
+void dfree(fmmgpu_ctx* c, void* p, cudaStream_t s) {
+  if (p) cache_free(c, p, s);
 }
 
 // ---- near field -----------------------------------------------------------------
@@ -216,15 +220,15 @@ __global__ void k_group_off(const unsigned long long* __restrict__ pos, uint64_t
 
 void lists_free(fmmgpu_ctx* c) {
   cudaStream_t s = c->s_far;
-  if (c->d_near_off) cudaFreeAsync(c->d_near_off, s);
-  if (c->d_near_cells) cudaFreeAsync(c->d_near_cells, s);
+  dfree(c, c->d_near_off, s);
+  dfree(c, c->d_near_cells, s);
   c->d_near_off = nullptr;
   c->d_near_cells = nullptr;
   for (auto& L : c->lv) {
-    if (L.far_target) cudaFreeAsync(L.far_target, s);
-    if (L.far_source) cudaFreeAsync(L.far_source, s);
-    if (L.far_vec) cudaFreeAsync(L.far_vec, s);
-    if (L.far_group_off) cudaFreeAsync(L.far_group_off, s);
+    dfree(c, L.far_target, s);
+    dfree(c, L.far_source, s);
+    dfree(c, L.far_vec, s);
+    dfree(c, L.far_group_off, s);
     L.far_target = L.far_source = nullptr;
     L.far_vec = nullptr;
     L.far_group_off = nullptr;
@@ -237,8 +241,8 @@ uint64_t near_directional_count(fmmgpu_ctx* c) {
   cudaStream_t s = c->s_far;
   const int leaf = c->height - 1;
   const Level& L = c->lv[leaf];
-  uint32_t* cnt = dalloc<uint32_t>(L.n, s);
-  unsigned long long* work = dalloc<unsigned long long>(L.n + 1, s);
+  uint32_t* cnt = dalloc<uint32_t>(c, L.n, s);
+  unsigned long long* work = dalloc<unsigned long long>(c, L.n + 1, s);
   k_near_count<<<blocks(L.n, 128), 128, 0, s>>>(L.view(leaf), L.particle_count, cnt, work);
   FMM_CUDA(cudaGetLastError());
   size_t tb = 0;
@@ -247,8 +251,8 @@ uint64_t near_directional_count(fmmgpu_ctx* c) {
   unsigned long long total = 0;
   FMM_CUDA(cudaMemcpyAsync(&total, work + L.n, 8, cudaMemcpyDeviceToHost, s));
   FMM_CUDA(cudaStreamSynchronize(s));
-  cudaFreeAsync(cnt, s);
-  cudaFreeAsync(work, s);
+  dfree(c, cnt, s);
+  dfree(c, work, s);
   return total;
 }
 
@@ -260,12 +264,12 @@ void lists_build(fmmgpu_ctx* c) {
   // near CSR
   {
     const Level& L = c->lv[leaf];
-    uint32_t* cnt = dalloc<uint32_t>(L.n + 1, s);
-    unsigned long long* work = dalloc<unsigned long long>(L.n + 1, s);
+    uint32_t* cnt = dalloc<uint32_t>(c, L.n + 1, s);
+    unsigned long long* work = dalloc<unsigned long long>(c, L.n + 1, s);
     FMM_CUDA(cudaMemsetAsync(cnt + L.n, 0, 4, s));
     k_near_count<<<blocks(L.n, 128), 128, 0, s>>>(L.view(leaf), L.particle_count, cnt, work);
     FMM_CUDA(cudaGetLastError());
-    c->d_near_off = dalloc<uint32_t>(L.n + 1, s);
+    c->d_near_off = dalloc<uint32_t>(c, L.n + 1, s);
     size_t tb = 0;
     FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, c->d_near_off, static_cast<int>(L.n + 1), s));
     FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, cnt, c->d_near_off, static_cast<int>(L.n + 1), s));
@@ -278,11 +282,11 @@ void lists_build(fmmgpu_ctx* c) {
     FMM_CUDA(cudaStreamSynchronize(s));
     c->near_entries = entries;
     c->near_directional = total;
-    c->d_near_cells = dalloc<uint32_t>(entries, s);
+    c->d_near_cells = dalloc<uint32_t>(c, entries, s);
     k_near_fill<<<blocks(L.n, 128), 128, 0, s>>>(L.view(leaf), c->d_near_off, c->d_near_cells);
     FMM_CUDA(cudaGetLastError());
-    cudaFreeAsync(cnt, s);
-    cudaFreeAsync(work, s);
+    dfree(c, cnt, s);
+    dfree(c, work, s);
   }
   // far pairs per level
   for (int v = 2; v <= leaf; ++v) {
@@ -291,8 +295,8 @@ void lists_build(fmmgpu_ctx* c) {
     const uint64_t nb = L.block_offsets.size() - 1;
     const uint64_t ng = nb * 16;
     const uint64_t slots = ng * c->group;
-    uint32_t* cnt = dalloc<uint32_t>(slots, s);
-    unsigned long long* pos = dalloc<unsigned long long>(slots + 1, s);
+    uint32_t* cnt = dalloc<uint32_t>(c, slots, s);
+    unsigned long long* pos = dalloc<unsigned long long>(c, slots + 1, s);
     FMM_CUDA(cudaMemsetAsync(cnt, 0, 4 * slots, s));
     FarArgs a{L.view(v), P.view(v - 1), L.parent, P.first_child, P.child_count, c->d_canon,
               static_cast<uint32_t>(c->group)};
@@ -308,15 +312,15 @@ void lists_build(fmmgpu_ctx* c) {
     FMM_CUDA(cudaStreamSynchronize(s));
     const uint64_t total = last_pos + last_cnt;
     L.far_pairs = total;
-    L.far_target = dalloc<uint32_t>(total, s);
-    L.far_source = dalloc<uint32_t>(total, s);
-    L.far_vec = dalloc<uint16_t>(total, s);
-    L.far_group_off = dalloc<uint64_t>(ng + 1, s);
+    L.far_target = dalloc<uint32_t>(c, total, s);
+    L.far_source = dalloc<uint32_t>(c, total, s);
+    L.far_vec = dalloc<uint16_t>(c, total, s);
+    L.far_group_off = dalloc<uint64_t>(c, ng + 1, s);
     k_group_off<<<blocks(ng + 1, 256), 256, 0, s>>>(pos, ng, c->group, total, L.far_group_off);
     k_far_fill_warp<<<blocks(uint64_t(L.n) * 32, 256), 256, 0, s>>>(a, pos, L.far_target, L.far_source, L.far_vec);
     FMM_CUDA(cudaGetLastError());
-    cudaFreeAsync(cnt, s);
-    cudaFreeAsync(pos, s);
+    dfree(c, cnt, s);
+    dfree(c, pos, s);
   }
   FMM_CUDA(cudaStreamSynchronize(s));
   c->have_lists = true;

@@ -571,8 +571,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   fmmgpu_invalidate_graph(c);
   partition_free(c);
   tree_free(c);
-  lists_free(c);
   ++c->cache.epoch;
+  lists_free(c);  // after the epoch bump: the next lists build reuses these blocks
   trace("free");
 
   // input -> device (input order); a pipelined run (fmmgpu_run_async) has already

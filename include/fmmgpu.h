@@ -155,6 +155,13 @@ int fmmgpu_upload_expansion(fmmgpu_ctx* ctx, int level, int which, const double*
 uint64_t fmmgpu_near_entries(const fmmgpu_ctx* ctx);
 int fmmgpu_download_near(fmmgpu_ctx* ctx, uint32_t* near_offsets, uint32_t* near_cells,
                          uint64_t* total_directional);
+/* NearFieldPlan's block arrays (direct.cpp:36-58): task_interactions (one per leaf block),
+ * partners_above and contributors_below as CSR (offsets: blocks + 1 entries). Any array
+ * may be NULL; *n_above / *n_below = the list lengths (query with NULL lists first).
+ * Needs fmmgpu_build_lists. */
+int fmmgpu_download_near_blocks(fmmgpu_ctx* ctx, uint64_t* task_interactions, uint32_t* above_off,
+                                uint32_t* above, uint32_t* below_off, uint32_t* below, uint64_t* n_above,
+                                uint64_t* n_below);
 uint64_t fmmgpu_far_pairs(const fmmgpu_ctx* ctx, int level);
 /* M2LPairRef (m2l.hpp:66-70) as three arrays, and group_offsets (blocks*16+1). */
 int fmmgpu_download_far(fmmgpu_ctx* ctx, int level, uint32_t* target, uint32_t* source,

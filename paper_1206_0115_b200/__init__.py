@@ -105,6 +105,7 @@ def lib():
         L.fmmgpu_comm_destroy.argtypes = [c_void_p]
         L.fmmgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
         L.fmmgpu_exchange_plan.argtypes = [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+        L.fmmgpu_download_near_blocks.argtypes = [c_void_p] + [c_void_p] * 7
         L.fmmgpu_set_measurement.argtypes = [c_void_p, c_int]
         L.fmmgpu_root_from_bounds.argtypes = [c_void_p, c_void_p]
         L.fmmgpu_dist_local.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_void_p]
@@ -283,6 +284,23 @@ class FmmContext:
         tot = c_uint64()
         self._check(self._lib.fmmgpu_download_near(self.h, _p(off), _p(cells), byref(tot)))
         return off, cells[:ne], tot.value
+
+    def near_blocks(self):
+        """NearFieldPlan block arrays (direct.cpp:36-58): (task_interactions, partners_above
+        offsets, partners_above, contributors_below offsets, contributors_below)."""
+        na, nb_ = c_uint64(), c_uint64()
+        self._check(self._lib.fmmgpu_download_near_blocks(self.h, None, None, None, None, None, byref(na),
+                                                          byref(nb_)))
+        nc = self._lib.fmmgpu_level_cells(self.h, self.height - 1)
+        nblk = (nc + self.group_size - 1) // self.group_size
+        ti = np.zeros(nblk, dtype=np.uint64)
+        ao = np.zeros(nblk + 1, dtype=np.uint32)
+        bo = np.zeros(nblk + 1, dtype=np.uint32)
+        a = np.zeros(max(na.value, 1), dtype=np.uint32)
+        b = np.zeros(max(nb_.value, 1), dtype=np.uint32)
+        self._check(self._lib.fmmgpu_download_near_blocks(self.h, _p(ti), _p(ao), _p(a), _p(bo), _p(b), byref(na),
+                                                          byref(nb_)))
+        return ti, ao, a[:na.value], bo, b[:nb_.value]
 
     def far(self, v: int):
         npairs = self._lib.fmmgpu_far_pairs(self.h, v)

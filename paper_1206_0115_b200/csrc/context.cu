@@ -1092,6 +1092,14 @@ int fmmgpu_download_near(fmmgpu_ctx* c, uint32_t* off, uint32_t* cells, uint64_t
   });
 }
 
+int fmmgpu_download_near_blocks(fmmgpu_ctx* c, uint64_t* task_interactions, uint32_t* above_off, uint32_t* above,
+                                uint32_t* below_off, uint32_t* below, uint64_t* n_above, uint64_t* n_below) {
+  return guarded(c, [&] {
+    FMM_CUDA(cudaSetDevice(c->device));
+    near_blocks(c, task_interactions, above_off, above, below_off, below, n_above, n_below);
+  });
+}
+
 uint64_t fmmgpu_far_pairs(const fmmgpu_ctx* c, int v) {
   if (!c || !c->have_lists || v < 2 || v >= c->height) return 0;
   return c->lv[v].far_pairs;

@@ -209,6 +209,39 @@ __global__ void __launch_bounds__(256) k_far_fill_warp(FarArgs a, const unsigned
   }
 }
 
+// NearFieldPlan block arrays (build_near_field_plan, direct.cpp:36-58): per leaf cell c of
+// block b, its near cells o owned by b's side (ob > b, or ob == b and o > c) add
+// 2 n_c n_o directional interactions to b's task, and every ob != b is a partner above b;
+// n_c (n_c - 1) for the cell itself. Integer atomics: the sums are order-free.
+__global__ void k_near_blocks(LevelView L, const uint32_t* __restrict__ count, const uint32_t* __restrict__ off,
+                              const uint32_t* __restrict__ cells, uint32_t group,
+                              unsigned long long* __restrict__ task, unsigned long long* __restrict__ keys,
+                              unsigned int* __restrict__ nkeys) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= L.n) return;
+  const uint32_t b = c / group;
+  const unsigned long long nc = count[c];
+  unsigned long long owned = nc * (nc - 1);
+  for (uint32_t k = off[c]; k < off[c + 1]; ++k) {
+    const uint32_t o = cells[k], ob = o / group;
+    if (ob < b || (ob == b && o < c)) continue;
+    if (ob != b) keys[atomicAdd(nkeys, 1u)] = (static_cast<unsigned long long>(b) << 32) | ob;
+    owned += 2 * nc * count[o];
+  }
+  atomicAdd(&task[b], owned);
+}
+__global__ void k_split_keys(const unsigned long long* __restrict__ keys, uint32_t n, int hi_first,
+                             uint32_t* __restrict__ lo_out, unsigned long long* __restrict__ swapped,
+                             uint32_t* __restrict__ cnt) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t hi = static_cast<uint32_t>(keys[i] >> 32), lo = static_cast<uint32_t>(keys[i]);
+  lo_out[i] = lo;
+  atomicAdd(&cnt[hi], 1u);
+  if (swapped) swapped[i] = (static_cast<unsigned long long>(lo) << 32) | hi;
+  (void)hi_first;
+}
+
 __global__ void k_group_off(const unsigned long long* __restrict__ pos, uint64_t ngroups, uint32_t group,
                             uint64_t total, uint64_t* __restrict__ goff) {
   const uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -324,6 +357,74 @@ void lists_build(fmmgpu_ctx* c) {
   }
   FMM_CUDA(cudaStreamSynchronize(s));
   c->have_lists = true;
+}
+
+
+// The block-level near plan (partners_above / contributors_below as CSR, task_interactions)
+// from the near CSR; host arrays, NULL = skip. Returns the two list lengths.
+void near_blocks(fmmgpu_ctx* c, uint64_t* task_out, uint32_t* above_off, uint32_t* above, uint32_t* below_off,
+                 uint32_t* below, uint64_t* n_above, uint64_t* n_below) {
+  if (!c->have_lists) throw Error(FMMGPU_LOGIC_ERROR, "no lists: call fmmgpu_build_lists first");
+  cudaStream_t s = c->s_far;
+  const int leaf = c->height - 1;
+  const Level& L = c->lv[leaf];
+  const uint32_t nb = static_cast<uint32_t>(L.block_offsets.size() - 1);
+  const uint32_t group = static_cast<uint32_t>(c->group);
+  unsigned long long* task = dalloc<unsigned long long>(c, nb, s);
+  unsigned long long* keys = dalloc<unsigned long long>(c, c->near_entries + 1, s);
+  unsigned long long* keys2 = dalloc<unsigned long long>(c, c->near_entries + 1, s);
+  uint32_t* nkeys = dalloc<uint32_t>(c, 2, s);
+  FMM_CUDA(cudaMemsetAsync(task, 0, 8ull * nb, s));
+  FMM_CUDA(cudaMemsetAsync(nkeys, 0, 8, s));
+  k_near_blocks<<<blocks(L.n, 128), 128, 0, s>>>(L.view(leaf), L.particle_count, c->d_near_off, c->d_near_cells,
+                                                 group, task, keys, nkeys);
+  FMM_CUDA(cudaGetLastError());
+  uint32_t nk = 0;
+  FMM_CUDA(cudaMemcpyAsync(&nk, nkeys, 4, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  size_t tb = 0;
+  // unique sorted (b, b') pairs: partners_above in order
+  uint32_t nu = 0;
+  if (nk) {
+    FMM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, static_cast<int>(nk), 0, 64, s));
+    FMM_CUDA(cub::DeviceRadixSort::SortKeys(scratch(c, tb), tb, keys, keys2, static_cast<int>(nk), 0, 64, s));
+    FMM_CUDA(cub::DeviceSelect::Unique(nullptr, tb, keys2, keys, nkeys + 1, static_cast<int>(nk), s));
+    FMM_CUDA(cub::DeviceSelect::Unique(scratch(c, tb), tb, keys2, keys, nkeys + 1, static_cast<int>(nk), s));
+    FMM_CUDA(cudaMemcpyAsync(&nu, nkeys + 1, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+  }
+  uint32_t* lo = dalloc<uint32_t>(c, nu + 1, s);
+  uint32_t* cnt = dalloc<uint32_t>(c, nb + 1, s);
+  uint32_t* offs = dalloc<uint32_t>(c, nb + 1, s);
+  auto csr = [&](const unsigned long long* k, unsigned long long* swapped, uint32_t* off_out, uint32_t* list_out) {
+    FMM_CUDA(cudaMemsetAsync(cnt, 0, 4ull * (nb + 1), s));
+    if (nu) {
+      k_split_keys<<<blocks(nu, 256), 256, 0, s>>>(k, nu, 1, lo, swapped, cnt);
+      FMM_CUDA(cudaGetLastError());
+    }
+    FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs, static_cast<int>(nb + 1), s));
+    FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, cnt, offs, static_cast<int>(nb + 1), s));
+    if (off_out) FMM_CUDA(cudaMemcpyAsync(off_out, offs, 4ull * (nb + 1), cudaMemcpyDeviceToHost, s));
+    if (list_out && nu) FMM_CUDA(cudaMemcpyAsync(list_out, lo, 4ull * nu, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+  };
+  csr(keys, keys2, above_off, above);  // keys2 <- (b', b): the transposed pairs
+  if (nu) {  // contributors_below: the transposed pairs sorted
+    FMM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys2, keys, static_cast<int>(nu), 0, 64, s));
+    FMM_CUDA(cub::DeviceRadixSort::SortKeys(scratch(c, tb), tb, keys2, keys, static_cast<int>(nu), 0, 64, s));
+  }
+  csr(keys, nullptr, below_off, below);
+  if (task_out) FMM_CUDA(cudaMemcpyAsync(task_out, task, 8ull * nb, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  if (n_above) *n_above = nu;
+  if (n_below) *n_below = nu;
+  dfree(c, task, s);
+  dfree(c, keys, s);
+  dfree(c, keys2, s);
+  dfree(c, nkeys, s);
+  dfree(c, lo, s);
+  dfree(c, cnt, s);
+  dfree(c, offs, s);
 }
 
 }  // namespace fmmgpu

@@ -79,6 +79,10 @@ def compare_lists(c, ref, h):
     roff, rcells, _, rtot = ref.near()
     out = {"near": bool(np.array_equal(goff, roff) and np.array_equal(gcells, rcells) and gtot == rtot),
            "near_entries": int(len(rcells)), "near_directional": int(rtot)}
+    # NearFieldPlan block arrays (partners_above, contributors_below, task_interactions)
+    gb, rb = c.near_blocks(), ref.near_blocks()
+    out["near_blocks"] = bool(all(np.array_equal(x, y) for x, y in zip(gb, rb)))
+    out["near"] = out["near"] and out["near_blocks"]
     bad, pairs = [], 0
     for v in range(2, h):
         g = c.far(v)

@@ -305,7 +305,13 @@ class RefContext:
         bo = np.zeros(nb + 1, dtype=np.uint32)
         b = np.zeros(max(below_total.value, 1), dtype=np.uint32)
         self.L.ref_near_blocks(self.h, _p(ti), _p(ao), _p(a), _p(bo), _p(b))
+        self._blocks = (ti, ao, a[:na], bo, b[:below_total.value])
         return off, cells, ti, int(self.L.ref_near_total_directional(self.h))
+
+    def near_blocks(self):
+        """NearFieldPlan block arrays: (task_interactions, above_off, above, below_off, below)."""
+        self.near()
+        return self._blocks
 
     def far(self, v):
         npairs = self.L.ref_far_pairs(self.h, v)

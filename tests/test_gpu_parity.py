@@ -74,11 +74,30 @@ def test_tree_and_lists_bit_exact(fmm, case):
         assert np.array_equal(gb, ob), f"level {v} blocks"
     c.build_lists()
     goff, gcells, gtot = c.near()
-    ooff, ocells, _, otot = ot.near()
+    ooff, ocells, oti, otot = ot.near()
     assert np.array_equal(goff, ooff) and np.array_equal(gcells, ocells) and gtot == otot
+    assert np.array_equal(c.near_blocks()[0], oti)  # task_interactions per block
     for v in range(2, h):
         for a, b in zip(c.far(v), ot.far(v)):
             assert np.array_equal(a, b), f"far level {v}"
+
+
+@pytest.mark.parametrize("case,group", [((20000, 5, 5, "uniform", 3, True), 250), ((20000, 4, 4, "sphere", 9, True), 7),
+                                        ((40000, 6, 5, "ellipsoid", 4, False), 1)],
+                         ids=["uniform_g250", "sphere_g7", "ellipsoid_g1"])
+def test_near_block_plan_matches_reference(fmm, case, group):
+    """NearFieldPlan's block arrays (direct.cpp:36-58: partners_above, contributors_below,
+    task_interactions) bit-exact with the reference's plan, for several group sizes."""
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    n, h, l, dist, seed, rw = case
+    xyzw = make_particles(n, dist, seed, rw)
+    ref = RefContext(xyzw, h, l, group_size=group)
+    c = ctx_for(fmm, xyzw, h, l, group=group)
+    c.build_lists()
+    for a, b in zip(c.near_blocks(), ref.near_blocks()):
+        assert np.array_equal(a, b)
+    c.close()
 
 
 def test_tree_matches_reference_itself(fmm):

@@ -162,6 +162,10 @@ int fmmgpu_download_near(fmmgpu_ctx* ctx, uint32_t* near_offsets, uint32_t* near
 int fmmgpu_download_near_blocks(fmmgpu_ctx* ctx, uint64_t* task_interactions, uint32_t* above_off,
                                 uint32_t* above, uint32_t* below_off, uint32_t* below, uint64_t* n_above,
                                 uint64_t* n_below);
+/* LevelM2L::source_blocks (taskflow.cpp:96-102): per block of `level` the blocks of its
+ * far sources, ascending, as CSR (offsets: blocks + 1); NULL arrays = query *count. */
+int fmmgpu_download_far_source_blocks(fmmgpu_ctx* ctx, int level, uint32_t* offsets, uint32_t* blocks,
+                                      uint64_t* count);
 uint64_t fmmgpu_far_pairs(const fmmgpu_ctx* ctx, int level);
 /* M2LPairRef (m2l.hpp:66-70) as three arrays, and group_offsets (blocks*16+1). */
 int fmmgpu_download_far(fmmgpu_ctx* ctx, int level, uint32_t* target, uint32_t* source,

@@ -106,6 +106,7 @@ def lib():
         L.fmmgpu_comm_unique_id.argtypes = [ctypes.c_char_p]
         L.fmmgpu_exchange_plan.argtypes = [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
         L.fmmgpu_download_near_blocks.argtypes = [c_void_p] + [c_void_p] * 7
+        L.fmmgpu_download_far_source_blocks.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p]
         L.fmmgpu_set_measurement.argtypes = [c_void_p, c_int]
         L.fmmgpu_root_from_bounds.argtypes = [c_void_p, c_void_p]
         L.fmmgpu_dist_local.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_void_p]
@@ -301,6 +302,17 @@ class FmmContext:
         self._check(self._lib.fmmgpu_download_near_blocks(self.h, _p(ti), _p(ao), _p(a), _p(bo), _p(b), byref(na),
                                                           byref(nb_)))
         return ti, ao, a[:na.value], bo, b[:nb_.value]
+
+    def far_source_blocks(self, v: int):
+        """LevelM2L::source_blocks of level v as (offsets, blocks)."""
+        n = c_uint64()
+        self._check(self._lib.fmmgpu_download_far_source_blocks(self.h, v, None, None, byref(n)))
+        nc = self._lib.fmmgpu_level_cells(self.h, v)
+        nblk = (nc + self.group_size - 1) // self.group_size
+        off = np.zeros(nblk + 1, dtype=np.uint32)
+        blk = np.zeros(max(n.value, 1), dtype=np.uint32)
+        self._check(self._lib.fmmgpu_download_far_source_blocks(self.h, v, _p(off), _p(blk), byref(n)))
+        return off, blk[:n.value]
 
     def far(self, v: int):
         npairs = self._lib.fmmgpu_far_pairs(self.h, v)

@@ -322,6 +322,7 @@ void lists_build(fmmgpu_ctx* c);
 void lists_free(fmmgpu_ctx* c);
 void near_blocks(fmmgpu_ctx* c, uint64_t* task, uint32_t* above_off, uint32_t* above, uint32_t* below_off,
                  uint32_t* below, uint64_t* n_above, uint64_t* n_below);
+void far_source_blocks(fmmgpu_ctx* c, int v, uint32_t* off, uint32_t* list, uint64_t* n);
 void launch_p2m(fmmgpu_ctx* c, cudaStream_t s);
 void launch_m2m(fmmgpu_ctx* c, int parent_level, cudaStream_t s);
 void launch_l2l(fmmgpu_ctx* c, int parent_level, cudaStream_t s);

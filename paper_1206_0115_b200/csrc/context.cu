@@ -1100,6 +1100,14 @@ int fmmgpu_download_near_blocks(fmmgpu_ctx* c, uint64_t* task_interactions, uint
   });
 }
 
+int fmmgpu_download_far_source_blocks(fmmgpu_ctx* c, int level, uint32_t* offsets, uint32_t* blocks,
+                                      uint64_t* count) {
+  return guarded(c, [&] {
+    FMM_CUDA(cudaSetDevice(c->device));
+    far_source_blocks(c, level, offsets, blocks, count);
+  });
+}
+
 uint64_t fmmgpu_far_pairs(const fmmgpu_ctx* c, int v) {
   if (!c || !c->have_lists || v < 2 || v >= c->height) return 0;
   return c->lv[v].far_pairs;

@@ -242,6 +242,13 @@ __global__ void k_split_keys(const unsigned long long* __restrict__ keys, uint32
   (void)hi_first;
 }
 
+// far pairs of level v -> (target block << 32 | source block) keys
+__global__ void k_far_block_keys(const uint32_t* __restrict__ tgt, const uint32_t* __restrict__ src, uint64_t n,
+                                 uint32_t group, unsigned long long* __restrict__ keys) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) keys[i] = (static_cast<unsigned long long>(tgt[i] / group) << 32) | (src[i] / group);
+}
+
 __global__ void k_group_off(const unsigned long long* __restrict__ pos, uint64_t ngroups, uint32_t group,
                             uint64_t total, uint64_t* __restrict__ goff) {
   const uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -422,6 +429,54 @@ void near_blocks(fmmgpu_ctx* c, uint64_t* task_out, uint32_t* above_off, uint32_
   dfree(c, keys, s);
   dfree(c, keys2, s);
   dfree(c, nkeys, s);
+  dfree(c, lo, s);
+  dfree(c, cnt, s);
+  dfree(c, offs, s);
+}
+
+
+// LevelM2L::source_blocks (taskflow.cpp:96-102): per target block of level v, its far
+// sources' blocks, ascending and unique, as CSR (host arrays, NULL = skip).
+void far_source_blocks(fmmgpu_ctx* c, int v, uint32_t* off_out, uint32_t* list_out, uint64_t* n_out) {
+  if (!c->have_lists) throw Error(FMMGPU_LOGIC_ERROR, "no lists: call fmmgpu_build_lists first");
+  if (v < 2 || v >= c->height) throw Error(FMMGPU_OUT_OF_RANGE, "far_source_blocks: level out of range");
+  cudaStream_t s = c->s_far;
+  const Level& L = c->lv[v];
+  const uint32_t nb = static_cast<uint32_t>(L.block_offsets.size() - 1);
+  const uint64_t np = L.far_pairs;
+  unsigned long long* keys = dalloc<unsigned long long>(c, np + 1, s);
+  unsigned long long* keys2 = dalloc<unsigned long long>(c, np + 1, s);
+  uint32_t* nu_d = dalloc<uint32_t>(c, 1, s);
+  uint32_t nu = 0;
+  size_t tb = 0;
+  if (np) {
+    k_far_block_keys<<<static_cast<unsigned>((np + 255) / 256), 256, 0, s>>>(L.far_target, L.far_source, np,
+                                                                             static_cast<uint32_t>(c->group), keys);
+    FMM_CUDA(cudaGetLastError());
+    FMM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, static_cast<int>(np), 0, 64, s));
+    FMM_CUDA(cub::DeviceRadixSort::SortKeys(scratch(c, tb), tb, keys, keys2, static_cast<int>(np), 0, 64, s));
+    FMM_CUDA(cub::DeviceSelect::Unique(nullptr, tb, keys2, keys, nu_d, static_cast<int>(np), s));
+    FMM_CUDA(cub::DeviceSelect::Unique(scratch(c, tb), tb, keys2, keys, nu_d, static_cast<int>(np), s));
+    FMM_CUDA(cudaMemcpyAsync(&nu, nu_d, 4, cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+  }
+  uint32_t* lo = dalloc<uint32_t>(c, nu + 1, s);
+  uint32_t* cnt = dalloc<uint32_t>(c, nb + 1, s);
+  uint32_t* offs = dalloc<uint32_t>(c, nb + 1, s);
+  FMM_CUDA(cudaMemsetAsync(cnt, 0, 4ull * (nb + 1), s));
+  if (nu) {
+    k_split_keys<<<blocks(nu, 256), 256, 0, s>>>(keys, nu, 1, lo, nullptr, cnt);
+    FMM_CUDA(cudaGetLastError());
+  }
+  FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs, static_cast<int>(nb + 1), s));
+  FMM_CUDA(cub::DeviceScan::ExclusiveSum(scratch(c, tb), tb, cnt, offs, static_cast<int>(nb + 1), s));
+  if (off_out) FMM_CUDA(cudaMemcpyAsync(off_out, offs, 4ull * (nb + 1), cudaMemcpyDeviceToHost, s));
+  if (list_out && nu) FMM_CUDA(cudaMemcpyAsync(list_out, lo, 4ull * nu, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  if (n_out) *n_out = nu;
+  dfree(c, keys, s);
+  dfree(c, keys2, s);
+  dfree(c, nu_d, s);
   dfree(c, lo, s);
   dfree(c, cnt, s);
   dfree(c, offs, s);

@@ -91,6 +91,9 @@ def compare_lists(c, ref, h):
         if not all(np.array_equal(a, b) for a, b in zip(g, r)):
             bad.append(v)
         del g, r
+        # LevelM2L::source_blocks (taskflow.cpp:96-102)
+        if not all(np.array_equal(a, b) for a, b in zip(c.far_source_blocks(v), ref.far_source_blocks(v))):
+            bad.append(v)
     out["far_levels_bad"] = bad
     out["m2l_pairs"] = pairs
     out["bit_exact"] = out["near"] and not bad

@@ -313,6 +313,15 @@ class RefContext:
         self.near()
         return self._blocks
 
+    def far_source_blocks(self, v):
+        """LevelM2L::source_blocks of level v as (offsets, blocks)."""
+        total = self.L.ref_far_source_blocks_total(self.h, v)
+        nb = self.L.ref_level_blocks(self.h, v)
+        off = np.zeros(nb + 1, dtype=np.uint32)
+        blk = np.zeros(max(total, 1), dtype=np.uint32)
+        self.L.ref_far_source_blocks(self.h, v, _p(off), _p(blk))
+        return off, blk[:total]
+
     def far(self, v):
         npairs = self.L.ref_far_pairs(self.h, v)
         nb = self.L.ref_level_blocks(self.h, v)

@@ -87,7 +87,8 @@ def test_tree_and_lists_bit_exact(fmm, case):
                          ids=["uniform_g250", "sphere_g7", "ellipsoid_g1"])
 def test_near_block_plan_matches_reference(fmm, case, group):
     """NearFieldPlan's block arrays (direct.cpp:36-58: partners_above, contributors_below,
-    task_interactions) bit-exact with the reference's plan, for several group sizes."""
+    task_interactions) and every level's LevelM2L::source_blocks (taskflow.cpp:96-102)
+    bit-exact with the reference's plan, for several group sizes."""
     if not RefLib.available():
         pytest.skip("oracle/_ref not built")
     n, h, l, dist, seed, rw = case
@@ -97,6 +98,9 @@ def test_near_block_plan_matches_reference(fmm, case, group):
     c.build_lists()
     for a, b in zip(c.near_blocks(), ref.near_blocks()):
         assert np.array_equal(a, b)
+    for v in range(2, h):  # LevelM2L::source_blocks (taskflow.cpp:96-102)
+        for a, b in zip(c.far_source_blocks(v), ref.far_source_blocks(v)):
+            assert np.array_equal(a, b), v
     c.close()
 
 

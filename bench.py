@@ -8,9 +8,11 @@ octree of config B: 10M uniform particles (bench.cpp:29-39, seed 42), height 7,
 Chebyshev order 5, eps 1e-5, group size 250 -- BASELINE.json configs[1].
 
 ours:       value = Mparticles/s from CUDA events on the launching stream (max over
-            ranks), inputs resident in HBM; e2e = the same metric through the C ABI
-            (fmmgpu_run) with pinned host buffers: H2D of the particles, tree build,
-            evaluation, D2H of the four fields, every step.
+            ranks), inputs resident in HBM; e2e = the same metric through the C ABI with
+            pinned host buffers: H2D of the particles, tree build, evaluation, D2H of the
+            four fields, every step (N = 1: fmmgpu_run_async pipelined, the serial
+            fmmgpu_run beside it; N > 1: each rank's slice through
+            fmmgpu_build_tree_distributed + evaluate + download).
 reference:  the reference's own CPU implementation (oracle/_ref: the unmodified
             reference sources, FmmContext + execute with all host threads) on a
             bounded sample of the workload, rank 0 only.
@@ -70,7 +72,10 @@ def config_dict(name, world=1):
     """The workload description shared by both arms' JSON lines."""
     n, dist, h, order, desc = CONFIGS[name]
     return {"workload": desc, "n": n, "height": h, "order": order, "eps": 10.0 ** -order, "group_size": 250,
-            "parallelism": f"morton-range partition x{world}; NCCL exchange per upward level: all-gather at the alignment level, per-peer halo send/recv below"
+            "parallelism": f"morton-range partition x{world}; distributed input (each rank holds 1/{world} of the "
+                           "particles: keys all-gathered, owned + halo particle records exchanged over NCCL); "
+                           "multipole exchange per upward level: all-gather at the alignment level, per-peer halo "
+                           "send/recv below"
                            if world > 1 else "single",
             "l2": "inputs (32 B/particle + 1 KB per leaf expansion array) exceed the 126 MB L2"}
 

@@ -14,8 +14,9 @@ ours:       value = Mparticles/s from CUDA events on the launching stream (max o
             fmmgpu_run beside it; N > 1: each rank's slice through
             fmmgpu_build_tree_distributed + evaluate + download).
 reference:  the reference's own CPU implementation (oracle/_ref: the unmodified
-            reference sources, FmmContext + execute with all host threads) on a
-            bounded sample of the workload, rank 0 only.
+            reference sources, FmmContext + execute with all host threads) on the same
+            configuration (--cpu-sample: the labelled 1/8 sample), rank 0 only; setup,
+            exec and the 1-worker time reported separately.
 """
 import argparse
 import json

@@ -530,12 +530,14 @@ void enqueue_evaluation(fmmgpu_ctx* c) {
   }
   record(c, e[3], s);
   // Measured (tools/gpu/gpu_r02af.sh, ms per evaluation single stream / aux stream): A 0.97 /
-  // 0.99, B 24.54 / 24.62, C 80.18 / 79.61, E 240.54 / 240.73 -- used above order 5 only.
+  // 0.99, B 24.54 / 24.62, C 80.18 / 79.61, E 240.54 / 240.73; a config-B rank of 8
+  // (partitioned, tools/gpu/gpu_r02ak.sh) 4.28 / 3.94 -- used above order 5 and for
+  // partitioned evaluations, whose small per-rank levels are latency-bound.
   static const int aux_env = [] {  // FMMGPU_AUX=0/1 forces it (A/B aid)
     const char* v = std::getenv("FMMGPU_AUX");
     return v ? std::atoi(v) : -1;
   }();
-  const bool aux = aux_env >= 0 ? aux_env != 0 : c->ldE > 128;
+  const bool aux = aux_env >= 0 ? aux_env != 0 : (c->ldE > 128 || c->part_n > 1);
   if (aux && leaf > 2) {
     // M2L of every level reads only that level's multipoles, complete after the upward
     // pass, so the coarse levels' M2L and the L2L chain (which needs local(v) = own + down

@@ -104,9 +104,8 @@ struct FarArgs {
   uint32_t group;
 };
 
-template <bool FILL>
-__global__ void k_far(FarArgs a, uint32_t* __restrict__ cnt, const unsigned long long* __restrict__ pos,
-                      uint32_t* __restrict__ tgt, uint32_t* __restrict__ src, uint16_t* __restrict__ vec) {
+// counts per (block, class, cell) of the far pairs (the fill is k_far_fill_warp)
+__global__ void k_far_count(FarArgs a, uint32_t* __restrict__ cnt) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= a.L.n) return;
   const uint64_t code = a.L.code[c];
@@ -127,25 +126,17 @@ __global__ void k_far(FarArgs a, uint32_t* __restrict__ cnt, const unsigned long
       const int d = max(abs(ti), max(abs(tj), abs(tk)));
       if (d <= 1) continue;
       const int slot = (ti + 3) * 49 + (tj + 3) * 7 + (tk + 3);
-      const int q = a.canon[slot];
-      if (FILL) {
-        const unsigned long long p = pos[(size_t(b) * 16 + q) * a.group + cl] + k16[q];
-        tgt[p] = c;
-        src[p] = ch;
-        vec[p] = static_cast<uint16_t>(slot);
-      }
-      ++k16[q];
+      ++k16[a.canon[slot]];
     }
   }
-  if (!FILL)
-    for (int q = 0; q < 16; ++q) cnt[(size_t(b) * 16 + q) * a.group + cl] = k16[q];
+  for (int q = 0; q < 16; ++q) cnt[(size_t(b) * 16 + q) * a.group + cl] = k16[q];
 }
 
 // The fill as one warp per target cell: the candidate sources (children of the sorted
 // parent neighbours, ascending) are spread over the lanes in order; each 32-candidate step
 // groups the lanes by canonical class (__match_any_sync), so a class's entries of the step
 // are written to consecutive slots (a few segments per store instead of 32 scattered
-// ones). Same positions as k_far<true>: within a (block, class) group the cells in order,
+// ones). Positions: within a (block, class) group the cells in order,
 // within a cell the sources ascending.
 __global__ void __launch_bounds__(256) k_far_fill_warp(FarArgs a, const unsigned long long* __restrict__ pos,
                                                        uint32_t* __restrict__ tgt, uint32_t* __restrict__ src,
@@ -230,7 +221,8 @@ __global__ void k_near_blocks(LevelView L, const uint32_t* __restrict__ count, c
   }
   atomicAdd(&task[b], owned);
 }
-__global__ void k_split_keys(const unsigned long long* __restrict__ keys, uint32_t n, int hi_first,
+// sorted (hi << 32 | lo) keys -> lo list, counts per hi, optionally the swapped keys
+__global__ void k_split_keys(const unsigned long long* __restrict__ keys, uint32_t n,
                              uint32_t* __restrict__ lo_out, unsigned long long* __restrict__ swapped,
                              uint32_t* __restrict__ cnt) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -239,7 +231,6 @@ __global__ void k_split_keys(const unsigned long long* __restrict__ keys, uint32
   lo_out[i] = lo;
   atomicAdd(&cnt[hi], 1u);
   if (swapped) swapped[i] = (static_cast<unsigned long long>(lo) << 32) | hi;
-  (void)hi_first;
 }
 
 // far pairs of level v -> (target block << 32 | source block) keys
@@ -340,7 +331,7 @@ void lists_build(fmmgpu_ctx* c) {
     FMM_CUDA(cudaMemsetAsync(cnt, 0, 4 * slots, s));
     FarArgs a{L.view(v), P.view(v - 1), L.parent, P.first_child, P.child_count, c->d_canon,
               static_cast<uint32_t>(c->group)};
-    k_far<false><<<blocks(L.n, 128), 128, 0, s>>>(a, cnt, nullptr, nullptr, nullptr, nullptr);
+    k_far_count<<<blocks(L.n, 128), 128, 0, s>>>(a, cnt);
     FMM_CUDA(cudaGetLastError());
     size_t tb = 0;
     FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, pos, static_cast<int>(slots), s));
@@ -406,7 +397,7 @@ void near_blocks(fmmgpu_ctx* c, uint64_t* task_out, uint32_t* above_off, uint32_
   auto csr = [&](const unsigned long long* k, unsigned long long* swapped, uint32_t* off_out, uint32_t* list_out) {
     FMM_CUDA(cudaMemsetAsync(cnt, 0, 4ull * (nb + 1), s));
     if (nu) {
-      k_split_keys<<<blocks(nu, 256), 256, 0, s>>>(k, nu, 1, lo, swapped, cnt);
+      k_split_keys<<<blocks(nu, 256), 256, 0, s>>>(k, nu, lo, swapped, cnt);
       FMM_CUDA(cudaGetLastError());
     }
     FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs, static_cast<int>(nb + 1), s));
@@ -465,7 +456,7 @@ void far_source_blocks(fmmgpu_ctx* c, int v, uint32_t* off_out, uint32_t* list_o
   uint32_t* offs = dalloc<uint32_t>(c, nb + 1, s);
   FMM_CUDA(cudaMemsetAsync(cnt, 0, 4ull * (nb + 1), s));
   if (nu) {
-    k_split_keys<<<blocks(nu, 256), 256, 0, s>>>(keys, nu, 1, lo, nullptr, cnt);
+    k_split_keys<<<blocks(nu, 256), 256, 0, s>>>(keys, nu, lo, nullptr, cnt);
     FMM_CUDA(cudaGetLastError());
   }
   FMM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs, static_cast<int>(nb + 1), s));

@@ -233,8 +233,6 @@ struct GemmArgs {
   int vtMax2;
   int ksplit;             // phase B split-K factor (1 = accumulate directly)
   int rowB0;              // phase B: first row of this launch's M-tiles (tail launches)
-  int skip_dead;          // phase A: skip M-tiles without an existing owned target
-  uint32_t own0, own1;    // owned target cells of the level
   int msplit;             // phase A M-split factor (coarse levels)
   int cls_fast;           // phase A grid: parity class in blockIdx.x (else blockIdx.y)
   int ow;                 // phase B: write local_own instead of accumulating (evaluation)
@@ -428,47 +426,17 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) k_m2l_phase_a(const GemmAr
   const int per = (MTILES + g.msplit - 1) / g.msplit;
   const int mt0 = blockIdx.z * per, mt1 = min(MTILES, mt0 + per);
   if (mt0 >= mt1) return;
-  // Dead M-tiles (g.skip_dead: sparse levels and partitioned runs): an M-tile none of whose
-  // vectors takes any of the CTA's columns to an existing (owned) target produces no Yt
-  // row anyone reads, so its slices are neither loaded nor multiplied. The CTA streams the
-  // list of live tiles instead of [mt0, mt1).
-  __shared__ uint8_t live_tiles[64];
-  __shared__ int n_live;
-  if (g.skip_dead) {
-    if (tid == 0) n_live = 0;
-    __syncthreads();
-    for (int m = mt0; m < mt1; ++m) {
-      const int* vec = g.tileVec + (size_t(cls) * MTILES + m) * g.vtMax;
-      int live = 0;
-      for (int e = tid; e < g.vtMax * BN && !live; e += PA_THREADS) {
-        const int j = e % BN, slot = __ldg(vec + e / BN);
-        if (slot >= 0 && col_cell[j] != NPOS) {
-          const uint32_t tc = find_ijk(g.lv, col_ijk[j][0] - (slot / 49 - 3), col_ijk[j][1] - ((slot / 7) % 7 - 3),
-                                       col_ijk[j][2] - (slot % 7 - 3));
-          live = tc != NPOS && tc >= g.own0 && tc < g.own1;
-        }
-      }
-      if (__syncthreads_or(live) && tid == 0) live_tiles[n_live++] = static_cast<uint8_t>(m);
-    }
-    __syncthreads();
-  }
-  const int ntiles = g.skip_dead ? n_live : mt1 - mt0;
-  auto tile_at = [&](int i) { return g.skip_dead ? static_cast<int>(live_tiles[i]) : mt0 + i; };
-  if (ntiles == 0) {
-    cp_wait<0>();
-    return;
-  }
-  const int TOTAL = ntiles * KT;
+  const int TOTAL = (mt1 - mt0) * KT;
   // ring producer position (tile, k-slice), advanced without divisions
-  int pti = 0, pkt = 0, pstage = 0;
+  int pmt = mt0, pkt = 0, pstage = 0;
   auto load_next = [&]() {
     double* as = As + pstage * PA_BM * PA_SPAD;
-    const double* src = A + size_t(tile_at(pti) * PA_BM) * g.lda + pkt * PA_BK;
+    const double* src = A + size_t(pmt * PA_BM) * g.lda + pkt * PA_BK;
     for (int ch = tid; ch < PA_BM * (PA_BK / 2); ch += PA_THREADS) {
       const int r = ch / (PA_BK / 2), q = (ch % (PA_BK / 2)) * 2;
       cp16(as + r * PA_SPAD + q, src + size_t(r) * g.lda + q);
     }
-    if (++pkt == KT) { pkt = 0; ++pti; }
+    if (++pkt == KT) { pkt = 0; ++pmt; }
     if (++pstage == PA_ST) pstage = 0;
   };
 #pragma unroll
@@ -489,7 +457,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) k_m2l_phase_a(const GemmAr
   const int kt_fill = KT / 2;
   int4 rowinfo[MT];  // consumed only by the tile's epilogue, KT k-slices after the load
   int slot_e0 = -1, slot_e1 = -1;
-  int cti = 0, mt = tile_at(0), kt = 0, stage = 0;
+  int mt = mt0, kt = 0, stage = 0;
   for (int t = 0; t < TOTAL; ++t) {
     cp_wait<PA_ST - 2>();
     __syncthreads();
@@ -551,10 +519,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) k_m2l_phase_a(const GemmAr
       }
     }
     if (++stage == PA_ST) stage = 0;
-    if (++kt == KT) {
-      kt = 0;
-      if (++cti < ntiles) mt = tile_at(cti);
-    }
+    if (++kt == KT) { kt = 0; ++mt; }
   }
   cp_wait<0>();
 }
@@ -863,12 +828,6 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
   g.lv = L.view(v);
   // phase A runs over the sources (partitioned: those with an owned target), phase B
   // over the targets (partitioned: the owned ones)
-  // dead-tile skipping where whole M-tiles can lack targets: sparse levels (surface
-  // clouds) and partitioned runs (halo sources reach only a few owned targets); on full
-  // unpartitioned levels every tile of a 64-column block is live (0 of 189 vectors dead)
-  g.skip_dead = (!L.full || c->part_n > 1) && T.rowsA / 64 <= 64 ? 1 : 0;
-  g.own0 = L.own0;
-  g.own1 = L.own1;
   g.cls_cells = L.srcA ? L.srcA : L.cls_cells;
   std::copy(L.srcA ? L.srcA_off : L.cls_off, (L.srcA ? L.srcA_off : L.cls_off) + 9, g.cls_off);
   g.W = L.multipole;

@@ -429,6 +429,9 @@ def run_ours(args, world, rank, local):
             "share_of_step": iso["P2P"] / ms_step,
             "peak_source": "FP64 DFMA measured by tools/microbench/fp64_peaks.cu (profiles/r01_fp64_peaks.txt); "
                            "MEASURED_PEAKS.json has no FP64 figure",
+            "traffic_note": "ncu DRAM bytes of the mutual kernel + its drain per evaluation: 0.64 GB of particles and "
+                            "near fields plus the [13][n] P2PBuffers-style slot array (4.16 GB written, read back by "
+                            "the ordered drain); the kernel stays FP64-bound (DRAM ~6% busy during it)",
             "flop_convention": "reference ledger (bench.hpp:49-53): 15 flop per directional interaction; the "
                                f"kernel issues {dp_per_dir} FP64 instructions per directional interaction and the "
                                f"peak counts 2 flop per DFMA, so frac <= 15/{2 * dp_per_dir} = "

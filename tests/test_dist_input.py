@@ -212,3 +212,34 @@ def test_two_processes_distributed_input_over_gloo(case):
         assert relative_l2_error(g[0], ref[0]) <= 1e-12
         assert force_error(*g[1:], *ref[1:]) <= 1e-12
         assert 0 < res[r][1] < n  # halo records only
+
+
+def test_nccl_distributed_build_single_rank():
+    """The in-library NCCL path of the distributed build (fmmgpu_build_tree_distributed:
+    bounds / keys / flags all-gathers as broadcast groups, per-peer record exchange,
+    coincident check) on a one-rank communicator -- the only NCCL run one GPU allows --
+    gives the single-device tree and fields bit for bit."""
+    import paper_1206_0115_b200 as P
+    xyzw = _cloud(30000, "uniform", 12)
+    full = P.FmmContext(None, order=4)
+    full.build_tree(xyzw, 5)
+    full.evaluate()
+    ref = full.gather()
+    c = P.FmmContext(None, order=4)
+    c.comm_init(P.comm_unique_id(), 1, 0)
+    c.build_tree_distributed(xyzw, 5)
+    for v in range(5):
+        a, ba = c.level(v)
+        b, bb = full.level(v)
+        assert np.array_equal(a, b) and np.array_equal(ba, bb)
+    c.evaluate()
+    got = c.gather()
+    for x, y in zip(got, ref):
+        assert np.array_equal(x, y)
+    # coincident particles are refused on every rank through the same path
+    dup = xyzw.copy()
+    dup[17, :3] = dup[4, :3]
+    with pytest.raises(P.DomainError):
+        c.build_tree_distributed(dup, 5)
+    for x in (c, full):
+        x.close()

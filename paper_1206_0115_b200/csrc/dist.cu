@@ -128,7 +128,6 @@ void particle_plan(fmmgpu_ctx* c) {
   ++c->launches;
   // per peer p: send = {slots with id in my slice, leaf needed by p} (p == me: the local
   // copy), recv = {slots with id in p's slice, leaf needed by me} (p != me)
-  std::vector<std::vector<uint32_t>> parts;
   uint32_t* tmp_out = dev_alloc<uint32_t>(c->n);
   uint32_t* d_cnt = dev_alloc<uint32_t>(1);
   size_t tb = 0;
@@ -485,7 +484,6 @@ int fmmgpu_build_tree_distributed(fmmgpu_ctx* c, const double* xyzw_local, uint6
     cudaFree(keys);
     if (rc != FMMGPU_OK) throw Error(rc, c->err);
     // particle records of the owned + halo leaves, per peer
-    const uint64_t ns = c->dsend_off.back() - (c->dsend_off[me + 1] - c->dsend_off[me]);
     const uint64_t nv = c->drecv_off.back();
     double4* sbuf = dev_alloc<double4>(c->dsend_off.back());
     double4* rbuf = dev_alloc<double4>(nv);
@@ -515,7 +513,6 @@ int fmmgpu_build_tree_distributed(fmmgpu_ctx* c, const double* xyzw_local, uint6
     FMM_CUDA(cudaStreamSynchronize(s));
     cudaFree(sbuf);
     cudaFree(rbuf);
-    (void)ns;
     // coincident particles anywhere -> every rank raises
     int cf = 0;
     rc = fmmgpu_dist_check(c, &cf);

@@ -595,6 +595,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   const int leaf = height - 1;
   const uint32_t grid = 1u << leaf;
   double* geo_mem = dalloc<double>(c, sizeof(TreeGeo) / sizeof(double), s);
+  FMM_CUDA(cudaMemsetAsync(geo_mem, 0, sizeof(TreeGeo), s));
   TreeGeo* geo = reinterpret_cast<TreeGeo*>(geo_mem);
   {
     const int nb = root4 ? 1 : static_cast<int>(std::min<uint64_t>(1184, blocks(n, 256)));
@@ -808,6 +809,7 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
   // expansions (cell-major, stride ldE, zero padding). The class offsets of every level
   // and the error flag come back in one readback at the end.
   uint32_t* d_offs = dalloc<uint32_t>(c, 9 * height + 1, s);
+  FMM_CUDA(cudaMemsetAsync(d_offs, 0, sizeof(uint32_t) * (9 * height + 1), s));  // levels 0, 1 stay 0
   for (int v = 0; v < height; ++v) {
     Level& V = c->lv[v];
     V.block_offsets.clear();

@@ -3,7 +3,7 @@
 # reference baselines, the reference arm, launch list + ncu of the top kernels at B,
 # scaling projection and distributed-input volumes
 cd "$GRAFT_REPO_ROOT"
-O=gpurun_out/final2; mkdir -p $O
+O=gpurun_out/final3; mkdir -p $O
 nproc > $O/host.txt; free -g >> $O/host.txt; nvidia-smi >> $O/host.txt
 timeout 1800 python -m pytest tests -m gpu -q -rs > $O/pytest_gpu.log 2>&1; echo "exit $?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
@@ -17,7 +17,7 @@ cap() {
   timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$2" -s "$3" -c 1 -o $O/$1 -f python tools/profile_eval.py 10000000 7 5 1 > $O/$1.out 2>&1
 }
 cap prof_p2p 'k_p2p_mutual' 0
-cap prof_drain 'k_p2p_drain' 0
+cap prof_l2p "k_l2p_block" 0
 cap prof_m2la 'k_m2l_phase_a' 4
 cap prof_m2lb 'k_m2l_phase_b' 4
 timeout 900 python tools/scaling_projection.py B > $O/scaling_projection_B.json 2> $O/scaling.err

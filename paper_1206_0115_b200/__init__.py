@@ -18,6 +18,7 @@ same meaning (ValueError = invalid_argument, DomainError = domain_error, ...).
 from __future__ import annotations
 
 import ctypes
+import importlib.util
 import os
 from ctypes import c_double, c_int, c_uint64, c_void_p, byref
 from dataclasses import dataclass
@@ -66,6 +67,16 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise FmmError(f"{LIB_PATH} missing: build it with `make -C {_HERE}` (no CPU fallback)")
+        if "FMMGPU_NCCL_LIB" not in os.environ:
+            # the library dlopens NCCL only when a communicator is used; point it at torch's
+            # bundled copy so both share one libnccl.so.2 (a system NCCL loaded first would
+            # shadow it and break a later `import torch`)
+            spec = importlib.util.find_spec("nvidia.nccl")
+            for d in (spec.submodule_search_locations or []) if spec else []:
+                cand = os.path.join(d, "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["FMMGPU_NCCL_LIB"] = cand
+                    break
         L = ctypes.CDLL(LIB_PATH)
         L.fmmgpu_last_error.restype = ctypes.c_char_p
         L.fmmgpu_last_error.argtypes = [c_void_p]

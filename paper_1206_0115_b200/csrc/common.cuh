@@ -33,6 +33,9 @@ struct Error : std::runtime_error {
                                                       __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
 
+// dlopen of NCCL shared by the partitioned evaluation and the distributed build (partition.cu)
+void* open_nccl();
+
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 // ---------------------------------------------------------------- Morton codes

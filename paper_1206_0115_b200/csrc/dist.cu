@@ -195,9 +195,7 @@ struct NcclDist {
 NcclDist& ncd() {
   static NcclDist api;
   if (!api.groupStart) {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) throw Error(FMMGPU_RUNTIME_ERROR, "NCCL not available (dlopen libnccl.so.2 failed)");
+    void* h = open_nccl();  // partition.cu
     api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
     api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
     api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(h, "ncclBroadcast"));

@@ -730,6 +730,11 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s, bool fuse_drain) {
       int b = 0;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, MU_WARPS * 32, smem) != cudaSuccess || b < 1) b = 1;
+      static const int cps = [] {
+        const char* e = std::getenv("FMMGPU_MU_CPS");
+        return e ? std::atoi(e) : 0;
+      }();
+      if (cps > 0 && cps < b) b = cps;
       // one CTA per SM: the kernel holds every SM for its ~10 ms and the far chain follows
       // (per-launch trace at config B: P2M starts at 10.45 ms); leaving 4-32 SMs to the far
       // chain measured 24.62-24.55 vs 24.65 ms per evaluation (the sum of the kernels is

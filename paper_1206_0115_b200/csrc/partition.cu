@@ -51,12 +51,28 @@ struct NcclApi {
   const char* (*errorString)(ncclResult_t) = nullptr;
 };
 
+}  // namespace
+
+// The NCCL the process already has (torch's, when torch.distributed is up) wins; else
+// FMMGPU_NCCL_LIB (the Python binding points it at torch's bundled libnccl, so a later
+// `import torch` finds the NCCL it was built against under the same soname); else the
+// system libnccl.so.2.
+void* open_nccl() {
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  const char* env = std::getenv("FMMGPU_NCCL_LIB");
+  if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) throw Error(FMMGPU_RUNTIME_ERROR, "NCCL not available (dlopen libnccl.so.2 failed)");
+  return h;
+}
+
+namespace {
+
 NcclApi& nccl() {
   static NcclApi api;
   if (!api.handle) {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) throw Error(FMMGPU_RUNTIME_ERROR, "NCCL not available (dlopen libnccl.so.2 failed)");
+    void* h = open_nccl();
     api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
     api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));

@@ -70,3 +70,21 @@ def test_root_from_bounds_matches_bounding_cube(dist, seed):
     assert np.array_equal(P.root_from_bounds(lohi), OracleTree(xyzw, 3).root_cube())
     with pytest.raises(P.InvalidArgument):
         P.root_from_bounds(np.array([1.0, 0, 0, 0, 1, 1]))  # min > max on x
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libfmmgpu.so not built")
+def test_nccl_load_keeps_torch_importable():
+    """The library's lazy NCCL load (fmmgpu_comm_unique_id) must not shadow torch's
+    bundled libnccl.so.2: a later `import torch` in the same process has to succeed (the
+    system NCCL 2.27 lacks symbols torch 2.11 links against)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, ctypes; sys.path.insert(0, %r); import paper_1206_0115_b200 as P\n"
+        "buf = ctypes.create_string_buffer(128); rc = P.lib().fmmgpu_comm_unique_id(buf)\n"
+        "import torch; print('rc', rc)\n" % ROOT
+    )
+    env = {k: v for k, v in os.environ.items() if k != "FMMGPU_NCCL_LIB"}
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]

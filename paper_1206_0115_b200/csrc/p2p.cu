@@ -730,15 +730,13 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s, bool fuse_drain) {
       int b = 0;
       FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, MU_WARPS * 32, smem) != cudaSuccess || b < 1) b = 1;
-      static const int cps = [] {
-        const char* e = std::getenv("FMMGPU_MU_CPS");
-        return e ? std::atoi(e) : 0;
-      }();
-      if (cps > 0 && cps < b) b = cps;
       // one CTA per SM: the kernel holds every SM for its ~10 ms and the far chain follows
       // (per-launch trace at config B: P2M starts at 10.45 ms); leaving 4-32 SMs to the far
       // chain measured 24.62-24.55 vs 24.65 ms per evaluation (the sum of the kernels is
-      // the evaluation either way)
+      // the evaluation either way). Sharing each SM instead (8- or 6-warp near-field CTAs,
+      // one per SM, every evaluation kernel at the maximum shared-memory carveout so the
+      // far chain's CTAs co-reside; tools/gpu/gpu_r02ar.sh): 26.85 / 27.70 ms, the M2L
+      // GEMMs and the pair loop compete for the one FP64 pipe
       const uint32_t grid = std::min<uint32_t>(static_cast<uint32_t>(sms * b), (nl + MU_WARPS - 1) / MU_WARPS);
       FMM_CUDA(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint32_t), s));
       kern<<<grid, MU_WARPS * 32, smem, s>>>(a);

@@ -472,7 +472,10 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) k_m2l_phase_a(const GemmAr
       slot_e1 = tid + PA_THREADS < g.vtMax * BN ? __ldg(vec + (tid + PA_THREADS) / BN) : -1;
     }
     if (kt == kt_fill) {
-      // one lookup per (vector, source column) of this M-tile: target = source - v
+      // one lookup per (vector, source column) of this M-tile: target = source - v.
+      // (Looking the first two entries up before this slice's DMMAs and storing them after,
+      // so the lookups' loads wait behind the DMMAs: 100 -> 118 registers, config-B M2L
+      // 12.33 -> 12.40 ms, same fields bit for bit; tools/gpu/gpu_r02at.sh. Not adopted.)
       const int* vec = g.tileVec + (size_t(cls) * MTILES + mt) * g.vtMax;
       int u = 0;
       for (int e = tid; e < g.vtMax * BN; e += PA_THREADS, ++u) {

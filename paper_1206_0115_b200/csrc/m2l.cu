@@ -888,6 +888,8 @@ void launch_m2l(fmmgpu_ctx* c, int v, cudaStream_t s) {
     // Also measured (tools/gpu/gpu_r02o.sh, evaluation ms at config B / C): 64 x 64 with 4
     // warps of 32 x 32 (24.84 vs 24.53), 64 x 32 with 4 warps and 3 CTAs per SM (24.62), the
     // same with a 3-stage ring (25.79); at l = 7, 128 x 32 with one CTA per SM (97.76 vs 88.76).
+    // Round 2: 128-row M-tiles with 8 warps of 32 x 32 and a 2-stage ring of 16-wide slices
+    // (two CTAs per SM, 128 registers; tools/gpu/gpu_r02au.sh): M2L 12.85 vs 12.33 ms at B.
     // l >= 6: the streamed kernel (config C 87.94 -> 80.21 ms per evaluation, l = 6
     // 49.06 -> 45.42; at l = 5 it measured slower, 25.30 vs 24.59 ms at B). Streamed
     // shapes also measured at C: 128 x 128 with 16 warps (84.42), 3-stage ring (88.50),

@@ -342,6 +342,8 @@ struct FullLevels {
   uint32_t* child_count[22];
   uint32_t* parent[22];
   uint32_t* cls_cells[22];
+  uint32_t* first_particle[22];  // parent levels: zero (the reference keeps them 0)
+  uint32_t* particle_count[22];
   uint64_t start[23];  // first flattened index of level v
   int leaf;
 };
@@ -355,6 +357,8 @@ __global__ void k_full_levels(const FullLevels f) {
     f.code[v][i] = i;
     f.first_child[v][i] = static_cast<uint32_t>(8 * i);
     f.child_count[v][i] = 8;
+    f.first_particle[v][i] = 0;
+    f.particle_count[v][i] = 0;
   }
   f.parent[v][i] = static_cast<uint32_t>(i >> 3);  // level 0: 0, as the general path
   if (v >= 2) f.cls_cells[v][(i & 7) * (n >> 3) + (i >> 3)] = static_cast<uint32_t>(i);
@@ -411,11 +415,16 @@ const void* readback(fmmgpu_ctx* c, const void* src, size_t bytes, cudaStream_t 
   k_copy_words<<<std::max(1u, std::min(64u, (nw + 255) / 256)), 256, 0, s>>>(static_cast<const uint32_t*>(src), nw, d);
   FMM_CUDA(cudaGetLastError());
   static const bool tr = std::getenv("FMMGPU_TRACE") != nullptr;
+  static std::chrono::steady_clock::time_point last{};
   const auto t0 = std::chrono::steady_clock::now();
   FMM_CUDA(cudaStreamSynchronize(s));
   if (tr) {
-    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    if (ms > 0.5) std::fprintf(stderr, "[readback] sync took %.3f ms\n", ms);
+    const auto t1 = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    const double host = std::chrono::duration<double, std::milli>(t0 - last).count();
+    std::fprintf(stderr, "[readback] %zu B: sync %.3f ms, host work since the previous readback %.3f ms\n", bytes, ms,
+                 host < 1e4 ? host : -1.0);
+    last = t1;
   }
   return c->h_rb;
 }
@@ -739,8 +748,6 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
         V.parent = dalloc<uint32_t>(c, nv, s);
         V.first_particle = dalloc<uint32_t>(c, nv, s);
         V.particle_count = dalloc<uint32_t>(c, nv, s);
-        FMM_CUDA(cudaMemsetAsync(V.first_particle, 0, 4 * nv, s));
-        FMM_CUDA(cudaMemsetAsync(V.particle_count, 0, 4 * nv, s));
       }
       if (v >= 2) {
         V.cls_cells = dalloc<uint32_t>(c, nv, s);
@@ -751,6 +758,8 @@ void tree_build(fmmgpu_ctx* c, const double* xyzw, uint64_t n, bool on_device, i
       f.child_count[v] = V.child_count;
       f.parent[v] = V.parent;
       f.cls_cells[v] = V.cls_cells;
+      f.first_particle[v] = v < leaf ? V.first_particle : nullptr;
+      f.particle_count[v] = v < leaf ? V.particle_count : nullptr;
     }
     k_full_levels<<<blocks(f.start[leaf + 1], 256), 256, 0, s>>>(f);
     FMM_CUDA(cudaGetLastError());

@@ -713,7 +713,8 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s, bool fuse_drain) {
              reinterpret_cast<double4*>(c->d_slot), c->n, L.own0, L.own1, c->d_ctr, p2p_order(c, L, s), c->ow ? 1 : 0};
     // 12-warp CTAs, one per SM at <= 168 registers (164 used): config B P2P 10.97 -> 10.89
     // ms, config D 163.4 -> 160.0 ms against 8-warp CTAs, 2 per SM at 128 registers. Also
-    // measured (tools/gpu/gpu_r02g.sh): 10 warps at 164 registers (11.36 / 165.2 ms), 8 warps
+    // measured (tools/gpu/gpu_r02g.sh, gpu_r02ax.sh): 11 warps at 164 registers (11.10 / 160.3 ms),
+    // 13 warps at 128 (11.79 / 173.0), 10 warps at 164 registers (11.36 / 165.2 ms), 8 warps
     // at up to 255 registers (11.97 / 171.7), 6 sources per lane with 8 or 12 warps (12.16 /
     // 162.2, 12.45 / 169.0), the pairs of a step written stage by stage (ptxas schedules
     // them the same way: no change). Loop ceiling of this sub-ring layout without memory

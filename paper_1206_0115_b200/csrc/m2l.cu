@@ -284,7 +284,9 @@ __global__ void __launch_bounds__(WM* WN * 32) k_m2l_phase_b(const GemmArgs g) {
       cp16(as + r * SPAD + q, A + size_t(r) * g.lda + k0 + q);
     }
     // Yt blocks of absent sources were never written by phase A and stay zero from
-    // the allocation (one Yt per level), so the operand is a plain copy.
+    // the allocation (one Yt per level), so the operand is a plain copy. (Resolving the
+    // thread's column row pointers once per CTA instead of per slice: 98 -> 128 registers,
+    // config-B M2L 12.28 -> 12.34 ms, C 56.94 -> 57.20 ms; tools/gpu/gpu_r02ba.sh.)
     for (int ch = tid; ch < BN * (BK / 2); ch += T) {
       const int j = ch / (BK / 2), q = (ch % (BK / 2)) * 2;
       const uint32_t cell = col_cell[j];
@@ -504,18 +506,24 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) k_m2l_phase_a(const GemmAr
         for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     if (kt == KT - 1) {
-      // scatter block v of source s to target s - v, target-side column info.x
+      // scatter block v of source s to target s - v, target-side column info.x. The
+      // targets of all the thread's elements are read first (one 8-byte LDS per column
+      // pair), so the stores do not wait on a shared load each: the compiler cannot move
+      // those loads above the global stores itself (generic pointers may alias)
+      uint2 tcv[MT][NT];
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        if (rowinfo[i].x >= 0) {
-          const uint32_t* trow = tg + rowinfo[i].z * BN;
+        const uint2* trow = reinterpret_cast<const uint2*>(tg + max(rowinfo[i].z, 0) * BN + wn * WTN + 2 * tq);
 #pragma unroll
-          for (int j = 0; j < NT; ++j)
+        for (int j = 0; j < NT; ++j) tcv[i][j] = rowinfo[i].x >= 0 ? trow[j * 4] : make_uint2(NPOS, NPOS);
+      }
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const uint32_t tcell = trow[wn * WTN + j * 8 + 2 * tq + e];
-              if (tcell != NPOS) g.Yt[size_t(tcell) * g.ldY + rowinfo[i].y] = acc[i][j][e];
-            }
+      for (int i = 0; i < MT; ++i) {
+        double* yrow = g.Yt + rowinfo[i].y;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          if (tcv[i][j].x != NPOS) yrow[size_t(tcv[i][j].x) * g.ldY] = acc[i][j][0];
+          if (tcv[i][j].y != NPOS) yrow[size_t(tcv[i][j].y) * g.ldY] = acc[i][j][1];
         }
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;

@@ -714,7 +714,9 @@ void launch_p2p(fmmgpu_ctx* c, cudaStream_t s, bool fuse_drain) {
     // 12-warp CTAs, one per SM at <= 168 registers (164 used): config B P2P 10.97 -> 10.89
     // ms, config D 163.4 -> 160.0 ms against 8-warp CTAs, 2 per SM at 128 registers. Also
     // measured (tools/gpu/gpu_r02g.sh, gpu_r02ax.sh): 11 warps at 164 registers (11.10 / 160.3 ms),
-    // 13 warps at 128 (11.79 / 173.0), 10 warps at 164 registers (11.36 / 165.2 ms), 8 warps
+    // 13 warps at 128 (11.79 / 173.0), the next leaf claimed one leaf ahead (10.59 / 157.4 vs
+    // 10.52 / 155.9: a warp holding a claimed leaf delays it), 10 warps at 164 registers
+    // (11.36 / 165.2 ms), 8 warps
     // at up to 255 registers (11.97 / 171.7), 6 sources per lane with 8 or 12 warps (12.16 /
     // 162.2, 12.45 / 169.0), the pairs of a step written stage by stage (ptxas schedules
     // them the same way: no change). Loop ceiling of this sub-ring layout without memory

@@ -614,6 +614,8 @@ struct RunL2P {
     // higher orders: the n2 sums factored as well (config-C leaf 1.65 -> 1.22 ms; at
     // order 5 the factored loop needs 162-188 registers and measured 0.59-0.79 vs 0.56 ms)
     constexpr bool factored = L > 5;
+    // (5 / 6 CTAs per SM at 96 / 80 registers with small spills: B 24.25 / 24.41-24.58 vs
+    // 24.28-24.46 ms, E 234.2 / 235.4 vs 233.6 ms; tools/gpu/gpu_r02be.sh: kept at 4)
     auto kern = k_l2p_block<L, factored, factored ? 0 : 4>;
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<(nc + L2P_CELLS - 1) / L2P_CELLS, L2P_THREADS, smem, s>>>(a);

@@ -413,6 +413,9 @@ __device__ __forceinline__ void add4(double4& a, const double4 b) {
 // after RING steps lane l of every sub-ring holds its partial sums of target t0 + l, and
 // the 32 / RING sub-rings are combined by a fixed butterfly (commutative pairs: every
 // lane forms the bitwise same total).
+// (Loading the next step's target a step ahead, against the short-scoreboard waits ncu's
+// source view shows on the first subtraction: 166 registers, P2P 10.75 vs 10.50 ms at B,
+// D 159.0 vs 156.0 ms; tools/gpu/gpu_r02bf.sh. Not adopted.)
 template <int TS, int RING, bool SELF, class W>
 __device__ __forceinline__ void mu_tile(W& w, const int t0, const double4 (&ps)[TS], double4 (&as)[TS],
                                         const int lane, const double c375) {
